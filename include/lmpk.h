@@ -1,0 +1,194 @@
+/*
+ * lmpk.h -- C ABI of the B200-native level-blocked matrix power kernel (MPK).
+ *
+ * This is the drop-in boundary that replaces the numba/numpy hot paths of the
+ * reference package `levelmpk` (arXiv 2205.01598, /root/reference/pkg).  The
+ * reference selects its kernels through LEVELMPK_BACKEND at import time
+ * (pkg/src/levelmpk/backend.py:21-40); a `cuda` backend binds these entry
+ * points with ctypes (see INTEGRATION.md for the binding a maintainer adds).
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers owned by the caller (torch
+ *     tensors in the Python host layer).  The library never frees them.
+ *   - CRS layout follows pkg/src/levelmpk/csr.py:16-20,35-37: row_ptr int32
+ *     [n+1], col int32 [nnz] (strictly increasing per row), val f64 [nnz].
+ *   - Power vectors follow PowerVectors (pkg/src/levelmpk/executor.py:33-53):
+ *     slot s of a y block is y + s*ldy, each slot n contiguous doubles.
+ *     Complex128 state (Chebyshev, LMPK_COMPLEX) stores interleaved (re, im)
+ *     pairs, i.e. slot s occupies 2*n doubles starting at y + s*ldy.
+ *   - `stream` is a cudaStream_t passed as void*; NULL is the legacy stream.
+ *     Calls are stream-ordered and asynchronous unless stated otherwise.
+ *   - Every entry point returns an int status: 0 (LMPK_OK) or a negative
+ *     code; lmpk_last_error() returns a thread-local message.  The Python
+ *     layer maps LMPK_ERR_ARG to ValueError and everything else to
+ *     RuntimeError, mirroring the reference's exception contract
+ *     (SURVEY.md section 8b "Errors").
+ *   - Summation semantics (bit-exact mode, the default): every output row is
+ *     tmp = 0.0; for k in row order: tmp = tmp + val[k]*x[col[k]] with
+ *     separately rounded multiply and add (no FMA contraction), exactly the
+ *     numba kernel csr.py:195-201 / executor.py:127-135.  Results are bitwise
+ *     identical to the reference's numba backend on the same permuted matrix.
+ */
+#ifndef LMPK_H
+#define LMPK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LMPK_ABI_VERSION 1
+
+/* status codes */
+#define LMPK_OK 0
+#define LMPK_ERR_ARG -1         /* invalid argument -> ValueError            */
+#define LMPK_ERR_CUDA -2        /* CUDA runtime failure -> RuntimeError       */
+#define LMPK_ERR_WATCHDOG -3    /* device spin watchdog fired -> RuntimeError */
+#define LMPK_ERR_NOMEM -4       /* allocation failure -> RuntimeError         */
+#define LMPK_ERR_UNSUPPORTED -5 /* configuration not supported                */
+
+/* kernel ids per power (pkg/src/levelmpk/plan.py:34-35) */
+#define LMPK_KERNEL_SPMV 0 /* y_out = A y_in                                */
+#define LMPK_KERNEL_CHEB 1 /* y_out = 2 A y_in - y_prev (Chebyshev T_{n+1}) */
+
+/* flags */
+#define LMPK_FLAG_COMPLEX 0x1       /* vectors are complex128 (interleaved)      */
+#define LMPK_FLAG_MODE_STREAM 0x10  /* force streaming (L2) wavefront mode       */
+#define LMPK_FLAG_MODE_RESIDENT 0x20/* force SMEM-resident wavefront mode       */
+#define LMPK_FLAG_NO_TMA 0x40       /* stage tiles with plain loads, not TMA     */
+
+#define LMPK_MAX_POWERS 64
+
+typedef struct lmpk_ctx lmpk_ctx;       /* per-device scratch + epoch counters */
+typedef struct lmpk_tiling lmpk_tiling; /* tile geometry of one matrix for MPK */
+
+/* ---------------------------------------------------------------- misc */
+int lmpk_abi_version(void);
+const char* lmpk_last_error(void);
+/* Device properties used for planning. */
+int lmpk_device_info(int device, int* sm_count, int* max_smem_per_block,
+                     int* max_smem_per_sm, int* l2_bytes, int* cc_major, int* cc_minor);
+
+int lmpk_ctx_create(lmpk_ctx** out, int device);
+int lmpk_ctx_destroy(lmpk_ctx* ctx);
+/* Number of kernel launches this ctx issued since creation (for gpu_launches). */
+int64_t lmpk_ctx_launch_count(const lmpk_ctx* ctx);
+
+/* ---------------------------------------------------------------- SpMV
+ * out[r] = sum_k val[k]*x[col[k]] for r in [r0, r1); other rows untouched.
+ * Replaces spmv_rows / _spmv_rows_kernel (pkg/src/levelmpk/csr.py:192-233);
+ * spmv_range's inclusive-bounds and alias checks live in the Python layer
+ * (csr.py:235-249).  x and out must not alias. */
+int lmpk_spmv_rows(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                   const double* val, const double* x, double* out, int32_t r0, int32_t r1,
+                   int flags, void* stream);
+
+/* Baseline MPK: p_m back-to-back full-range SpMV sweeps,
+ *   y[p] = A y[p-1], p = 1..p_m, slot p at y + p*ldy.
+ * Replaces run_baseline / build_baseline_plan (executor.py:233-266): one
+ * kernel launch per power (the "k back-to-back SpMVs" roofline). */
+int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                      const double* val, double* y, int64_t ldy, int32_t p_m, int flags,
+                      void* stream);
+
+/* ---------------------------------------------------------------- level-blocked MPK
+ * Tiling: contiguous row tiles of the (level-permuted) matrix sized to the
+ * on-chip budget, plus each tile's dependency range [dep_lo, dep_hi] (tiles
+ * owning its column indices).  The kernel walks the power/tile wavefront:
+ * tile t at power p runs only after tiles dep_lo(t)..dep_hi(t) finished
+ * power p-1 -- the GPU form of the Lp-diagram conditions (A)/(B)/(C)
+ * (pkg/src/levelmpk/schedule.py:195-240, plan.py:322-370). */
+typedef struct lmpk_tiling_info {
+  int32_t n_tiles;
+  int32_t p_m;
+  int32_t mode;          /* 1 = SMEM-resident, 2 = streaming (L2)               */
+  int32_t grid;          /* CTAs launched                                       */
+  int32_t block;         /* threads per CTA                                     */
+  int32_t smem_bytes;    /* dynamic shared memory per CTA                       */
+  int32_t tile_nnz_cap;  /* max nonzeros per tile                               */
+  int32_t max_fwd_reach; /* max over tiles of (dep_hi - t)                      */
+  int32_t chain_reach;   /* max (p_m-1)-step forward dependency chain, in tiles */
+  int32_t max_row_nnz;
+  int64_t nnz;
+} lmpk_tiling_info;
+
+/* Build the tiling for an n-row matrix already resident on the device.
+ * tile_nnz_hint <= 0 lets the library choose; mode_flags may force a mode.
+ * Synchronizes `stream` (small D2H of tile geometry). */
+int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                       int32_t p_m, int32_t tile_nnz_hint, int32_t ctas_per_sm_hint,
+                       int mode_flags, lmpk_tiling** out, lmpk_tiling_info* info, void* stream);
+int lmpk_tiling_destroy(lmpk_tiling* t);
+/* Copy tile geometry to host arrays: tile_row[n_tiles+1], dep_lo/dep_hi[n_tiles]. */
+int lmpk_tiling_geometry(const lmpk_tiling* t, int32_t* tile_row, int32_t* dep_lo,
+                         int32_t* dep_hi);
+
+/* Per-power kernel configuration (plan.py:206-211 out_slot/in_slot/prev_slot/
+ * kernel/acc_coef, which in the reference depend only on an item's power). */
+typedef struct lmpk_power_cfg {
+  int32_t n_powers;                    /* p = 1..n_powers                       */
+  int32_t out_slot[LMPK_MAX_POWERS];   /* index by p-1                          */
+  int32_t in_slot[LMPK_MAX_POWERS];
+  int32_t prev_slot[LMPK_MAX_POWERS];
+  int32_t kernel[LMPK_MAX_POWERS];     /* LMPK_KERNEL_SPMV | LMPK_KERNEL_CHEB   */
+  double acc_coef_re[LMPK_MAX_POWERS]; /* acc += coef * y_out (if use_acc)      */
+  double acc_coef_im[LMPK_MAX_POWERS]; /* imaginary part (LMPK_FLAG_COMPLEX)    */
+} lmpk_power_cfg;
+
+/* Run the level-blocked MPK over `tiling` (built for this matrix).
+ * Replaces run_plan / _run_numba / _walk (executor.py:84-230).  y holds
+ * n_slots slots of stride ldy (in doubles); acc (length n, or 2n complex)
+ * is accumulated in place when use_acc != 0 (cheb.py:229,240). */
+int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* tiling, const int32_t* row_ptr,
+                 const int32_t* col, const double* val, double* y, int64_t ldy, int32_t n_slots,
+                 const lmpk_power_cfg* cfg, double* acc, int use_acc, int flags, void* stream);
+
+/* Synchronize `stream` and report a device-side failure of the last MPK
+ * launches (watchdog: a dependency spin exceeded its bound, the analogue of
+ * the reference's join watchdog executor.py:173-179). */
+int lmpk_ctx_check(lmpk_ctx* ctx, void* stream);
+
+/* ---------------------------------------------------------------- BFS levels + permutation
+ * Level construction of levels.py:48-114: BFS distance classes of the
+ * symmetrized pattern A|A^T from `root`; each level sorted ascending by
+ * vertex id; exhausted components restart at the lowest unvisited vertex.
+ * Outputs perm (new->old), inv_perm (old->new) and level_ptr (int64, up to
+ * n+1 entries; *n_levels receives L so that level_ptr[0..L] is valid).
+ * Bit-exact with the reference.  Synchronizes `stream`. */
+int lmpk_bfs_levels(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                    int32_t root, int32_t* perm, int32_t* inv_perm, int64_t* level_ptr,
+                    int64_t* n_levels, void* stream);
+
+/* Symmetrized pattern A|A^T (levels.py:48-61).  Returns via *sym_nnz the
+ * pattern size; if the pattern of A is already symmetric *is_symmetric = 1
+ * and nothing is written.  Otherwise out_row_ptr (int64[n+1]) and out_col
+ * (capacity cap) receive the canonical pattern; call with out_col == NULL
+ * to query the size first.  Synchronizes `stream`. */
+int lmpk_symmetrized_pattern(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr,
+                             const int32_t* col, int* is_symmetric, int64_t* sym_nnz,
+                             int64_t* out_row_ptr, int32_t* out_col, int64_t cap, void* stream);
+
+/* B[i,j] = A[perm[i], perm[j]], canonical (csr.py:169-187).  out arrays are
+ * n+1 / nnz long.  Bit-exact with the reference. */
+int lmpk_permute_symmetric(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                           const double* val, const int32_t* perm, const int32_t* inv_perm,
+                           int32_t* out_row_ptr, int32_t* out_col, double* out_val, void* stream);
+
+/* Vector permutations (csr.py:158-166, executor.py:69-76) on `n_vec`
+ * vectors of `width` doubles per entry (1 real, 2 complex), stride ldv.
+ * gather:  out[v][i] = in[v][perm[i]]   (apply_to_vector)
+ * scatter: out[v][perm[i]] = in[v][i]   (undo_on_vector / undo_permutation) */
+int lmpk_permute_vectors(lmpk_ctx* ctx, int32_t n, const int32_t* perm, const double* in,
+                         int64_t ld_in, double* out, int64_t ld_out, int32_t n_vec, int32_t width,
+                         int scatter, void* stream);
+
+/* Per-level nonzero counts: out[i] = row_ptr[level_ptr[i+1]] - row_ptr[level_ptr[i]]
+ * (groups.py:257-262 _level_nnz on the permuted matrix). */
+int lmpk_level_nnz(lmpk_ctx* ctx, const int32_t* row_ptr, const int64_t* level_ptr,
+                   int64_t n_levels, int64_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMPK_H */

@@ -1,0 +1,573 @@
+// bfs.cu -- BFS level construction and level ordering on sm_100a.
+//
+// Reference semantics (pkg/src/levelmpk/levels.py:48-114):
+//   * traverse the symmetrized pattern A|A^T (levels.py:48-61);
+//   * level 0 = {root}; level i+1 = sorted unvisited neighbours of level i;
+//   * when a component is exhausted, restart at the lowest unvisited vertex.
+// Restated (bit-exact): perm = stable sort of vertex ids by
+// the key (component rank, BFS distance), where the root's component ranks
+// first and the remaining components follow in order of their minimum
+// vertex, each traversed from that minimum vertex.  The lowest unvisited
+// vertex after finishing a set of whole components is always the minimum of
+// its own component, so this is exactly the reference's restart order.
+//
+// GPU pipeline:
+//   1. symmetry check of the pattern (binary search of (c, r) for every
+//      (r, c)); if asymmetric, A|A^T is built by a stable radix transpose and
+//      a per-row sorted union.
+//   2. frontier BFS from root in ONE cooperative persistent kernel (grid
+//      barrier per level, warp-cooperative load-balanced edge expansion,
+//      atomicCAS visit, warp-aggregated queue pushes).
+//   3. if vertices remain: connected components of the rest by min-root
+//      hooking (root = minimum vertex id), then a multi-source BFS from all
+//      component roots (same kernel).
+//   4. level ids: root component -> dist; other components -> L0 + offset
+//      (exclusive scan over roots in id order) + dist.
+//   5. perm = stable radix sort of ids by level id; level_ptr = exclusive
+//      scan of the level histogram; inv_perm = scatter.
+#include <algorithm>
+
+#include "lmpk_internal.cuh"
+#include "radix_sort.cuh"
+
+namespace lmpk {
+
+constexpr int kBfsThreads = 256;
+
+struct GridBar {
+  unsigned int count;
+  unsigned int gen;
+};
+
+__device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* vgen = &gb->gen;
+    const unsigned int g = *vgen;
+    __threadfence();
+    if (atomicAdd(&gb->count, 1u) == nblocks - 1) {
+      gb->count = 0;
+      __threadfence();
+      atomicAdd(&gb->gen, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- symmetry
+template <typename RP>
+__global__ void k_check_symmetric(int32_t n, const RP* row_ptr, const int32_t* col, int* asym) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int64_t k = row_ptr[r]; k < int64_t(row_ptr[r + 1]); ++k) {
+    const int32_t c = col[k];
+    if (c == r) continue;
+    int64_t lo = row_ptr[c], hi = int64_t(row_ptr[c + 1]) - 1;
+    bool found = false;
+    while (lo <= hi) {
+      int64_t mid = (lo + hi) >> 1;
+      int32_t v = col[mid];
+      if (v == r) {
+        found = true;
+        break;
+      }
+      if (v < r)
+        lo = mid + 1;
+      else
+        hi = mid - 1;
+    }
+    if (!found) {
+      atomicExch(asym, 1);
+      return;
+    }
+  }
+}
+
+__global__ void k_expand_rows(int32_t n, const int32_t* row_ptr, uint32_t* rows_out) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; ++k) rows_out[k] = uint32_t(r);
+}
+
+__global__ void k_iota_u32(uint32_t* p, int64_t n) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = uint32_t(i);
+}
+
+// transpose row pointer: counts of each column
+__global__ void k_col_counts(const int32_t* col, int64_t nnz, int64_t* cnt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nnz; i += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(reinterpret_cast<unsigned long long*>(cnt + col[i]), 1ull);
+}
+
+// merge row r of A (sorted cols) with row r of A^T (sorted rows): union size / write
+__global__ void k_union_rows(int32_t n, const int32_t* arp, const int32_t* acol, const int64_t* trp,
+                             const uint32_t* tcol, int64_t* out_cnt, const int64_t* out_rp,
+                             int32_t* out_col) {
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t i = arp[r], ie = arp[r + 1], j = trp[r], je = trp[r + 1];
+  int64_t w = out_rp ? out_rp[r] : 0, c = 0;
+  while (i < ie || j < je) {
+    int32_t a = i < ie ? acol[i] : INT32_MAX;
+    int32_t b = j < je ? int32_t(tcol[j]) : INT32_MAX;
+    int32_t v;
+    if (a < b) {
+      v = a;
+      ++i;
+    } else if (b < a) {
+      v = b;
+      ++j;
+    } else {
+      v = a;
+      ++i;
+      ++j;
+    }
+    if (out_col) out_col[w + c] = v;
+    ++c;
+  }
+  if (out_cnt) out_cnt[r] = c;
+}
+
+// ------------------------------------------------------------- BFS kernel
+struct BfsState {
+  int32_t* dist;      // -1 = unvisited (in this phase: eligible)
+  int32_t* qa;        // frontier queues
+  int32_t* qb;
+  uint32_t* sizes;    // [0] size of qa, [1] size of qb, [2] max level reached
+  GridBar* bar;
+  int32_t n;
+};
+
+// Expand the frontier q_in (size n_in) at level `lev` into q_out.
+// Warp-cooperative: each warp takes 32 frontier vertices, computes the
+// exclusive prefix of their degrees and strides the lanes over the combined
+// edge list (load balance independent of the degree distribution).
+template <typename RP>
+__device__ void bfs_expand(const RP* row_ptr, const int32_t* col, const BfsState& S,
+                           const int32_t* q_in, uint32_t n_in, int32_t* q_out, uint32_t* out_size,
+                           int32_t lev) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t base = warp_global * 32; base < n_in; base += n_warps * 32) {
+    const int64_t qi = base + lane;
+    int64_t start = 0, deg = 0;
+    if (qi < n_in) {
+      const int32_t u = q_in[qi];
+      start = row_ptr[u];
+      deg = int64_t(row_ptr[u + 1]) - start;
+    }
+    // inclusive scan of deg across the warp
+    int64_t inc = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const int64_t total = __shfl_sync(0xffffffffu, inc, 31);
+    const int64_t excl = inc - deg;
+    for (int64_t e0 = 0; e0 < total; e0 += 32) {
+      const int64_t e = e0 + lane;
+      const bool act = e < total;
+      const int64_t ee = act ? e : total - 1;
+      // owner = largest lane whose exclusive degree prefix is <= ee
+      int owner = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = owner + step;
+        const int64_t ex_c = __shfl_sync(0xffffffffu, excl, cand & 31);
+        if (cand < 32 && ex_c <= ee) owner = cand;
+      }
+      const int64_t st_o = __shfl_sync(0xffffffffu, start, owner);
+      const int64_t ex_o = __shfl_sync(0xffffffffu, excl, owner);
+      const int32_t v = act ? col[st_o + (ee - ex_o)] : -1;
+      bool push = false;
+      if (v >= 0 && S.dist[v] == -1) push = (atomicCAS(S.dist + v, -1, lev + 1) == -1);
+      const uint32_t m = __ballot_sync(0xffffffffu, push);
+      if (m) {
+        uint32_t off = 0;
+        if (lane == 0) off = atomicAdd(out_size, uint32_t(__popc(m)));
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (push) q_out[off + __popc(m & ((1u << lane) - 1u))] = v;
+      }
+    }
+  }
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kBfsThreads) k_bfs(const RP* row_ptr, const int32_t* col, BfsState S) {
+  int32_t lev = 0;
+  int32_t* qin = S.qa;
+  int32_t* qout = S.qb;
+  int cur = 0;
+  while (true) {
+    const uint32_t n_in = *((volatile uint32_t*)&S.sizes[cur]);
+    if (n_in == 0) break;
+    bfs_expand(row_ptr, col, S, qin, n_in, qout, &S.sizes[cur ^ 1], lev);
+    grid_barrier(S.bar, gridDim.x);
+    // reset the consumed queue size for the next round (one thread), then
+    // a second barrier so nobody reads the stale size
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S.sizes[cur] = 0;
+      if (*((volatile uint32_t*)&S.sizes[cur ^ 1]) > 0) S.sizes[2] = uint32_t(lev + 1);
+    }
+    grid_barrier(S.bar, gridDim.x);
+    int32_t* t = qin;
+    qin = qout;
+    qout = t;
+    cur ^= 1;
+    ++lev;
+  }
+}
+
+// ------------------------------------------------------------- components
+__device__ __forceinline__ int32_t cc_find(int32_t* parent, int32_t x) {
+  int32_t p = *((volatile int32_t*)&parent[x]);
+  while (p != x) {
+    const int32_t gp = *((volatile int32_t*)&parent[p]);
+    if (gp != p) atomicCAS(parent + x, p, gp);  // path halving
+    x = p;
+    p = gp;
+  }
+  return x;
+}
+
+__global__ void k_cc_init(int32_t n, const int32_t* dist, int32_t* parent) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    parent[v] = v;
+}
+
+template <typename RP>
+__global__ void k_cc_hook(int32_t n, const RP* row_ptr, const int32_t* col, const int32_t* dist,
+                          int32_t* parent) {
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    if (dist[u] != -1) continue;  // belongs to the root component
+    for (int64_t k = row_ptr[u]; k < int64_t(row_ptr[u + 1]); ++k) {
+      const int32_t v = col[k];
+      if (v <= u) continue;  // each undirected edge once (pattern is symmetric)
+      int32_t ru = cc_find(parent, u), rv = cc_find(parent, v);
+      while (ru != rv) {
+        if (ru < rv) {
+          const int32_t t = ru;
+          ru = rv;
+          rv = t;
+        }
+        // link the larger root under the smaller one: roots stay minimal
+        const int32_t old = atomicCAS(parent + ru, ru, rv);
+        if (old == ru) break;
+        ru = cc_find(parent, ru);
+        rv = cc_find(parent, rv);
+      }
+    }
+  }
+}
+
+// finalize labels; seed the multi-source frontier with the component roots
+__global__ void k_cc_finalize(int32_t n, int32_t* dist, int32_t* parent, int32_t* q, uint32_t* qsize) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (dist[v] != -1) continue;
+    const int32_t r = cc_find(parent, v);
+    parent[v] = r;
+    if (r == v) {
+      dist[v] = 0;
+      q[atomicAdd(qsize, 1u)] = v;
+    }
+  }
+}
+
+__global__ void k_comp_maxdist(int32_t n, const int32_t* dist, const int32_t* label,
+                               const uint8_t* is_tail, int32_t* cmax) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (is_tail[v]) atomicMax(cmax + label[v], dist[v]);
+}
+
+__global__ void k_comp_levels(int32_t n, const int32_t* label, const uint8_t* is_tail,
+                              const int32_t* cmax, int32_t* nlev) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    nlev[v] = (is_tail[v] && label[v] == v) ? cmax[v] + 1 : 0;
+}
+
+__global__ void k_level_ids(int32_t n, const int32_t* dist, const int32_t* label, const uint8_t* is_tail,
+                            const int64_t* cbase, uint32_t L0, uint32_t* keys, uint32_t* vals,
+                            unsigned long long* hist) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    uint32_t lid;
+    if (is_tail && is_tail[v])
+      lid = L0 + uint32_t(cbase[label[v]]) + uint32_t(dist[v]);
+    else
+      lid = uint32_t(dist[v]);
+    keys[v] = lid;
+    vals[v] = uint32_t(v);
+    atomicAdd(hist + lid, 1ull);
+  }
+}
+
+__global__ void k_mark_tail(int32_t n, const int32_t* dist, uint8_t* is_tail) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    is_tail[v] = dist[v] == -1 ? 1 : 0;
+}
+
+__global__ void k_perm_out(int32_t n, const uint32_t* sorted_vals, int32_t* perm, int32_t* inv) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t v = int32_t(sorted_vals[i]);
+    perm[i] = v;
+    inv[v] = i;
+  }
+}
+
+template <typename RP>
+static int launch_bfs(lmpk_ctx* ctx, const RP* row_ptr, const int32_t* col, BfsState S, cudaStream_t st) {
+  int occ = 0;
+  LMPK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs<RP>, kBfsThreads, 0));
+  occ = std::max(1, std::min(occ, 4));
+  const int grid = occ * ctx->sm_count;
+  void* args[] = {(void*)&row_ptr, (void*)&col, (void*)&S};
+  LMPK_CHECK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs<RP>), dim3(grid),
+                                              dim3(kBfsThreads), args, 0, st));
+  launch_count_add(ctx, 1);
+  return LMPK_OK;
+}
+
+static inline int grid_for(lmpk_ctx* ctx, int64_t n) {
+  return int(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, int64_t(ctx->sm_count) * 16)));
+}
+
+template <typename RP>
+static int bfs_core(lmpk_ctx* ctx, int32_t n, const RP* row_ptr, const int32_t* col, int32_t root,
+                    int32_t* perm, int32_t* inv, int64_t* level_ptr, int64_t* n_levels, cudaStream_t st) {
+  // scratch layout (ctx->s_a .. s_e)
+  const size_t N = size_t(n);
+  LMPK_TRY(ctx->s_a.ensure(N * 4 * 4 + 4096));  // dist, qa, qb, parent
+  int32_t* dist = reinterpret_cast<int32_t*>(ctx->s_a.ptr);
+  int32_t* qa = dist + N;
+  int32_t* qb = qa + N;
+  int32_t* parent = qb + N;
+  LMPK_TRY(ctx->s_small.ensure(4096));
+  uint32_t* sizes = reinterpret_cast<uint32_t*>(ctx->s_small.ptr);
+  GridBar* bar = reinterpret_cast<GridBar*>(sizes + 8);
+  LMPK_CHECK_CUDA(cudaMemsetAsync(ctx->s_small.ptr, 0, 256, st));
+  LMPK_CHECK_CUDA(cudaMemsetAsync(dist, 0xff, N * 4, st));
+  // seed: dist[root] = 0, qa = [root]
+  const int32_t zero = 0;
+  const uint32_t one = 1;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(dist + root, &zero, 4, cudaMemcpyHostToDevice, st));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(qa, &root, 4, cudaMemcpyHostToDevice, st));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(sizes, &one, 4, cudaMemcpyHostToDevice, st));
+  BfsState S{dist, qa, qb, sizes, bar, n};
+  LMPK_TRY(launch_bfs<RP>(ctx, row_ptr, col, S, st));
+  uint32_t h_sizes[4];
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(h_sizes, sizes, 16, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  const uint32_t L0 = h_sizes[2] + 1;  // levels of the root component
+
+  // count unvisited via the tail mask
+  LMPK_TRY(ctx->s_b.ensure(N + 64));
+  uint8_t* is_tail = reinterpret_cast<uint8_t*>(ctx->s_b.ptr);
+  k_mark_tail<<<grid_for(ctx, n), 256, 0, st>>>(n, dist, is_tail);
+  launch_count_add(ctx, 1);
+
+  // scratch for sort + scans
+  const int64_t cnt_len = radix_counts_len(n);
+  const int64_t tmp_len = std::max(scan_tmp_len(cnt_len), scan_tmp_len(int64_t(n) + 1)) + 8;
+  LMPK_TRY(ctx->s_c.ensure(N * 4 * 4 + 64));  // keys0, vals0, keys1, vals1
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(ctx->s_c.ptr);
+  uint32_t* v0 = k0 + N;
+  uint32_t* k1 = v0 + N;
+  uint32_t* v1 = k1 + N;
+  LMPK_TRY(ctx->s_d.ensure(size_t(cnt_len) * 4 + size_t(cnt_len) * 8 + size_t(tmp_len) * 8 + 64));
+  uint32_t* counts = reinterpret_cast<uint32_t*>(ctx->s_d.ptr);
+  int64_t* offsets = reinterpret_cast<int64_t*>(counts + ((cnt_len + 1) & ~int64_t(1)));
+  int64_t* stmp = offsets + cnt_len;
+  LMPK_TRY(ctx->s_e.ensure((N + 2) * 8 * 2 + 64));
+  unsigned long long* hist = reinterpret_cast<unsigned long long*>(ctx->s_e.ptr);
+  int64_t* cbase = reinterpret_cast<int64_t*>(hist + N + 1);
+
+  uint32_t total_levels = L0;
+  // number of visited = 1 + all pushes; pushes are not counted separately, so
+  // reduce the tail mask instead (cheap: one scan)
+  int64_t tail_count = 0;
+  LMPK_TRY(device_excl_scan<uint8_t, int64_t>(ctx, is_tail, n, cbase, 0, true, stmp, st));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&tail_count, cbase + n, 8, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+
+  if (tail_count > 0) {
+    // connected components of the remaining vertices, roots = minimum ids
+    k_cc_init<<<grid_for(ctx, n), 256, 0, st>>>(n, dist, parent);
+    k_cc_hook<RP><<<grid_for(ctx, n), 256, 0, st>>>(n, row_ptr, col, dist, parent);
+    LMPK_CHECK_CUDA(cudaMemsetAsync(sizes, 0, 16, st));
+    k_cc_finalize<<<grid_for(ctx, n), 256, 0, st>>>(n, dist, parent, qa, sizes);
+    launch_count_add(ctx, 3);
+    // multi-source BFS over the tail (main-component vertices have dist >= 0)
+    LMPK_TRY(launch_bfs<RP>(ctx, row_ptr, col, S, st));
+    // per-component level counts -> exclusive scan in root-id order
+    int32_t* cmax = qb;  // reuse
+    LMPK_CHECK_CUDA(cudaMemsetAsync(cmax, 0xff, N * 4, st));
+    k_comp_maxdist<<<grid_for(ctx, n), 256, 0, st>>>(n, dist, parent, is_tail, cmax);
+    int32_t* nlev = qa;  // reuse
+    k_comp_levels<<<grid_for(ctx, n), 256, 0, st>>>(n, parent, is_tail, cmax, nlev);
+    launch_count_add(ctx, 2);
+    LMPK_TRY(device_excl_scan<int32_t, int64_t>(ctx, nlev, n, cbase, 0, true, stmp, st));
+    int64_t tail_levels = 0;
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(&tail_levels, cbase + n, 8, cudaMemcpyDeviceToHost, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+    total_levels = L0 + uint32_t(tail_levels);
+  }
+  LMPK_CHECK_CUDA(cudaMemsetAsync(hist, 0, (size_t(total_levels) + 1) * 8, st));
+  k_level_ids<<<grid_for(ctx, n), 256, 0, st>>>(n, dist, parent, tail_count > 0 ? is_tail : nullptr, cbase,
+                                                L0, k0, v0, hist);
+  launch_count_add(ctx, 1);
+  int bits = 0;
+  while (bits < 32 && (uint64_t(1) << bits) < uint64_t(total_levels)) ++bits;
+  bool in_first = true;
+  LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, n, bits, counts, offsets, stmp, &in_first, st));
+  k_perm_out<<<grid_for(ctx, n), 256, 0, st>>>(n, in_first ? v0 : v1, perm, inv);
+  launch_count_add(ctx, 1);
+  // level_ptr = exclusive scan of the histogram, L+1 entries
+  LMPK_TRY(device_excl_scan<unsigned long long, int64_t>(ctx, hist, total_levels, level_ptr, 0, true,
+                                                         stmp, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  *n_levels = total_levels;
+  return LMPK_OK;
+}
+
+}  // namespace lmpk
+
+using namespace lmpk;
+
+// Returns 1 in *asym if the pattern is not symmetric.
+static int check_symmetric(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                           int* asym, cudaStream_t st) {
+  LMPK_TRY(ctx->s_small.ensure(4096));
+  int* d = reinterpret_cast<int*>(ctx->s_small.ptr) + 64;
+  LMPK_CHECK_CUDA(cudaMemsetAsync(d, 0, 4, st));
+  k_check_symmetric<int32_t><<<div_up(n, 256), 256, 0, st>>>(n, row_ptr, col, d);
+  launch_count_add(ctx, 1);
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(asym, d, 4, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  return LMPK_OK;
+}
+
+// Build A|A^T into (sym_rp int64 [n+1], sym_col) allocated in ctx->s_f/s_g.
+static int build_union(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                       int64_t** out_rp, int32_t** out_col, int64_t* out_nnz, cudaStream_t st) {
+  int32_t h_nnz = 0;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_nnz, row_ptr + n, 4, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  const int64_t nnz = h_nnz;
+  const size_t N = size_t(n);
+  // transpose: stable sort of (col -> row) pairs, rows enter in ascending order
+  LMPK_TRY(ctx->s_c.ensure(size_t(nnz) * 16 + 64));
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(ctx->s_c.ptr);
+  uint32_t* v0 = k0 + nnz;
+  uint32_t* k1 = v0 + nnz;
+  uint32_t* v1 = k1 + nnz;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(k0, col, size_t(nnz) * 4, cudaMemcpyDeviceToDevice, st));
+  k_expand_rows<<<div_up(n, 256), 256, 0, st>>>(n, row_ptr, v0);
+  launch_count_add(ctx, 1);
+  const int64_t cnt_len = radix_counts_len(nnz);
+  const int64_t tmp_len = std::max(scan_tmp_len(cnt_len), scan_tmp_len(int64_t(n) + 1)) + 8;
+  LMPK_TRY(ctx->s_d.ensure(size_t(cnt_len) * 12 + size_t(tmp_len) * 8 + 64));
+  uint32_t* counts = reinterpret_cast<uint32_t*>(ctx->s_d.ptr);
+  int64_t* offsets = reinterpret_cast<int64_t*>(counts + ((cnt_len + 1) & ~int64_t(1)));
+  int64_t* stmp = offsets + cnt_len;
+  int bits = 0;
+  while (bits < 32 && (int64_t(1) << bits) < int64_t(n)) ++bits;
+  bool in_first = true;
+  LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, nnz, bits, counts, offsets, stmp, &in_first, st));
+  uint32_t* trows = in_first ? v0 : v1;
+  // transposed row pointer
+  LMPK_TRY(ctx->s_e.ensure((N + 2) * 8 * 3 + 64));
+  int64_t* cnt = reinterpret_cast<int64_t*>(ctx->s_e.ptr);
+  int64_t* trp = cnt + N + 2;
+  int64_t* urp = trp + N + 2;
+  LMPK_CHECK_CUDA(cudaMemsetAsync(cnt, 0, N * 8, st));
+  k_col_counts<<<grid_for(ctx, nnz), 256, 0, st>>>(col, nnz, cnt);
+  launch_count_add(ctx, 1);
+  LMPK_TRY(device_excl_scan<int64_t, int64_t>(ctx, cnt, n, trp, 0, true, stmp, st));
+  // union sizes -> row pointer -> write
+  k_union_rows<<<div_up(n, 256), 256, 0, st>>>(n, row_ptr, col, trp, trows, cnt, nullptr, nullptr);
+  launch_count_add(ctx, 1);
+  LMPK_TRY(device_excl_scan<int64_t, int64_t>(ctx, cnt, n, urp, 0, true, stmp, st));
+  int64_t unnz = 0;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&unnz, urp + n, 8, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  LMPK_TRY(ctx->s_f.ensure((N + 1) * 8 + 64));
+  LMPK_TRY(ctx->s_g.ensure(size_t(unnz) * 4 + 64));
+  int64_t* srp = reinterpret_cast<int64_t*>(ctx->s_f.ptr);
+  int32_t* scol = reinterpret_cast<int32_t*>(ctx->s_g.ptr);
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(srp, urp, (N + 1) * 8, cudaMemcpyDeviceToDevice, st));
+  k_union_rows<<<div_up(n, 256), 256, 0, st>>>(n, row_ptr, col, trp, trows, nullptr, srp, scol);
+  launch_count_add(ctx, 1);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  *out_rp = srp;
+  *out_col = scol;
+  *out_nnz = unnz;
+  return LMPK_OK;
+}
+
+extern "C" int lmpk_symmetrized_pattern(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr,
+                                        const int32_t* col, int* is_symmetric, int64_t* sym_nnz,
+                                        int64_t* out_row_ptr, int32_t* out_col, int64_t cap,
+                                        void* stream) {
+  LMPK_ARG_CHECK(ctx && is_symmetric && sym_nnz, "lmpk_symmetrized_pattern: NULL argument");
+  cudaStream_t st = as_stream(stream);
+  int asym = 0;
+  if (n > 0) LMPK_TRY(check_symmetric(ctx, n, row_ptr, col, &asym, st));
+  if (!asym) {
+    int32_t h_nnz = 0;
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_nnz, row_ptr + n, 4, cudaMemcpyDeviceToHost, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+    *is_symmetric = 1;
+    *sym_nnz = h_nnz;
+    return LMPK_OK;
+  }
+  *is_symmetric = 0;
+  int64_t* srp;
+  int32_t* scol;
+  int64_t unnz;
+  LMPK_TRY(build_union(ctx, n, row_ptr, col, &srp, &scol, &unnz, st));
+  *sym_nnz = unnz;
+  if (out_col != nullptr) {
+    LMPK_ARG_CHECK(cap >= unnz, "out_col capacity %lld < %lld", (long long)cap, (long long)unnz);
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(out_row_ptr, srp, (size_t(n) + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(out_col, scol, size_t(unnz) * 4, cudaMemcpyDeviceToDevice, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
+  return LMPK_OK;
+}
+
+extern "C" int lmpk_bfs_levels(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                               int32_t root, int32_t* perm, int32_t* inv_perm, int64_t* level_ptr,
+                               int64_t* n_levels, void* stream) {
+  LMPK_ARG_CHECK(ctx && perm && inv_perm && level_ptr && n_levels, "lmpk_bfs_levels: NULL argument");
+  LMPK_ARG_CHECK(n >= 1, "matrix must have at least one row");
+  LMPK_ARG_CHECK(0 <= root && root < n, "root %d out of range for n=%d", root, n);
+  cudaStream_t st = as_stream(stream);
+  int asym = 0;
+  LMPK_TRY(check_symmetric(ctx, n, row_ptr, col, &asym, st));
+  if (!asym) return bfs_core<int32_t>(ctx, n, row_ptr, col, root, perm, inv_perm, level_ptr, n_levels, st);
+  int64_t* srp;
+  int32_t* scol;
+  int64_t unnz;
+  LMPK_TRY(build_union(ctx, n, row_ptr, col, &srp, &scol, &unnz, st));
+  return bfs_core<int64_t>(ctx, n, srp, scol, root, perm, inv_perm, level_ptr, n_levels, st);
+}
+
+__global__ void k_level_nnz(const int32_t* row_ptr, const int64_t* level_ptr, int64_t L, int64_t* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < L; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = int64_t(row_ptr[level_ptr[i + 1]]) - int64_t(row_ptr[level_ptr[i]]);
+}
+
+extern "C" int lmpk_level_nnz(lmpk_ctx* ctx, const int32_t* row_ptr, const int64_t* level_ptr,
+                              int64_t n_levels, int64_t* out, void* stream) {
+  LMPK_ARG_CHECK(ctx && row_ptr && level_ptr && out, "lmpk_level_nnz: NULL argument");
+  if (n_levels <= 0) return LMPK_OK;
+  k_level_nnz<<<grid_for(ctx, n_levels), 256, 0, as_stream(stream)>>>(row_ptr, level_ptr, n_levels, out);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 1);
+  return LMPK_OK;
+}

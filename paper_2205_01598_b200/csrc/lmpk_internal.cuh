@@ -1,0 +1,263 @@
+// lmpk_internal.cuh -- shared device/host helpers of liblmpk (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <vector>
+
+#include "lmpk.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "liblmpk is written for sm_100a (B200) only"
+#endif
+
+namespace lmpk {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+
+#define LMPK_CHECK_CUDA(call)                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      cudaGetLastError();                                                                  \
+      ::lmpk::set_error("%s:%d: %s failed: %s", __FILE__, __LINE__, #call,                 \
+                        cudaGetErrorString(e_));                                           \
+      return LMPK_ERR_CUDA;                                                                \
+    }                                                                                      \
+  } while (0)
+
+#define LMPK_ARG_CHECK(cond, ...)                                                          \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      ::lmpk::set_error(__VA_ARGS__);                                                      \
+      return LMPK_ERR_ARG;                                                                 \
+    }                                                                                      \
+  } while (0)
+
+#define LMPK_TRY(...)                                                                      \
+  do {                                                                                     \
+    int rc_ = (__VA_ARGS__);                                                               \
+    if (rc_ != LMPK_OK) return rc_;                                                        \
+  } while (0)
+
+// ------------------------------------------------------------------ ctx
+// Grow-only device scratch buffer owned by a ctx.
+struct Scratch {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  void release();
+};
+
+struct DeviceFlags {  // host-mapped pinned words the device writes on failure
+  volatile int* host = nullptr;
+  int* dev = nullptr;
+};
+
+}  // namespace lmpk
+
+struct lmpk_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int max_smem_block = 0;  // opt-in max per block
+  int max_smem_sm = 0;
+  int l2_bytes = 0;
+  int64_t launches = 0;
+  lmpk::DeviceFlags err;   // watchdog / device error word
+  // MPK synchronisation state (epoch-tagged counters, never memset per call)
+  uint32_t epoch = 0;
+  // scratch pools
+  lmpk::Scratch s_small, s_a, s_b, s_c, s_d, s_e, s_f, s_g;
+  uint64_t* queue_ctr = nullptr;  // monotone work-queue counter (device)
+  uint64_t queue_base = 0;        // host mirror of the counter value
+};
+
+struct lmpk_tiling {
+  lmpk_ctx* ctx = nullptr;
+  lmpk_tiling_info info{};
+  int32_t n = 0;
+  int32_t* d_tile_row = nullptr;  // [n_tiles+1]
+  int32_t* d_dep_lo = nullptr;    // [n_tiles]
+  int32_t* d_dep_hi = nullptr;    // [n_tiles]
+  int32_t* d_items = nullptr;     // streaming-mode item order, packed t*128+p
+  uint32_t* d_progress = nullptr; // [n_tiles] epoch-tagged power counters
+  std::vector<int32_t> h_tile_row, h_dep_lo, h_dep_hi;
+  int32_t rows_cap = 0;
+};
+
+namespace lmpk {
+
+int ctx_check_device_error(lmpk_ctx* ctx, const char* what);
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 1-D TMA bulk copy global -> shared (cp.async.bulk), completion on mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                         uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Coherent (weak, L1-allocating) global load -- never the .nc path, since the
+// MPK kernel reads vectors other CTAs write during the same launch.
+__device__ __forceinline__ double ld_weak(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_weak2(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_cg(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Bit-exact CRS row sum: tmp = 0.0; tmp = tmp + v[k]*x[c[k]] in storage order,
+// each multiply and add separately rounded (csr.py:196-201, executor.py:127-130).
+// The gathers of a chunk of 8 are issued before the dependent add chain.
+template <typename LoadX>
+__device__ __forceinline__ double row_sum_exact(const int32_t* c, const double* v, int len,
+                                                LoadX ldx) {
+  double tmp = 0.0;
+  int k = 0;
+  for (; k + 8 <= len; k += 8) {
+    int cc[8];
+    double vv[8], xx[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      cc[j] = c[k + j];
+      vv[j] = v[k + j];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xx[j] = ldx(cc[j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tmp = __dadd_rn(tmp, __dmul_rn(vv[j], xx[j]));
+  }
+  const int rem = len - k;
+  if (rem > 0) {
+    int cc[8];
+    double vv[8], xx[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < rem) {
+        cc[j] = c[k + j];
+        vv[j] = v[k + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < rem) xx[j] = ldx(cc[j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < rem) tmp = __dadd_rn(tmp, __dmul_rn(vv[j], xx[j]));
+  }
+  return tmp;
+}
+
+// Same for complex128 vectors with a real matrix: real and imaginary parts
+// are two independent storage-order sums.
+template <typename LoadX2>
+__device__ __forceinline__ double2 row_sum_exact_c(const int32_t* c, const double* v, int len,
+                                                   LoadX2 ldx) {
+  double tr = 0.0, ti = 0.0;
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    int cc[4];
+    double vv[4];
+    double2 xx[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      cc[j] = c[k + j];
+      vv[j] = v[k + j];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xx[j] = ldx(cc[j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      tr = __dadd_rn(tr, __dmul_rn(vv[j], xx[j].x));
+      ti = __dadd_rn(ti, __dmul_rn(vv[j], xx[j].y));
+    }
+  }
+  for (; k < len; ++k) {
+    const double vv = v[k];
+    const double2 xx = ldx(c[k]);
+    tr = __dadd_rn(tr, __dmul_rn(vv, xx.x));
+    ti = __dadd_rn(ti, __dmul_rn(vv, xx.y));
+  }
+  return make_double2(tr, ti);
+}
+
+// ------------------------------------------------------------------ host helpers
+int launch_count_add(lmpk_ctx* ctx, int n);
+static inline int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace lmpk

@@ -1,0 +1,235 @@
+"""Torch-facing wrappers of the C-ABI (include/lmpk.h).
+
+torch is used only for device memory and streams: every tensor here is a
+buffer handed to liblmpk by pointer.  All functions fail loudly when the
+library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, context, ptr, stream_handle
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+@dataclass
+class DeviceCsr:
+    """CRS arrays resident in HBM (row_ptr int32[n+1], col int32[nnz], val f64[nnz])."""
+
+    n: int
+    row_ptr: "object"
+    col: "object"
+    val: "object"
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.shape[0])
+
+    @classmethod
+    def from_host(cls, row_ptr, col, val, device=None):
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        rp = torch.from_numpy(np.ascontiguousarray(row_ptr, dtype=np.int32)).to(dev, non_blocking=False)
+        c = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int32)).to(dev)
+        v = torch.from_numpy(np.ascontiguousarray(val, dtype=np.float64)).to(dev)
+        return cls(int(rp.shape[0] - 1), rp, c, v)
+
+    def to_host(self):
+        return (self.row_ptr.cpu().numpy(), self.col.cpu().numpy(), self.val.cpu().numpy())
+
+
+def spmv_rows(a: DeviceCsr, x, out, r0, r1, flags=0, stream=None):
+    """out[r] = sum val*x[col] for r in [r0, r1) (csr.py:195-201 bitwise)."""
+    ctx = context()
+    check(ctx.lib.lmpk_spmv_rows(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
+                                 ptr(x), ptr(out), int(r0), int(r1), int(flags),
+                                 stream_handle(stream)), "spmv_rows")
+
+
+def mpk_baseline(a: DeviceCsr, y, p_m, flags=0, stream=None):
+    """p_m back-to-back SpMV sweeps on the slots of y (shape [>=p_m+1, n])."""
+    ctx = context()
+    check(ctx.lib.lmpk_mpk_baseline(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
+                                    ptr(y), int(y.stride(0)), int(p_m), int(flags),
+                                    stream_handle(stream)), "mpk_baseline")
+
+
+class Tiling:
+    """Tile geometry of one device matrix for the level-blocked kernel."""
+
+    def __init__(self, a: DeviceCsr, p_m, tile_nnz=0, ctas_per_sm=0, mode_flags=0, stream=None):
+        self.ctx = context()
+        self.a = a
+        h = ctypes.c_void_p()
+        info = _lib.TilingInfo()
+        check(self.ctx.lib.lmpk_tiling_create(
+            self.ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), int(p_m), int(tile_nnz),
+            int(ctas_per_sm), int(mode_flags), ctypes.byref(h), ctypes.byref(info),
+            stream_handle(stream)), "tiling_create")
+        self.handle = h
+        self.info = info.as_dict()
+
+    @property
+    def mode(self) -> str:
+        return {1: "resident", 2: "streaming"}[self.info["mode"]]
+
+    def geometry(self):
+        nt = self.info["n_tiles"]
+        tr = np.empty(nt + 1, dtype=np.int32)
+        lo = np.empty(nt, dtype=np.int32)
+        hi = np.empty(nt, dtype=np.int32)
+        check(self.ctx.lib.lmpk_tiling_geometry(
+            self.handle, tr.ctypes.data_as(ctypes.c_void_p), lo.ctypes.data_as(ctypes.c_void_p),
+            hi.ctypes.data_as(ctypes.c_void_p)))
+        return tr, lo, hi
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.ctx.lib.lmpk_tiling_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def power_cfg(n_powers, out_slot, in_slot, prev_slot, kernel, coef_re=None, coef_im=None):
+    cfg = _lib.PowerCfg()
+    if not 1 <= n_powers <= _lib.MAX_POWERS:
+        raise ValueError(f"p_m must be in [1, {_lib.MAX_POWERS}] for the cuda backend")
+    cfg.n_powers = int(n_powers)
+    for i in range(n_powers):
+        cfg.out_slot[i] = int(out_slot[i])
+        cfg.in_slot[i] = int(in_slot[i])
+        cfg.prev_slot[i] = int(prev_slot[i])
+        cfg.kernel[i] = int(kernel[i])
+        cfg.acc_coef_re[i] = float(coef_re[i]) if coef_re is not None else 0.0
+        cfg.acc_coef_im[i] = float(coef_im[i]) if coef_im is not None else 0.0
+    return cfg
+
+
+def mpk_power_cfg(p_m):
+    """Plain MPK: out = p, in = p-1, prev = max(p-2, 0) (plan.py:307-312)."""
+    p = np.arange(1, p_m + 1)
+    return power_cfg(p_m, p, p - 1, np.maximum(p - 2, 0), np.zeros(p_m, dtype=int))
+
+
+def mpk_run(tiling: Tiling, y, cfg, acc=None, use_acc=False, complex_state=False, flags=0,
+            stream=None, check_errors=True):
+    """Level-blocked MPK over the slots of y (torch float64, [n_slots, n] or
+    [n_slots, 2n] for complex state viewed as float64)."""
+    ctx = tiling.ctx
+    a = tiling.a
+    f = int(flags) | (_lib.FLAG_COMPLEX if complex_state else 0)
+    check(ctx.lib.lmpk_mpk_run(ctx.handle, tiling.handle, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
+                               ptr(y), int(y.stride(0)), int(y.shape[0]), ctypes.byref(cfg),
+                               ptr(acc), 1 if use_acc else 0, f, stream_handle(stream)), "mpk_run")
+    if check_errors:
+        check(ctx.lib.lmpk_ctx_check(ctx.handle, stream_handle(stream)), "mpk_run")
+
+
+def bfs_levels(a: DeviceCsr, root=0, stream=None):
+    """Returns (perm int32 tensor, inv_perm int32 tensor, level_ptr int64 numpy)."""
+    torch = _torch()
+    ctx = context()
+    dev = a.row_ptr.device
+    perm = torch.empty(a.n, dtype=torch.int32, device=dev)
+    inv = torch.empty(a.n, dtype=torch.int32, device=dev)
+    lp = torch.empty(a.n + 1, dtype=torch.int64, device=dev)
+    nl = ctypes.c_int64()
+    check(ctx.lib.lmpk_bfs_levels(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), int(root),
+                                  ptr(perm), ptr(inv), ptr(lp), ctypes.byref(nl),
+                                  stream_handle(stream)), "bfs_levels")
+    L = int(nl.value)
+    return perm, inv, lp[: L + 1].cpu().numpy()
+
+
+def symmetrized_pattern(a: DeviceCsr, stream=None):
+    """(row_ptr int64, col int32) tensors of A|A^T, or None if A is symmetric."""
+    torch = _torch()
+    ctx = context()
+    sym = ctypes.c_int()
+    nnz = ctypes.c_int64()
+    check(ctx.lib.lmpk_symmetrized_pattern(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col),
+                                           ctypes.byref(sym), ctypes.byref(nnz), None, None, 0,
+                                           stream_handle(stream)), "symmetrized_pattern")
+    if sym.value:
+        return None
+    dev = a.row_ptr.device
+    rp = torch.empty(a.n + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(max(int(nnz.value), 1), dtype=torch.int32, device=dev)
+    check(ctx.lib.lmpk_symmetrized_pattern(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col),
+                                           ctypes.byref(sym), ctypes.byref(nnz), ptr(rp), ptr(col),
+                                           int(col.shape[0]), stream_handle(stream)),
+          "symmetrized_pattern")
+    return rp, col[: int(nnz.value)]
+
+
+def permute_symmetric(a: DeviceCsr, perm, inv, stream=None) -> DeviceCsr:
+    torch = _torch()
+    ctx = context()
+    dev = a.row_ptr.device
+    rp = torch.empty(a.n + 1, dtype=torch.int32, device=dev)
+    col = torch.empty(a.nnz, dtype=torch.int32, device=dev)
+    val = torch.empty(a.nnz, dtype=torch.float64, device=dev)
+    check(ctx.lib.lmpk_permute_symmetric(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
+                                         ptr(perm), ptr(inv), ptr(rp), ptr(col), ptr(val),
+                                         stream_handle(stream)), "permute_symmetric")
+    return DeviceCsr(a.n, rp, col, val)
+
+
+def permute_vectors(perm, src, dst, scatter=False, stream=None):
+    """gather: dst[v][i] = src[v][perm[i]]; scatter: dst[v][perm[i]] = src[v][i].
+    src/dst: float64 tensors [n_vec, n] or complex128 [n_vec, n]."""
+    torch = _torch()
+    ctx = context()
+    width = 1
+    if src.dtype == torch.complex128:
+        width = 2
+        src = torch.view_as_real(src)
+        dst = torch.view_as_real(dst)
+    if src.dim() == 1 or (width == 2 and src.dim() == 2):
+        src = src.unsqueeze(0)
+        dst = dst.unsqueeze(0)
+    n = int(perm.shape[0])
+    check(ctx.lib.lmpk_permute_vectors(ctx.handle, n, ptr(perm), ptr(src), int(src.stride(0)),
+                                       ptr(dst), int(dst.stride(0)), int(src.shape[0]), width,
+                                       1 if scatter else 0, stream_handle(stream)),
+          "permute_vectors")
+
+
+def level_nnz(a: DeviceCsr, level_ptr, stream=None):
+    torch = _torch()
+    ctx = context()
+    lp = torch.as_tensor(np.ascontiguousarray(level_ptr, dtype=np.int64), device=a.row_ptr.device)
+    L = int(lp.shape[0] - 1)
+    out = torch.empty(max(L, 1), dtype=torch.int64, device=a.row_ptr.device)
+    check(ctx.lib.lmpk_level_nnz(ctx.handle, ptr(a.row_ptr), ptr(lp), L, ptr(out),
+                                 stream_handle(stream)), "level_nnz")
+    return out[:L].cpu().numpy()
+
+
+def probe_read_bw(nbytes, reps=10, trials=5):
+    ctx = context()
+    g = ctypes.c_double()
+    check(ctx.lib.lmpk_probe_read_bw(ctx.handle, int(nbytes), int(reps), int(trials), ctypes.byref(g)))
+    return g.value
+
+
+def probe_flag_latency(iters=10000):
+    ctx = context()
+    g = ctypes.c_double()
+    check(ctx.lib.lmpk_probe_flag_latency(ctx.handle, int(iters), ctypes.byref(g)))
+    return g.value
