@@ -1,0 +1,395 @@
+"""Benchmark of the level-blocked MPK (BASELINE.json config 2 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): 3D 7-point Laplacian on a 200^3 grid
+(gen_stencil_3d(200, 2): N = 8.0M, nnz = 55.76M, fp64 values, int32 indices),
+BFS level ordering from row 0, x uniform[-1, 1] from seed 0, MPK k = 8.
+A step is one MPK call (y_1..y_8 from y_0) on HBM-resident inputs.
+
+Metric: effective GFLOP/s = 2 * nnz * k / t (executor.py:65-66).  The line
+also carries the read-once HBM roofline fraction (Q_ro = 12 nnz + 4 (N+1) +
+8 N (k+1) bytes per call), the end-to-end number through the public API with
+host buffers, the k x SpMV comparators, the CPU baseline (oracle restatement of
+the reference's p2p walker on the host cores) and SM clocks sampled during the
+timed region.  Working set per step 1.28 GB > 126 MB L2, so no L2 flush is
+needed between steps.
+
+--impl reference times the reference's CPU MPK (its lb_lg_p2p walker and
+plan, restated in C in oracle/, the Python reference does not travel to the
+GPU box) on the host cores, on the same config and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MPK effective GFLOP/s (2*nnz*k per call)"
+PEAK_FALLBACK_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return PEAK_FALLBACK_GBS, "fallback"
+
+
+def workload(cfg):
+    if cfg == "cfg2":
+        return dict(name="cfg2: 3D 7-pt Laplacian 200^3 (gen_stencil_3d(200,2)), k=8", n=200, k=8)
+    if cfg == "cfg2-small":
+        return dict(name="cfg2-small: 3D 7-pt Laplacian 64^3, k=8", n=64, k=8)
+    raise SystemExit(f"unknown config {cfg}")
+
+
+def q_ro(n, nnz, k):
+    return 12 * nnz + 4 * (n + 1) + 8 * n * (k + 1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed loop runs."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, device=0):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(a_rp, a_col, a_val, level_ptr, x_perm, k, reps=3, budget_s=30.0):
+    """Reference CPU MPK (lb_lg_p2p walker restated in C) on the host cores."""
+    from oracle import cpu as C
+
+    threads = C.threads()
+    n = a_rp.shape[0] - 1
+    nnz = int(a_rp[-1])
+    # the reference's cache parameter: host LLC-ish 32 MiB default (cli.py:380-384)
+    plan = C.CpuPlan(a_rp, a_col, level_ptr, k, 32 * 2**20, workers=threads, variant="lb_lg_p2p")
+    y = np.zeros((k + 1, n))
+    y[0] = x_perm
+    C.mpk_walk(a_rp, a_col, a_val, y, plan)  # warm (thread pool, pages)
+    ts = []
+    t_begin = time.perf_counter()
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        C.mpk_walk(a_rp, a_col, a_val, y, plan)
+        ts.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_begin > budget_s:
+            break
+    yb = np.zeros((k + 1, n))
+    yb[0] = x_perm
+    C.mpk_baseline(a_rp, a_col, a_val, yb, k, threads)
+    tb = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        C.mpk_baseline(a_rp, a_col, a_val, yb, k, threads)
+        tb.append(time.perf_counter() - t0)
+    t = min(ts)
+    return {
+        "value": 2.0 * nnz * k / t / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+        "sample": f"full workload, {len(ts)} timed lb_lg_p2p calls (min), C=32 MiB, W={threads}",
+        "seconds_min": t, "seconds_mean": sum(ts) / len(ts),
+        "baseline_kspmv_gflops": 2.0 * nnz * k / min(tb) / 1e9,
+        "bitwise_vs_baseline": bool(np.array_equal(y, yb)),
+    }, y
+
+
+def run_reference(args, cfgd):
+    """--impl reference: the reference's CPU MPK on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import cpu as C
+    from oracle import levelmpk_oracle as O
+
+    k = cfgd["k"]
+    t0 = time.perf_counter()
+    rp, col, val = O.gen_stencil_3d(cfgd["n"], 2)
+    perm, lp = C.bfs_levels(rp, col, 0)
+    arp, acol, aval = C.permute_symmetric(rp, col, val, perm)
+    n, nnz = arp.shape[0] - 1, int(arp[-1])
+    x = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+    threads = C.threads()
+    plan = C.CpuPlan(arp, acol, lp, k, 32 * 2**20, workers=threads, variant="lb_lg_p2p")
+    prep = time.perf_counter() - t0
+    y = np.zeros((k + 1, n))
+    y[0] = x[perm]
+    for _ in range(args.warmup):
+        C.mpk_walk(arp, acol, aval, y, plan)
+    ts = []
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        C.mpk_walk(arp, acol, aval, y, plan)
+        ts.append(time.perf_counter() - t1)
+    t = sum(ts) / len(ts)
+    value = 2.0 * nnz * k / t / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": cfgd["name"], "n_rows": n, "nnz": nnz, "k": k,
+                   "variant": "lb_lg_p2p", "cache_bytes": 32 * 2**20, "workers": threads,
+                   "inputs_exceed_l2": True},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} timed calls of the full workload (C restatement "
+                                   f"of the reference p2p walker, oracle/mpk_oracle.c)"},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "preprocess_seconds": prep,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfgd):
+    import torch
+
+    import paper_2205_01598_b200 as lm
+    from paper_2205_01598_b200 import _lib
+    from paper_2205_01598_b200 import kernels as K
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    k = cfgd["k"]
+    t0 = time.perf_counter()
+    a = lm.gen_stencil_3d(cfgd["n"], 2)
+    t_gen = time.perf_counter() - t0
+    n, nnz = a.n_rows, a.n_nz
+    x = np.random.default_rng(0).uniform(-1.0, 1.0, n)
+    # ---------------- preprocessing (GPU): BFS levels, permutation, groups, plan, tiling
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pre = lm.prepare(a, "lb_lg_p2p", k, 126e6)
+    plan = lm.build_plan(pre, "lb_lg_p2p", 1)
+    tparams = {}
+    if args.mode == "res":
+        tparams["mode_flags"] = _lib.FLAG_MODE_RESIDENT
+    elif args.mode == "stream":
+        tparams["mode_flags"] = _lib.FLAG_MODE_STREAM
+    if args.slots:
+        tparams["slots"] = args.slots
+    if args.tile_nnz:
+        tparams["tile_nnz"] = args.tile_nnz
+    til = plan.tiling(**tparams) if tparams else plan.tiling()
+    torch.cuda.synchronize()
+    t_pre = time.perf_counter() - t0
+    perm_d = pre.perm.device()[0]
+    cfg = plan.power_config()
+    ctx = _lib.context()
+    xd = torch.from_numpy(x).cuda()
+    y = torch.zeros((k + 1, n), dtype=torch.float64, device="cuda")
+    K.permute_vectors(perm_d, xd.unsqueeze(0), y[0:1])
+    y0 = y[0].clone()
+    # ---------------- device-resident timed loop
+    for _ in range(args.warmup):
+        K.mpk_run(til, y, cfg, check_errors=False)
+    K.mpk_run(til, y, cfg)  # also surfaces watchdog errors
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        e0.record()
+        for s in range(args.steps):
+            step_ev[s][0].record()
+            K.mpk_run(til, y, cfg, check_errors=False)
+            step_ev[s][1].record()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = ctx.launches() - launches0
+    _lib.check(ctx.lib.lmpk_ctx_check(ctx.handle, _lib.stream_handle()), "bench")
+    t_total = e0.elapsed_time(e1) * 1e-3
+    if world > 1:
+        tt = torch.tensor([t_total], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_total = float(tt.item())
+    per_launch = [a_.elapsed_time(b_) * 1e-3 for a_, b_ in step_ev]
+    t_step = t_total / args.steps
+    t_kernel = sum(per_launch) / len(per_launch)
+    flops = 2.0 * nnz * k
+    value = flops * world / t_step / 1e9
+    # ---------------- parity spot check of the timed result vs a fresh baseline
+    yb = torch.zeros_like(y)
+    yb[0] = y0
+    K.mpk_baseline(pre.a.device(), yb, k)
+    bitwise = bool(torch.equal(yb, y))
+    # ---------------- k x SpMV comparators on the same GPU
+    def ev(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        b0 = torch.cuda.Event(enable_timing=True)
+        b1 = torch.cuda.Event(enable_timing=True)
+        b0.record()
+        for _ in range(reps):
+            fn()
+        b1.record()
+        b1.synchronize()
+        return b0.elapsed_time(b1) * 1e-3 / reps
+
+    t_crs = ev(lambda: K.mpk_baseline(pre.a.device(), yb, k))
+    t_sweep = ev(lambda: K.mpk_run(til, yb, cfg, flags=_lib.FLAG_SWEEP, check_errors=False))
+    # ---------------- end to end through the public API surface with host buffers
+    hx = torch.from_numpy(x[pre.perm.perm].copy()).pin_memory()
+    hy = torch.empty((k, n), dtype=torch.float64).pin_memory()
+    ye = torch.zeros_like(y)
+    for _ in range(2):
+        ye[0].copy_(hx, non_blocking=True)
+        K.mpk_run(til, ye, cfg, check_errors=False)
+        hy.copy_(ye[1:], non_blocking=True)
+    torch.cuda.synchronize()
+    c0 = torch.cuda.Event(enable_timing=True)
+    c1 = torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for _ in range(args.steps):
+        ye[0].copy_(hx, non_blocking=True)
+        K.mpk_run(til, ye, cfg, check_errors=False)
+        hy.copy_(ye[1:], non_blocking=True)
+    c1.record()
+    c1.synchronize()
+    t_e2e = c0.elapsed_time(c1) * 1e-3 / args.steps
+    # preprocessing cost in SpMV equivalents (cli.py:157-159)
+    peak, peak_kind = measured_hbm_peak()
+    Q = q_ro(n, nnz, k)
+    achieved = Q / t_kernel / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfgd["name"], "n_rows": n, "nnz": nnz, "k": k,
+                   "mode": til.mode, "tiles": til.info["n_tiles"],
+                   "tile_nnz_cap": til.info["tile_nnz_cap"], "slots": tparams.get("slots"),
+                   "inputs_exceed_l2": True, "parallelism": "replicas" if world > 1 else "single"},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": Q},
+        "e2e": {"value": flops * world / t_e2e / 1e9, "unit": "GFLOP/s",
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n * k},
+        "gpu_launches": launches,
+        "bitwise_vs_baseline": bitwise,
+        "kspmv_baseline": {"crs_ms": t_crs * 1e3, "tiled_sweep_ms": t_sweep * 1e3,
+                           "speedup_vs_best": min(t_crs, t_sweep) / t_kernel},
+        "preprocess": {"seconds": t_pre, "spmv_equivalents": t_pre / (t_crs / k),
+                       "generate_seconds": t_gen},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            a_rp = pre.a.row_ptr
+            cb, _ = cpu_baseline(a_rp, pre.a.col, pre.a.val, pre.levels.level_ptr,
+                                 x[pre.perm.perm], k)
+            line["cpu_baseline"] = cb
+        except Exception as e:  # keep the GPU line even if the host leg fails
+            line["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--mode", choices=("auto", "res", "stream"), default="stream")
+    ap.add_argument("--slots", type=int, default=2)
+    ap.add_argument("--tile-nnz", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfgd = workload(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfgd)
+    else:
+        run_ours(args, cfgd)
+
+
+if __name__ == "__main__":
+    main()

@@ -57,6 +57,9 @@ extern "C" {
 #define LMPK_FLAG_MODE_STREAM 0x10  /* force streaming (L2) wavefront mode       */
 #define LMPK_FLAG_MODE_RESIDENT 0x20/* force SMEM-resident wavefront mode       */
 #define LMPK_FLAG_NO_TMA 0x40       /* stage tiles with plain loads, not TMA     */
+#define LMPK_FLAG_SWEEP 0x80        /* lmpk_mpk_run: n_powers dependency-free   */
+                                    /* sweeps (k back-to-back SpMVs) on the     */
+                                    /* same tiles -- the blocking-free baseline */
 
 #define LMPK_MAX_POWERS 64
 
@@ -110,15 +113,27 @@ typedef struct lmpk_tiling_info {
   int32_t max_fwd_reach; /* max over tiles of (dep_hi - t)                      */
   int32_t chain_reach;   /* max (p_m-1)-step forward dependency chain, in tiles */
   int32_t max_row_nnz;
+  int32_t queue_slack;   /* streaming: extra key spacing M - D between powers  */
   int64_t nnz;
+  int64_t block_bytes;   /* size of the tile-SELL-32 copy of the matrix         */
 } lmpk_tiling_info;
 
-/* Build the tiling for an n-row matrix already resident on the device.
- * tile_nnz_hint <= 0 lets the library choose; mode_flags may force a mode.
+/* Tuning knobs of lmpk_tiling_create (0 = library default). */
+typedef struct lmpk_tiling_params {
+  int32_t tile_nnz_hint; /* cap a tile block near this many nonzeros            */
+  int32_t ctas_per_sm;   /* co-resident CTAs per SM                             */
+  int32_t threads;       /* threads per CTA (multiple of 32, <= 512)            */
+  int32_t queue_slack;   /* streaming: key spacing M - D (tiles)                */
+  int32_t mode_flags;    /* LMPK_FLAG_MODE_STREAM / LMPK_FLAG_MODE_RESIDENT     */
+  int32_t slots;         /* streaming: smem ring slots per CTA (<= 8)           */
+} lmpk_tiling_params;
+
+/* Build the tiling for an n-row matrix already resident on the device and
+ * re-lay the matrix out as tile-SELL-32 blocks (a copy owned by the tiling).
  * Synchronizes `stream` (small D2H of tile geometry). */
 int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
-                       int32_t p_m, int32_t tile_nnz_hint, int32_t ctas_per_sm_hint,
-                       int mode_flags, lmpk_tiling** out, lmpk_tiling_info* info, void* stream);
+                       const double* val, int32_t p_m, const lmpk_tiling_params* params,
+                       lmpk_tiling** out, lmpk_tiling_info* info, void* stream);
 int lmpk_tiling_destroy(lmpk_tiling* t);
 /* Copy tile geometry to host arrays: tile_row[n_tiles+1], dep_lo/dep_hi[n_tiles]. */
 int lmpk_tiling_geometry(const lmpk_tiling* t, int32_t* tile_row, int32_t* dep_lo,
@@ -140,8 +155,7 @@ typedef struct lmpk_power_cfg {
  * Replaces run_plan / _run_numba / _walk (executor.py:84-230).  y holds
  * n_slots slots of stride ldy (in doubles); acc (length n, or 2n complex)
  * is accumulated in place when use_acc != 0 (cheb.py:229,240). */
-int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* tiling, const int32_t* row_ptr,
-                 const int32_t* col, const double* val, double* y, int64_t ldy, int32_t n_slots,
+int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* tiling, double* y, int64_t ldy, int32_t n_slots,
                  const lmpk_power_cfg* cfg, double* acc, int use_acc, int flags, void* stream);
 
 /* Synchronize `stream` and report a device-side failure of the last MPK
@@ -187,6 +201,13 @@ int lmpk_permute_vectors(lmpk_ctx* ctx, int32_t n, const int32_t* perm, const do
  * (groups.py:257-262 _level_nnz on the permuted matrix). */
 int lmpk_level_nnz(lmpk_ctx* ctx, const int32_t* row_ptr, const int64_t* level_ptr,
                    int64_t n_levels, int64_t* out, void* stream);
+
+/* Column range of row segments [seg_ptr[g], seg_ptr[g+1]): out_min[g] / out_max[g]
+ * = smallest / largest column index (INT32_MAX / -1 for empty segments).
+ * Feeds the point-to-point checks of plan.py:322-370 for whole level groups. */
+int lmpk_segment_col_range(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col,
+                           int64_t n_seg, const int64_t* seg_ptr, int32_t* out_min,
+                           int32_t* out_max, void* stream);
 
 #ifdef __cplusplus
 }

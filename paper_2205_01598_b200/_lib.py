@@ -30,6 +30,7 @@ FLAG_COMPLEX = 0x1
 FLAG_MODE_STREAM = 0x10
 FLAG_MODE_RESIDENT = 0x20
 FLAG_NO_TMA = 0x40
+FLAG_SWEEP = 0x80
 
 MAX_POWERS = 64
 
@@ -46,11 +47,16 @@ class TilingInfo(ctypes.Structure):
         ("n_tiles", _i32), ("p_m", _i32), ("mode", _i32), ("grid", _i32),
         ("block", _i32), ("smem_bytes", _i32), ("tile_nnz_cap", _i32),
         ("max_fwd_reach", _i32), ("chain_reach", _i32), ("max_row_nnz", _i32),
-        ("nnz", _i64),
+        ("queue_slack", _i32), ("nnz", _i64), ("block_bytes", _i64),
     ]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+class TilingParams(ctypes.Structure):
+    _fields_ = [("tile_nnz_hint", _i32), ("ctas_per_sm", _i32), ("threads", _i32),
+                ("queue_slack", _i32), ("mode_flags", _i32), ("slots", _i32)]
 
 
 class PowerCfg(ctypes.Structure):
@@ -76,18 +82,19 @@ SIGNATURES = {
     "lmpk_ctx_check": (_int, [_vp, _vp]),
     "lmpk_spmv_rows": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _int, _vp]),
     "lmpk_mpk_baseline": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _int, _vp]),
-    "lmpk_tiling_create": (_int, [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _int,
+    "lmpk_tiling_create": (_int, [_vp, _i32, _vp, _vp, _vp, _i32, ctypes.POINTER(TilingParams),
                                   ctypes.POINTER(_vp), ctypes.POINTER(TilingInfo), _vp]),
     "lmpk_tiling_destroy": (_int, [_vp]),
     "lmpk_tiling_geometry": (_int, [_vp, _vp, _vp, _vp]),
-    "lmpk_mpk_run": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32,
-                            ctypes.POINTER(PowerCfg), _vp, _int, _int, _vp]),
+    "lmpk_mpk_run": (_int, [_vp, _vp, _vp, _i64, _i32, ctypes.POINTER(PowerCfg), _vp, _int,
+                            _int, _vp]),
     "lmpk_bfs_levels": (_int, [_vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _i64p, _vp]),
     "lmpk_symmetrized_pattern": (_int, [_vp, _i32, _vp, _vp, ctypes.POINTER(_int), _i64p,
                                         _vp, _vp, _i64, _vp]),
     "lmpk_permute_symmetric": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lmpk_permute_vectors": (_int, [_vp, _i32, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _int, _vp]),
     "lmpk_level_nnz": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    "lmpk_segment_col_range": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     # micro-benchmarks (not part of the reference-facing ABI)
     "lmpk_probe_read_bw": (_int, [_vp, _i64, _int, _int, ctypes.POINTER(ctypes.c_double)]),
     "lmpk_probe_flag_latency": (_int, [_vp, _int, ctypes.POINTER(ctypes.c_double)]),

@@ -74,17 +74,23 @@ struct lmpk_ctx {
   uint64_t queue_base = 0;        // host mirror of the counter value
 };
 
+// Tile geometry + the matrix re-laid out as tile-SELL-32 blocks (see mpk.cu).
 struct lmpk_tiling {
   lmpk_ctx* ctx = nullptr;
   lmpk_tiling_info info{};
   int32_t n = 0;
-  int32_t* d_tile_row = nullptr;  // [n_tiles+1]
-  int32_t* d_dep_lo = nullptr;    // [n_tiles]
-  int32_t* d_dep_hi = nullptr;    // [n_tiles]
-  int32_t* d_items = nullptr;     // streaming-mode item order, packed t*128+p
-  uint32_t* d_progress = nullptr; // [n_tiles] epoch-tagged power counters
+  int32_t* d_tile_row = nullptr;   // [n_tiles+1] first row of each tile (multiples of 32)
+  int64_t* d_tile_ofs = nullptr;   // [n_tiles+1] byte offset of each tile block
+  int32_t* d_tile_E = nullptr;     // [n_tiles] padded entries (multiple of 32) per tile
+  int32_t* d_dep_lo = nullptr;     // [n_tiles]
+  int32_t* d_dep_hi = nullptr;     // [n_tiles]
+  int32_t* d_items = nullptr;      // streaming-mode item order, packed t*128+p
+  uint32_t* d_progress = nullptr;  // [n_tiles] epoch-tagged power counters
+  unsigned char* d_blocks = nullptr;  // tile-SELL-32 matrix blocks
+  int64_t block_bytes = 0;
+  int32_t max_block = 0;           // largest tile block (bytes)
+  int32_t slots = 1;               // pipelined kernel ring slots
   std::vector<int32_t> h_tile_row, h_dep_lo, h_dep_hi;
-  int32_t rows_cap = 0;
 };
 
 namespace lmpk {
@@ -111,11 +117,38 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acqrel_cta_smem(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"(smem_u32(p)), "r"(v)
+               : "memory");
+  return old;
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)

@@ -257,3 +257,53 @@ extern "C" int lmpk_permute_vectors(lmpk_ctx* ctx, int32_t n, const int32_t* per
   launch_count_add(ctx, 1);
   return LMPK_OK;
 }
+
+namespace lmpk {
+// one CTA per row segment: min of first columns, max of last columns
+__global__ void k_segment_col_range(const int32_t* row_ptr, const int32_t* col, int64_t n_seg,
+                                    const int64_t* seg_ptr, int32_t* out_min, int32_t* out_max) {
+  __shared__ int32_t s_mn[32], s_mx[32];
+  for (int64_t g = blockIdx.x; g < n_seg; g += gridDim.x) {
+    int32_t mn = INT32_MAX, mx = -1;
+    for (int64_t r = seg_ptr[g] + threadIdx.x; r < seg_ptr[g + 1]; r += blockDim.x) {
+      const int32_t a = row_ptr[r], b = row_ptr[r + 1];
+      if (b > a) {
+        mn = min(mn, col[a]);
+        mx = max(mx, col[b - 1]);
+      }
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+      s_mn[threadIdx.x >> 5] = mn;
+      s_mx[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int nw = blockDim.x >> 5;
+      mn = threadIdx.x < nw ? s_mn[threadIdx.x] : INT32_MAX;
+      mx = threadIdx.x < nw ? s_mx[threadIdx.x] : -1;
+      mn = __reduce_min_sync(0xffffffffu, mn);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if (threadIdx.x == 0) {
+        out_min[g] = mn;
+        out_max[g] = mx;
+      }
+    }
+    __syncthreads();
+  }
+}
+}  // namespace lmpk
+
+extern "C" int lmpk_segment_col_range(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col,
+                                      int64_t n_seg, const int64_t* seg_ptr, int32_t* out_min,
+                                      int32_t* out_max, void* stream) {
+  LMPK_ARG_CHECK(ctx && row_ptr && col && seg_ptr && out_min && out_max,
+                 "lmpk_segment_col_range: NULL argument");
+  if (n_seg <= 0) return LMPK_OK;
+  const int g = int(std::min<int64_t>(n_seg, int64_t(ctx->sm_count) * 8));
+  k_segment_col_range<<<g, 256, 0, as_stream(stream)>>>(row_ptr, col, n_seg, seg_ptr, out_min, out_max);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 1);
+  return LMPK_OK;
+}

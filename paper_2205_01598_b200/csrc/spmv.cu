@@ -91,7 +91,7 @@ __device__ __forceinline__ bool stage_tile(const SpmvArgs& a, const TileBuf& b, 
   return true;
 }
 
-__global__ void __launch_bounds__(256) spmv_tiles_kernel(SpmvArgs a) {
+__global__ void __launch_bounds__(512, 2) spmv_tiles_kernel(SpmvArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bars[2];
   TileBuf buf[2];
@@ -161,13 +161,13 @@ static int spmv_launch(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const i
                        const double* val, const double* x, double* out, int32_t r0, int32_t r1,
                        int64_t nz_base, int64_t nnz, int flags, cudaStream_t st) {
   if (r1 <= r0) return LMPK_OK;
-  const int threads = 256;
+  const int threads = 512;
   const int64_t rows = r1 - r0;
   const double avg = rows > 0 ? double(nnz) / double(rows) : 1.0;
-  // ~2 rows per thread per tile, bounded so three CTAs fit one SM
-  int32_t tile = static_cast<int32_t>(std::min<double>(std::max<double>(avg * 2 * threads, 512.0), 6144.0));
+  // ~1 row per thread per tile; rows longer than the slack run from global
+  int32_t tile = static_cast<int32_t>(std::min<double>(std::max<double>(avg * threads, 512.0), 4096.0));
   tile &= ~3;
-  int32_t cap = tile * 2;
+  int32_t cap = tile + 256;
   const size_t col_bytes = ((size_t(cap) + 8) * 4 + 15) & ~size_t(15);
   const size_t val_bytes = ((size_t(cap) + 4) * 8 + 15) & ~size_t(15);
   const size_t per = ((col_bytes + val_bytes) + 127) & ~size_t(127);

@@ -1,0 +1,253 @@
+"""MPK execution on the B200 (run_plan / run_baseline / run_mpk).
+
+Mirrors pkg/src/levelmpk/executor.py: PowerVectors (executor.py:33-53),
+MpkResult (executor.py:56-66), undo_permutation (executor.py:69-76),
+run_plan (executor.py:213-230), build_baseline_plan / run_baseline
+(executor.py:233-266), prepare / run_mpk (executor.py:269-298), warmup
+(executor.py:301-306).
+
+Execution goes through liblmpk only:
+
+* level-blocked variants (lb, lb_lg, lb_lg_p2p, lb_lg_p2p_rec) run the
+  persistent level-blocked kernel (lmpk_mpk_run) over the plan's tiling;
+* ``baseline`` plans run p_m back-to-back CRS SpMV launches
+  (lmpk_mpk_baseline), the blocking-free comparator.
+
+Every variant computes each row with the reference's per-row summation, so
+power vectors are bitwise identical across variants AND bitwise identical
+to the reference's numba backend.  ``PowerVectors`` may hold host (numpy)
+or device (torch CUDA) storage; host storage is staged through HBM.
+``MpkResult.seconds`` is the device time of the kernel launches (CUDA
+events); ``e2e_seconds`` adds the host<->device copies of a host call.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+
+from . import _lib
+from . import kernels as K
+from .csr import CsrMatrix, Permutation
+from .groups import Preprocessed, preprocess
+from .plan import VARIANTS, ExecPlan, FlatItem, _validate_coverage, build_plan
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+class PowerVectors:
+    """The p_max + 1 dense vectors y_0..y_{p_max}, each contiguous.
+
+    y_0 is the caller-supplied input and is never written by kernels.
+    ``data`` is a numpy array (host) or, with ``device=True``, a CUDA tensor.
+    """
+
+    def __init__(self, n_rows, p_max, n_slots=None, data=None, device=False, dtype=np.float64):
+        self.n_rows = n_rows
+        self.p_max = p_max
+        slots = n_slots if n_slots is not None else p_max + 1
+        if data is not None:
+            assert tuple(data.shape) == (slots, n_rows)
+            self.data = data
+        elif device:
+            torch = _torch()
+            tdt = torch.complex128 if np.dtype(dtype) == np.complex128 else torch.float64
+            self.data = torch.zeros((slots, n_rows), dtype=tdt, device="cuda")
+        else:
+            self.data = np.zeros((slots, n_rows), dtype=dtype)
+
+    @property
+    def on_device(self) -> bool:
+        return not isinstance(self.data, np.ndarray)
+
+    def vec(self, p):
+        return self.data[p]
+
+    def __getitem__(self, p):
+        return self.data[p]
+
+    def to_host(self) -> "PowerVectors":
+        if not self.on_device:
+            return self
+        return PowerVectors(self.n_rows, self.p_max, n_slots=self.data.shape[0],
+                            data=self.data.cpu().numpy())
+
+
+class MpkResult:
+    def __init__(self, y, seconds, variant, workers, plan=None, e2e_seconds=None):
+        self.y = y
+        self.seconds = seconds
+        self.e2e_seconds = seconds if e2e_seconds is None else e2e_seconds
+        self.variant = variant
+        self.workers = workers
+        self.plan = plan
+        self.barrier_count = plan.barrier_count() if plan is not None else 0
+
+    def gflops(self, n_nz, p_m) -> float:
+        return 2.0 * n_nz * p_m / self.seconds / 1e9
+
+
+def undo_permutation(result, perm: Permutation) -> PowerVectors:
+    """Bring power vectors computed in permuted order back to the original."""
+    y = result.y if isinstance(result, MpkResult) else result
+    if perm.n != y.n_rows:
+        raise ValueError(f"permutation length {perm.n} != vector length {y.n_rows}")
+    if y.on_device:
+        out = PowerVectors(y.n_rows, y.p_max, n_slots=y.data.shape[0], device=True,
+                           dtype=np.complex128 if y.data.is_complex() else np.float64)
+        K.permute_vectors(perm.device()[0], y.data, out.data, scatter=True)
+        return out
+    out = PowerVectors(y.n_rows, y.p_max, n_slots=y.data.shape[0], dtype=y.data.dtype)
+    out.data[:, perm.perm] = y.data
+    return out
+
+
+def _to_device_f64(arr):
+    torch = _torch()
+    if isinstance(arr, torch.Tensor):
+        return arr
+    return torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+
+
+def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
+    """Run one plan on device buffers; returns device seconds."""
+    torch = _torch()
+    cplx = yd.is_complex()
+    yv = torch.view_as_real(yd).reshape(yd.shape[0], -1) if cplx else yd
+    av = None
+    if use_acc:
+        av = torch.view_as_real(accd).reshape(-1) if accd.is_complex() else accd
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if plan.variant == "baseline":
+        if cplx or use_acc or np.any(plan.kernel != 0):
+            # baseline plans with Chebyshev slots: tiled dependency-free sweeps
+            cfg = plan.power_config()
+            K.mpk_run(plan.tiling(), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx,
+                      flags=flags | _lib.FLAG_SWEEP)
+        else:
+            K.mpk_baseline(plan.a.device(), yv, plan.p_m)
+    else:
+        cfg = plan.power_config()
+        K.mpk_run(plan.tiling(), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=flags)
+    e1.record()
+    e1.synchronize()
+    ctx = _lib.context()
+    _lib.check(ctx.lib.lmpk_ctx_check(ctx.handle, _lib.stream_handle()), "run_plan")
+    return e0.elapsed_time(e1) * 1e-3
+
+
+def run_plan(plan: ExecPlan, x=None, y=None, acc=None, use_acc=False, timeout=None):
+    """Execute a plan on the GPU; returns an MpkResult with the power vectors.
+
+    Semantics of executor.py:213-230: with ``y=None`` a PowerVectors is
+    allocated and y[0] = x; otherwise ``y`` (host or device) is updated in
+    place.  ``acc`` (with use_acc) is accumulated in place.  The device
+    watchdog (8 s without progress) replaces the reference's join timeout.
+    """
+    del timeout  # device-side watchdog
+    torch = _torch()
+    t_start = time.perf_counter()
+    n = plan.n_rows
+    if y is None:
+        if x is None:
+            raise ValueError("either x or y must be given")
+        xa = x if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64)
+        on_dev = isinstance(xa, torch.Tensor)
+        dt = np.complex128 if (on_dev and xa.is_complex()) or (not on_dev and np.iscomplexobj(xa)) else np.float64
+        pv = PowerVectors(n, plan.p_m, device=on_dev, dtype=dt)
+        pv.data[0] = xa
+    else:
+        pv = y
+    if pv.on_device:
+        yd = pv.data
+    else:
+        yd = _to_device_f64(pv.data)
+    accd = None
+    if use_acc:
+        if acc is None:
+            raise ValueError("use_acc requires acc")
+        accd = acc if isinstance(acc, torch.Tensor) else _to_device_f64(acc)
+    seconds = _launch(plan, yd, accd, use_acc)
+    if not pv.on_device:
+        pv.data[...] = yd.cpu().numpy()
+    if use_acc and not isinstance(acc, torch.Tensor):
+        acc[...] = accd.cpu().numpy()
+    e2e = time.perf_counter() - t_start
+    return MpkResult(pv, seconds, plan.variant, plan.workers, plan, e2e_seconds=e2e)
+
+
+def build_baseline_plan(a: CsrMatrix, p_m: int, workers: int) -> ExecPlan:
+    """p_m full-range SpMV sweeps with a barrier between sweeps (executor.py:233-258)."""
+    from .plan import _nnz_balanced_chunks
+
+    n = a.n_rows
+    items = [FlatItem(0, n, p, 0, "group", 0, label=("baseline",)) for p in range(1, p_m + 1)]
+    _validate_coverage(items, n, p_m)
+    row_start = np.zeros(p_m, dtype=np.int64)
+    row_end = np.full(p_m, n, dtype=np.int64)
+    power = np.arange(1, p_m + 1, dtype=np.int64)
+    chunks = np.empty((p_m, workers + 1), dtype=np.int64)
+    if workers == 1:
+        chunks[:] = (0, n)
+    else:
+        chunks[:] = _nnz_balanced_chunks(a.row_ptr, 0, n, workers)
+    return ExecPlan(
+        variant="baseline", p_m=p_m, workers=workers, n_rows=n, items=items,
+        barrier=True, row_start=row_start, row_end=row_end, power=power,
+        chunks=chunks, bnd_point=chunks[:, :-1].copy(),
+        check_ptr=np.zeros(p_m + 1, dtype=np.int64),
+        check_item=np.empty(0, dtype=np.int64),
+        check_kind=np.empty(0, dtype=np.int64),
+        a=a, pre=None, schedule=None,
+        out_slot=power.copy(), in_slot=power - 1,
+        prev_slot=np.maximum(power - 2, 0),
+        kernel=np.zeros(p_m, dtype=np.int64),
+        acc_coef=np.zeros(p_m, dtype=np.float64),
+    )
+
+
+def run_baseline(a: CsrMatrix, x, p_m: int, workers: int = 1, timeout=None) -> MpkResult:
+    """Baseline MPK: y_p = A y_{p-1} as p_m full sweeps (k back-to-back SpMVs)."""
+    if tuple(np.shape(x)) != (a.n_rows,):
+        raise ValueError("x length must equal n_rows")
+    plan = build_baseline_plan(a, p_m, workers)
+    return run_plan(plan, x=x, timeout=timeout)
+
+
+def prepare(a: CsrMatrix, variant: str, p_m: int, cache_bytes: float,
+            f: float = 0.5, s_m: int = 0, root: int = 0) -> Preprocessed:
+    """Preprocess with the grouping implied by the variant (executor.py:269-282)."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    if variant == "lb":
+        return preprocess(a, p_m, max(cache_bytes, 1.0), f, s_m=0, root=root, grouping="levels")
+    eff_sm = s_m if variant == "lb_lg_p2p_rec" else 0
+    return preprocess(a, p_m, cache_bytes, f, s_m=eff_sm, root=root)
+
+
+def run_mpk(a: CsrMatrix, x, variant: str, p_m: int, cache_bytes: float,
+            f: float = 0.5, s_m: int = 0, workers: int = 1, root: int = 0,
+            timeout=None):
+    """Preprocess, execute; returns (result in permuted order, pre) (executor.py:285-298)."""
+    if variant == "baseline":
+        return run_baseline(a, x, p_m, workers, timeout=timeout), None
+    pre = prepare(a, variant, p_m, cache_bytes, f, s_m, root)
+    plan = build_plan(pre, variant, workers)
+    x_perm = pre.perm.apply_to_vector(np.asarray(x, dtype=np.float64))
+    return run_plan(plan, x=x_perm, timeout=timeout), pre
+
+
+def warmup():
+    """Load the library, create the context and touch every kernel once."""
+    from .stencils import gen_stencil_2d7pt
+
+    a = gen_stencil_2d7pt(4, 4)
+    run_baseline(a, np.ones(a.n_rows), p_m=1, workers=1)
+    run_mpk(a, np.ones(a.n_rows), "lb_lg_p2p", 2, 10_000)

@@ -67,15 +67,19 @@ def mpk_baseline(a: DeviceCsr, y, p_m, flags=0, stream=None):
 class Tiling:
     """Tile geometry of one device matrix for the level-blocked kernel."""
 
-    def __init__(self, a: DeviceCsr, p_m, tile_nnz=0, ctas_per_sm=0, mode_flags=0, stream=None):
+    def __init__(self, a: DeviceCsr, p_m, tile_nnz=0, ctas_per_sm=0, mode_flags=0, threads=0,
+                 queue_slack=0, slots=0, stream=None):
         self.ctx = context()
         self.a = a
+        self.p_m = int(p_m)
         h = ctypes.c_void_p()
         info = _lib.TilingInfo()
+        prm = _lib.TilingParams(int(tile_nnz), int(ctas_per_sm), int(threads), int(queue_slack),
+                                int(mode_flags), int(slots))
         check(self.ctx.lib.lmpk_tiling_create(
-            self.ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), int(p_m), int(tile_nnz),
-            int(ctas_per_sm), int(mode_flags), ctypes.byref(h), ctypes.byref(info),
-            stream_handle(stream)), "tiling_create")
+            self.ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val), int(p_m),
+            ctypes.byref(prm), ctypes.byref(h), ctypes.byref(info), stream_handle(stream)),
+            "tiling_create")
         self.handle = h
         self.info = info.as_dict()
 
@@ -131,11 +135,10 @@ def mpk_run(tiling: Tiling, y, cfg, acc=None, use_acc=False, complex_state=False
     """Level-blocked MPK over the slots of y (torch float64, [n_slots, n] or
     [n_slots, 2n] for complex state viewed as float64)."""
     ctx = tiling.ctx
-    a = tiling.a
     f = int(flags) | (_lib.FLAG_COMPLEX if complex_state else 0)
-    check(ctx.lib.lmpk_mpk_run(ctx.handle, tiling.handle, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
-                               ptr(y), int(y.stride(0)), int(y.shape[0]), ctypes.byref(cfg),
-                               ptr(acc), 1 if use_acc else 0, f, stream_handle(stream)), "mpk_run")
+    check(ctx.lib.lmpk_mpk_run(ctx.handle, tiling.handle, ptr(y), int(y.stride(0)), int(y.shape[0]),
+                               ctypes.byref(cfg), ptr(acc), 1 if use_acc else 0, f,
+                               stream_handle(stream)), "mpk_run")
     if check_errors:
         check(ctx.lib.lmpk_ctx_check(ctx.handle, stream_handle(stream)), "mpk_run")
 
@@ -219,6 +222,21 @@ def level_nnz(a: DeviceCsr, level_ptr, stream=None):
     check(ctx.lib.lmpk_level_nnz(ctx.handle, ptr(a.row_ptr), ptr(lp), L, ptr(out),
                                  stream_handle(stream)), "level_nnz")
     return out[:L].cpu().numpy()
+
+
+def segment_col_range(a: DeviceCsr, seg_ptr, stream=None):
+    """(min col, max col) per row segment [seg_ptr[g], seg_ptr[g+1]) as numpy arrays."""
+    torch = _torch()
+    ctx = context()
+    dev = a.row_ptr.device
+    sp = torch.as_tensor(np.ascontiguousarray(seg_ptr, dtype=np.int64), device=dev)
+    G = int(sp.shape[0] - 1)
+    mn = torch.empty(max(G, 1), dtype=torch.int32, device=dev)
+    mx = torch.empty(max(G, 1), dtype=torch.int32, device=dev)
+    check(ctx.lib.lmpk_segment_col_range(ctx.handle, ptr(a.row_ptr), ptr(a.col), G, ptr(sp),
+                                         ptr(mn), ptr(mx), stream_handle(stream)),
+          "segment_col_range")
+    return mn[:G].cpu().numpy(), mx[:G].cpu().numpy()
 
 
 def probe_read_bw(nbytes, reps=10, trials=5):

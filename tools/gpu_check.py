@@ -19,10 +19,10 @@ def ev_time(fn, reps=10, warm=3):
 out = {}
 ctx = K.context()
 print("device", torch.cuda.get_device_name(), "SMs", ctx.sm_count, "smem/blk", ctx.max_smem_block, "smem/sm", ctx.max_smem_sm, "L2", ctx.l2_bytes)
-for mb in (8, 32, 64, 96):
+for mb in ([] if os.environ.get("NOPROBE") else (8, 32, 64, 96)):
     g = K.probe_read_bw(mb << 20, reps=50, trials=5); out[f"read_bw_{mb}MB"] = g; print(f"read bw {mb} MB: {g:.0f} GB/s")
-g = K.probe_read_bw(4 << 30, reps=1, trials=5); out["read_bw_4GB"] = g; print(f"read bw 4 GB: {g:.0f} GB/s")
-lat = K.probe_flag_latency(20000); out["flag_one_way_ns"] = lat; print(f"flag one-way latency {lat:.0f} ns")
+g = 0 if os.environ.get("NOPROBE") else K.probe_read_bw(4 << 30, reps=1, trials=5); out["read_bw_4GB"] = g; print(f"read bw 4 GB: {g:.0f} GB/s")
+lat = 0 if os.environ.get("NOPROBE") else K.probe_flag_latency(20000); out["flag_one_way_ns"] = lat; print(f"flag one-way latency {lat:.0f} ns")
 
 def check_matrix(name, rp, c, v, p_m=8, root=0):
     n = rp.shape[0] - 1
@@ -43,6 +43,9 @@ def check_matrix(name, rp, c, v, p_m=8, root=0):
     for mode, fl in (("resident", _lib.FLAG_MODE_RESIDENT), ("streaming", _lib.FLAG_MODE_STREAM)):
         try:
             t = K.Tiling(b, p_m, mode_flags=fl)
+            y3 = torch.zeros_like(y); y3[0] = y[0]
+            K.mpk_run(t, y3, K.mpk_power_cfg(p_m), flags=_lib.FLAG_SWEEP)
+            res[mode + "_sweep"] = bool(np.array_equal(y3.cpu().numpy(), ref))
             y2 = torch.zeros_like(y); y2[0] = y[0]
             K.mpk_run(t, y2, K.mpk_power_cfg(p_m))
             res[mode] = bool(np.array_equal(y2.cpu().numpy(), ref))
@@ -78,19 +81,24 @@ print(f"baseline k=8: {tmin:.3f} ms min {tmean:.3f} mean; {F/tmin/1e6:.0f} GF/s"
 out["cfg2_baseline_ms"] = tmin
 yb = y.clone()
 results = []
-for fl, tile, cps in [(_lib.FLAG_MODE_RESIDENT, 0, 0), (_lib.FLAG_MODE_RESIDENT, 0, 1), (_lib.FLAG_MODE_RESIDENT, 0, 3),
-                      (_lib.FLAG_MODE_RESIDENT, 4000, 2), (_lib.FLAG_MODE_RESIDENT, 6000, 2), (_lib.FLAG_MODE_RESIDENT, 3000, 3),
-                      (_lib.FLAG_MODE_STREAM, 0, 0), (_lib.FLAG_MODE_STREAM, 4096, 4), (_lib.FLAG_MODE_STREAM, 8192, 2), (_lib.FLAG_MODE_STREAM, 2048, 6)]:
+configs = [(_lib.FLAG_MODE_RESIDENT, 0, 0, 0, 0, 0), (_lib.FLAG_MODE_RESIDENT, 0, 0, 0, 0, 3), (_lib.FLAG_MODE_RESIDENT, 0, 0, 0, 0, 4),
+           (_lib.FLAG_MODE_RESIDENT, 0, 0, 0, 0, 6), (_lib.FLAG_MODE_RESIDENT, 0, 0, 0, 0, 8),
+           (_lib.FLAG_MODE_STREAM, 0, 0, 0, 0, 3), (_lib.FLAG_MODE_STREAM, 0, 0, 0, 0, 2),
+           ("sweep", 0, 0, 0, 0, 2), ("sweep", 0, 0, 0, 0, 3)]
+for fl, tile, cps, thr, slack, slots in configs:
     try:
-        t = K.Tiling(b, k, tile_nnz=tile, ctas_per_sm=cps, mode_flags=fl)
+        sweep = fl == "sweep"
+        t = K.Tiling(b, k, tile_nnz=tile, ctas_per_sm=cps, threads=thr, queue_slack=slack, slots=slots,
+                     mode_flags=_lib.FLAG_MODE_STREAM if sweep else fl)
         cfg = K.mpk_power_cfg(k)
         y2 = torch.zeros_like(y); y2[0] = x
         def run():
-            K.mpk_run(t, y2, cfg, check_errors=False)
+            K.mpk_run(t, y2, cfg, check_errors=False, flags=_lib.FLAG_SWEEP if sweep else 0)
         tmin, tmean = ev_time(run, reps=10)
-        K.mpk_run(t, y2, cfg)
+        K.mpk_run(t, y2, cfg, flags=_lib.FLAG_SWEEP if sweep else 0)
         same = bool(torch.equal(y2, yb))
-        r = dict(mode=t.mode, tile=t.info["tile_nnz_cap"], ctas=t.info["grid"] // ctx.sm_count, n_tiles=t.info["n_tiles"],
+        r = dict(mode="sweep" if sweep else t.mode, tile=t.info["tile_nnz_cap"], ctas=t.info["grid"] // ctx.sm_count,
+                 threads=t.info["block"], slack=t.info["queue_slack"], slots=slots, n_tiles=t.info["n_tiles"],
                  chain=t.info["chain_reach"], fwd=t.info["max_fwd_reach"], ms_min=tmin, ms_mean=tmean,
                  gflops=F / tmin / 1e6, ro_frac=Q_ro / (tmin * 1e-3) / 6531.6e9, bitwise=same)
     except Exception as e:
