@@ -23,11 +23,15 @@
  *     layer maps LMPK_ERR_ARG to ValueError and everything else to
  *     RuntimeError, mirroring the reference's exception contract
  *     (SURVEY.md section 8b "Errors").
- *   - Summation semantics (bit-exact mode, the default): every output row is
- *     tmp = 0.0; for k in row order: tmp = tmp + val[k]*x[col[k]] with
- *     separately rounded multiply and add (no FMA contraction), exactly the
- *     numba kernel csr.py:195-201 / executor.py:127-135.  Results are bitwise
- *     identical to the reference's numba backend on the same permuted matrix.
+ *   - Summation semantics.  Every output row is
+ *       tmp = 0.0; for k in row order: tmp = tmp + val[k]*x[col[k]]
+ *     (the numba kernel csr.py:195-201 / executor.py:127-135).  With
+ *     LMPK_FLAG_EXACT the multiply and add are separately rounded (no FMA
+ *     contraction): results are bitwise identical to the reference's numba
+ *     backend on the same permuted matrix.  Without it the same ordered chain
+ *     uses fused multiply-adds (one fp64 op per nonzero instead of two); the
+ *     per-power relative L2 error stays far below the 1e-12 the MPK contract
+ *     allows.  lmpk_spmv_rows / lmpk_mpk_baseline are always exact.
  */
 #ifndef LMPK_H
 #define LMPK_H
@@ -56,10 +60,14 @@ extern "C" {
 #define LMPK_FLAG_COMPLEX 0x1       /* vectors are complex128 (interleaved)      */
 #define LMPK_FLAG_MODE_STREAM 0x10  /* force streaming (L2) wavefront mode       */
 #define LMPK_FLAG_MODE_RESIDENT 0x20/* force SMEM-resident wavefront mode       */
-#define LMPK_FLAG_NO_TMA 0x40       /* stage tiles with plain loads, not TMA     */
+#define LMPK_FLAG_NO_TMA 0x40       /* read tile blocks from global memory (no   */
+                                    /* shared-memory staging)                   */
 #define LMPK_FLAG_SWEEP 0x80        /* lmpk_mpk_run: n_powers dependency-free   */
                                     /* sweeps (k back-to-back SpMVs) on the     */
                                     /* same tiles -- the blocking-free baseline */
+#define LMPK_FLAG_EXACT 0x400       /* bit-exact row sums (see Summation below) */
+/* bits 8-9 (0x100, 0x200): L2 eviction policy of staged blocks that a later
+ * power group re-reads: 0 evict_last, 1 evict_normal, 2/3 evict_first.      */
 
 #define LMPK_MAX_POWERS 64
 
@@ -77,6 +85,9 @@ int lmpk_ctx_create(lmpk_ctx** out, int device);
 int lmpk_ctx_destroy(lmpk_ctx* ctx);
 /* Number of kernel launches this ctx issued since creation (for gpu_launches). */
 int64_t lmpk_ctx_launch_count(const lmpk_ctx* ctx);
+/* Phase counters of the pipelined MPK kernels, collected only when the
+ * environment variable LMPK_PROFILE is set at ctx creation (16 words). */
+int lmpk_ctx_profile(lmpk_ctx* ctx, unsigned long long* out, int reset);
 
 /* ---------------------------------------------------------------- SpMV
  * out[r] = sum_k val[k]*x[col[k]] for r in [r0, r1); other rows untouched.
@@ -105,7 +116,7 @@ int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const in
 typedef struct lmpk_tiling_info {
   int32_t n_tiles;
   int32_t p_m;
-  int32_t mode;          /* 1 = SMEM-resident, 2 = streaming (L2)               */
+  int32_t mode;          /* 1 = SMEM-resident (q = p_m), 2 = grouped streaming  */
   int32_t grid;          /* CTAs launched                                       */
   int32_t block;         /* threads per CTA                                     */
   int32_t smem_bytes;    /* dynamic shared memory per CTA                       */
@@ -113,19 +124,23 @@ typedef struct lmpk_tiling_info {
   int32_t max_fwd_reach; /* max over tiles of (dep_hi - t)                      */
   int32_t chain_reach;   /* max (p_m-1)-step forward dependency chain, in tiles */
   int32_t max_row_nnz;
-  int32_t queue_slack;   /* streaming: extra key spacing M - D between powers  */
+  int32_t queue_slack;   /* key spacing M - q*D between power groups           */
   int64_t nnz;
   int64_t block_bytes;   /* size of the tile-SELL-32 copy of the matrix         */
+  int32_t powers_per_item; /* q: powers computed per staged tile block          */
+  int32_t slots;         /* R: staged items held per CTA                        */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */
 typedef struct lmpk_tiling_params {
   int32_t tile_nnz_hint; /* cap a tile block near this many nonzeros            */
-  int32_t ctas_per_sm;   /* co-resident CTAs per SM                             */
-  int32_t threads;       /* threads per CTA (multiple of 32, <= 512)            */
+  int32_t ctas_per_sm;   /* reserved (one CTA per SM)                           */
+  int32_t threads;       /* reserved (1 producer + LMPK_NC consumer warps)      */
   int32_t queue_slack;   /* streaming: key spacing M - D (tiles)                */
   int32_t mode_flags;    /* LMPK_FLAG_MODE_STREAM / LMPK_FLAG_MODE_RESIDENT     */
-  int32_t slots;         /* streaming: smem ring slots per CTA (<= 8)           */
+  int32_t slots;         /* staged items held per CTA (<= 4)                    */
+  int32_t powers_per_item; /* q: powers per staged tile (0 = plan; MODE_RESIDENT */
+                           /* forces q = p_m, MODE_STREAM defaults to q = 1)   */
 } lmpk_tiling_params;
 
 /* Build the tiling for an n-row matrix already resident on the device and

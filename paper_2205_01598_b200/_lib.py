@@ -31,6 +31,7 @@ FLAG_MODE_STREAM = 0x10
 FLAG_MODE_RESIDENT = 0x20
 FLAG_NO_TMA = 0x40
 FLAG_SWEEP = 0x80
+FLAG_EXACT = 0x400
 
 MAX_POWERS = 64
 
@@ -48,6 +49,7 @@ class TilingInfo(ctypes.Structure):
         ("block", _i32), ("smem_bytes", _i32), ("tile_nnz_cap", _i32),
         ("max_fwd_reach", _i32), ("chain_reach", _i32), ("max_row_nnz", _i32),
         ("queue_slack", _i32), ("nnz", _i64), ("block_bytes", _i64),
+        ("powers_per_item", _i32), ("slots", _i32),
     ]
 
     def as_dict(self):
@@ -56,7 +58,8 @@ class TilingInfo(ctypes.Structure):
 
 class TilingParams(ctypes.Structure):
     _fields_ = [("tile_nnz_hint", _i32), ("ctas_per_sm", _i32), ("threads", _i32),
-                ("queue_slack", _i32), ("mode_flags", _i32), ("slots", _i32)]
+                ("queue_slack", _i32), ("mode_flags", _i32), ("slots", _i32),
+                ("powers_per_item", _i32)]
 
 
 class PowerCfg(ctypes.Structure):
@@ -80,6 +83,7 @@ SIGNATURES = {
     "lmpk_ctx_destroy": (_int, [_vp]),
     "lmpk_ctx_launch_count": (_i64, [_vp]),
     "lmpk_ctx_check": (_int, [_vp, _vp]),
+    "lmpk_ctx_profile": (_int, [_vp, _vp, _int]),
     "lmpk_spmv_rows": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _int, _vp]),
     "lmpk_mpk_baseline": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _int, _vp]),
     "lmpk_tiling_create": (_int, [_vp, _i32, _vp, _vp, _vp, _i32, ctypes.POINTER(TilingParams),

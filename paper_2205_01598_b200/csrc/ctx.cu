@@ -1,5 +1,6 @@
 // ctx.cu -- error reporting, per-device context, scratch pools.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -113,6 +114,10 @@ extern "C" int lmpk_ctx_create(lmpk_ctx** out, int device) {
     }
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->queue_ctr, 64);
+  if (e == cudaSuccess && getenv("LMPK_PROFILE") != nullptr) {
+    e = cudaMalloc(&c->prof, 16 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->prof, 0, 16 * sizeof(unsigned long long));
+  }
   if (e == cudaSuccess) e = cudaMemset(c->queue_ctr, 0, 64);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -131,9 +136,26 @@ extern "C" int lmpk_ctx_destroy(lmpk_ctx* c) {
                       &c->s_d,     &c->s_e, &c->s_f, &c->s_g};
   for (Scratch* s : pools) s->release();
   if (c->queue_ctr) cudaFree(c->queue_ctr);
+  if (c->prof) cudaFree(c->prof);
   if (c->err.host) cudaFreeHost(const_cast<int*>(c->err.host));
   delete c;
   return LMPK_OK;
 }
 
 extern "C" int64_t lmpk_ctx_launch_count(const lmpk_ctx* c) { return c ? c->launches : 0; }
+
+// Phase counters of the pipelined kernels (LMPK_PROFILE=1 at ctx creation):
+// [0] consumer ns waiting for work, [1] consumer ns computing, [2] items
+// consumed (per warp), [3] producer dependency polls, [4] polls with nothing
+// ready, [5] producer ns alive, [6] items issued.  reset != 0 zeroes them.
+extern "C" int lmpk_ctx_profile(lmpk_ctx* c, unsigned long long* out, int reset) {
+  LMPK_ARG_CHECK(c && out, "lmpk_ctx_profile: NULL argument");
+  if (!c->prof) {
+    memset(out, 0, 16 * sizeof(unsigned long long));
+    return LMPK_OK;
+  }
+  LMPK_CHECK_CUDA(cudaDeviceSynchronize());
+  LMPK_CHECK_CUDA(cudaMemcpy(out, c->prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  if (reset) LMPK_CHECK_CUDA(cudaMemset(c->prof, 0, 16 * sizeof(unsigned long long)));
+  return LMPK_OK;
+}

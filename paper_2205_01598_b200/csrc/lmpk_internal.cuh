@@ -72,6 +72,7 @@ struct lmpk_ctx {
   lmpk::Scratch s_small, s_a, s_b, s_c, s_d, s_e, s_f, s_g;
   uint64_t* queue_ctr = nullptr;  // monotone work-queue counter (device)
   uint64_t queue_base = 0;        // host mirror of the counter value
+  unsigned long long* prof = nullptr;  // phase counters when LMPK_PROFILE is set
 };
 
 // Tile geometry + the matrix re-laid out as tile-SELL-32 blocks (see mpk.cu).
@@ -84,12 +85,13 @@ struct lmpk_tiling {
   int32_t* d_tile_E = nullptr;     // [n_tiles] padded entries (multiple of 32) per tile
   int32_t* d_dep_lo = nullptr;     // [n_tiles]
   int32_t* d_dep_hi = nullptr;     // [n_tiles]
-  int32_t* d_items = nullptr;      // streaming-mode item order, packed t*128+p
+  int32_t* d_items = nullptr;      // item queue order, packed (t << 8) | power group
+  int32_t n_items = 0;
   uint32_t* d_progress = nullptr;  // [n_tiles] epoch-tagged power counters
   unsigned char* d_blocks = nullptr;  // tile-SELL-32 matrix blocks
   int64_t block_bytes = 0;
   int32_t max_block = 0;           // largest tile block (bytes)
-  int32_t slots = 1;               // pipelined kernel ring slots
+  int32_t slots = 1;               // staged items held per CTA
   std::vector<int32_t> h_tile_row, h_dep_lo, h_dep_hi;
 };
 
@@ -206,6 +208,111 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+// Coherent global load of a gathered operand (non-volatile so the scheduler
+// may batch it; its address depends on data read after the acquire points).
+__device__ __forceinline__ double ldg_f64(const char* p) {
+  double v;
+  asm("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s32(uint32_t a) {
+  int32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// Readers of one staged tile block, by byte offset.  SmemBlk reads a block
+// staged in shared memory (volatile so nothing is hoisted above the mbarrier
+// wait that publishes the TMA bytes); GlbBlk reads the block straight from
+// global memory (immutable for the whole launch, so the .nc path is safe).
+struct SmemBlk {
+  uint32_t a;
+  __device__ __forceinline__ int32_t i1(uint32_t o) const {
+    int32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ int2 i2(uint32_t o) const {
+    int2 v;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ int4 i4(uint32_t o) const {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ double d1(uint32_t o) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ double2 d2(uint32_t o) const {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ uint32_t u16(uint32_t o) const {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a + o));
+    return v;
+  }
+};
+struct GlbBlk {
+  const unsigned char* a;
+  // streamed once per power: keep it out of L1 (the gathers own the L1)
+  __device__ __forceinline__ int32_t i1(uint32_t o) const {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ int2 i2(uint32_t o) const {
+    int2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ int4 i4(uint32_t o) const {
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ double d1(uint32_t o) const {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ double2 d2(uint32_t o) const {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ uint32_t u16(uint32_t o) const {
+    uint16_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(a + o));
+    return v;
+  }
+};
+__device__ __forceinline__ double2 ldg_f64x2(const char* p) {
+  double2 v;
+  asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

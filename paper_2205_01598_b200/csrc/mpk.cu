@@ -6,37 +6,43 @@
 //
 //   * the level-permuted matrix is cut into contiguous row TILES (multiples
 //     of 32 rows) sized to the shared-memory budget and re-laid out once as
-//     "tile-SELL-32" blocks: per 32-row slice the entries are stored
-//     column-major (entry j of row i at slice_base + 32*j + i), padded to the
-//     slice's longest row.  One contiguous block per tile -> ONE TMA bulk
-//     copy stages it; warps read it conflict-free; each row is still summed
-//     in its CRS storage order (padding is predicated away), so results stay
-//     bitwise identical to the reference;
+//     "tile-SELL-32" blocks.  Per 32-row slice of width w (its longest row)
+//     the entries are stored in CHUNKS of 4, 2 and 1 entries (w = 4Q + 2P + S):
+//     inside a chunk of c entries, lane i's c entries are contiguous, so one
+//     LDS.128 fetches four column indices and two LDS.128 four values; the
+//     warp reads each chunk as one conflict-free contiguous row of smem.
+//     Each row is still summed in CRS storage order (padding is skipped), so
+//     the bit-exact mode reproduces the reference bitwise;
 //   * tile t's dependency range [dep_lo(t), dep_hi(t)] is the set of tiles
 //     owning its column indices (level confinement, Eq. 4 of the paper,
 //     keeps it narrow: a tile couples only to its own and adjacent levels);
-//   * a persistent grid of CTAs replaces the reference's W threads.  Each
-//     (tile, power) node publishes an epoch-tagged counter with a gpu-scope
-//     release after its rows are stored; a consumer polls its dependency
-//     range with relaxed loads and then issues an acquire fence (which also
-//     invalidates the SM's L1 so later gathers see fresh vector data).  This
-//     is the device form of conditions (A)/(B)/(C): "tile t at power p only
-//     after tiles dep_lo..dep_hi finished p-1" (schedule.py:195-240);
-//   * RESIDENT mode (cooperative launch): a CTA grabs the next tile in order,
-//     stages its block into shared memory ONCE and computes all p_m powers on
-//     it -> the matrix is read from HBM once.  Deadlock freedom: the chain
-//     reach of the p_m-1 dependency steps must be smaller than the number of
-//     co-resident CTAs (checked at planning time);
-//   * STREAMING mode: CTAs grab (tile, power) items from a queue ordered by
-//     the skewed diagonal key (t + p*M, p), M = D + slack, D = max forward
-//     reach -- topologically valid for any M >= D; the slack keeps dependent
-//     items ~2 grids apart so the queue is never a serial chain.  The block
-//     is re-staged per power (served from L2 inside the diagonal window: the
-//     reference's cache blocking with the 126 MB L2 as the cache).
-//     Deadlock-free without co-residency;
-//   * SWEEP (LMPK_FLAG_SWEEP): n_powers dependency-free passes, one launch per
-//     power -- the blocking-free "k back-to-back SpMVs" baseline on the same
-//     tiles and the same row kernel.
+//   * WORK ITEMS are (tile t, power group g): the powers gq+1 .. gq+q of one
+//     tile, computed on ONE staged copy of the tile block (q = powers per
+//     item).  Items are queued by the skewed diagonal key (t + g*M, g),
+//     M = q*D + slack (D = max forward reach), which is topologically valid
+//     and keeps the items of one key window inside the 126 MB L2: the block
+//     is read from HBM once and re-staged from L2 once per group, i.e. the
+//     matrix crosses the L2->SM path ceil(p_m/q) times instead of p_m times.
+//     q = p_m is the fully SMEM-resident walk (one group), q = 1 the pure
+//     streaming walk;
+//   * a persistent grid (one CTA per SM: 1 producer warp + NC consumer warps)
+//     holds R items in R shared-memory slots.  The producer grabs items in
+//     queue order (one atomic ticket each), stages the block with one TMA
+//     bulk copy, and polls the dependencies of every held item WITHOUT
+//     blocking on any one of them (one batch of relaxed loads per round, then
+//     one fence.acq_rel.gpu: acquire + L1 invalidation).  A ready (slot, p)
+//     goes into a small smem work ring; consumer warps drain the ring with no
+//     CTA-wide barrier, and the last warp to finish a (tile, power) publishes
+//     the tile's epoch-tagged progress word with a gpu-scope release -- the
+//     device form of conditions (A)/(B)/(C) (schedule.py:195-240).
+//     Deadlock freedom: items are grabbed in queue order, so the oldest
+//     unfinished item X always progresses if every item it transitively waits
+//     on inside its group is held: at most G*(chain_q + 1) queue positions
+//     after X (G groups per key, chain_q = (q-1)-step forward chain reach),
+//     checked against grid*R when the tiling is planned;
+//   * SWEEP (LMPK_FLAG_SWEEP): n_powers dependency-free passes, one launch
+//     per power -- the blocking-free "k back-to-back SpMVs" baseline on the
+//     same tiles and the same row kernel.
 #include <string.h>
 
 #include <algorithm>
@@ -48,8 +54,13 @@ namespace lmpk {
 
 constexpr uint32_t kEpochStride = 128;  // > LMPK_MAX_POWERS
 constexpr unsigned long long kWatchdogNs = 8ull * 1000 * 1000 * 1000;
-constexpr int kMaxThreads = 512;
-constexpr bool kPairSlices = false;  // measured slower on cfg2 (load imbalance per item)
+constexpr int kMaxSlots = 4;
+constexpr int kWorkRing = 8;
+#ifndef LMPK_NC
+#define LMPK_NC 24
+#endif
+constexpr int kConsumers = LMPK_NC;  // consumer warps per CTA (+1 producer warp)
+constexpr int kBlockThreads = 32 * (kConsumers + 1);
 
 struct PowerCfgDev {
   int32_t out_slot[LMPK_MAX_POWERS];
@@ -67,7 +78,7 @@ struct MpkParams {
   const int32_t* tile_row;
   const int32_t* dep_lo;
   const int32_t* dep_hi;
-  const int32_t* items;
+  const int32_t* items;  // packed (t << 8) | g in queue order (NULL: item i = tile i, g = 0)
   double* y;
   int64_t ldy;
   double* acc;
@@ -76,14 +87,15 @@ struct MpkParams {
   unsigned long long* queue;  // [0] work counter, [1] abort flag
   unsigned long long queue_base;
   uint32_t epoch_base;
-  int32_t n_tiles;
   int32_t n_items;
   int32_t n_powers;
-  int32_t mode;      // 1 resident, 2 streaming, 3 sweep (one power, no deps)
-  int32_t smem_cap;  // bytes of one staging buffer
-  int32_t n_slots;   // pipelined kernel: ring slots
-  int32_t use_tma;
+  int32_t q;         // powers per item
+  int32_t mode;      // 1 group walk, 3 sweep (one power, no deps)
+  int32_t smem_cap;  // bytes of one slot
+  int32_t n_slots;   // R
+  int32_t flags;     // LMPK_FLAG_* (NO_TMA, policy bits 8-9)
   int* err;          // host-mapped
+  unsigned long long* prof;  // optional phase counters (LMPK_PROFILE), else null
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -94,539 +106,318 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __host__ __device__ inline int64_t align16(int64_t b) { return (b + 15) & ~int64_t(15); }
 
-// Block layout of a tile with ns slices and E padded entries:
-//   [slice_off int32 x ns4][lens uint16 x 32*ns] | align16 | [col int32 x E][val f64 x E]
-__host__ __device__ inline int64_t blk_col_off(int32_t ns) {
-  const int32_t ns4 = (ns + 3) & ~3;
-  return align16(int64_t(ns4) * 4 + int64_t(ns) * 64);
-}
+// Block layout of a tile with ns slices and E entries (E = 32 * sum of widths):
+//   [rec int2 x ns] [lens uint16 x 32*ns] | align16 | [col int32 x E] [val f64 x E]
+// rec[s] = {byte offset of slice s's first column index in the block,
+//           w | wmin << 16} (w = longest row, wmin = shortest row).
+__host__ __device__ inline int64_t blk_col_off(int32_t ns) { return align16(int64_t(ns) * 72); }
 __host__ __device__ inline int64_t blk_bytes(int32_t ns, int64_t E) {
   return (blk_col_off(ns) + E * 12 + 127) & ~int64_t(127);
 }
 
-// Stage tile block [ofs, ofs+bytes) into smem with one bulk copy.  Thread 0
-// arms the mbarrier (exactly one phase per call).  Returns false if the block
-// does not fit -- the tile is then computed straight from global memory.
-__device__ __forceinline__ bool stage_block(const MpkParams& P, unsigned char* buf, uint64_t* bar,
-                                            int64_t ofs, int64_t bytes, uint64_t policy) {
-  if (bytes > P.smem_cap) {
-    if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, 0);
-    return false;
-  }
-  if (P.use_tma) {
-    if (threadIdx.x == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(bar, uint32_t(bytes));
-      bulk_g2s(buf, P.blocks + ofs, uint32_t(bytes), bar, policy);
-    }
+// Entry index of (lane, j) inside a slice of width w starting at entry `base`:
+// quads first, then a pair, then a single entry.
+__host__ __device__ inline int64_t chunk_entry(int64_t base, int w, int lane, int j) {
+  const int Q = w >> 2;
+  if (j < 4 * Q) return base + int64_t(j >> 2) * 128 + lane * 4 + (j & 3);
+  const int r = j - 4 * Q;
+  if ((w & 2) && r < 2) return base + int64_t(Q) * 128 + lane * 2 + r;
+  return base + int64_t(Q) * 128 + ((w & 2) ? 64 : 0) + lane;
+}
+
+// ---------------------------------------------------------------- row kernel
+// Per-power operands, built once per launch in shared memory (the consumers
+// would otherwise re-derive them from the constant bank for every item).
+struct PowTab {
+  const char* yin;    // gathered vector y_{p-1}
+  double* yout;       // y_p
+  const double* ypv;  // y_{p-2} slot (Chebyshev)
+  double cre, cim;    // acc coefficient
+  int32_t general;    // Chebyshev step and/or accumulation
+  int32_t cheb;
+};
+
+template <bool EXACT>
+__device__ __forceinline__ double madd(double t, double v, double x) {
+  if constexpr (EXACT)
+    return __dadd_rn(t, __dmul_rn(v, x));  // tmp = tmp + v*x, separately rounded
+  else
+    return __fma_rn(v, x, t);
+}
+// t = madd(t, v, x) only for entries j < len (the row's own length): one
+// ISETP + predicated DFMA (or DMUL/DADD) instead of a select chain.
+template <bool EXACT>
+__device__ __forceinline__ void madd_if(double& t, double v, double x, int j, int len) {
+  if constexpr (EXACT) {
+    const double m = __dmul_rn(v, x);  // harmless for padding: only the add is predicated
+    asm("{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %2, %3;\n\t@q add.rn.f64 %0, %0, %1;\n\t}"
+        : "+d"(t)
+        : "d"(m), "r"(j), "r"(len));
   } else {
-    const int4* src = reinterpret_cast<const int4*>(P.blocks + ofs);
-    int4* dst = reinterpret_cast<int4*>(buf);
-    for (int64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-    if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, 0);
+    asm("{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %3, %4;\n\t@q fma.rn.f64 %0, %1, %2, %0;\n\t}"
+        : "+d"(t)
+        : "d"(v), "d"(x), "r"(j), "r"(len));
   }
-  return true;
+}
+__device__ __forceinline__ void stg_f64(double* p, double v) {
+  asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+__device__ __forceinline__ void stg_f64x2(double* p, double2 v) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y));
 }
 
-// Warp 0 waits until every tile in [lo, hi] published >= target.  Returns
-// false (and raises the abort flag) when the watchdog expires.
-__device__ __forceinline__ bool mpk_wait(const MpkParams& P, int32_t lo, int32_t hi,
-                                         uint32_t target) {
-  bool ok = true;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    unsigned long long t0 = 0;
-    for (int32_t i = lo + lane; i <= hi; i += 32) {
-      int spins = 0;
-      while (ld_relaxed_u32(P.progress + i) < target) {
-        if (++spins > 4) __nanosleep(32);
-        if ((spins & 255) == 0) {
-          if (t0 == 0) t0 = globaltimer();
-          const volatile unsigned long long* ab = P.queue + 1;
-          if (*ab != 0ull) {
-            ok = false;
-            break;
-          }
-          if (globaltimer() - t0 > kWatchdogNs) {
-            atomicExch(P.queue + 1, 1ull);
-            *P.err = 1;
-            ok = false;
-            break;
-          }
-        }
-      }
-      if (!ok) break;
-    }
-    ok = __all_sync(0xffffffffu, ok);
-    fence_acq_rel_gpu();  // acquire: order + invalidate L1 before the gathers
+// Row sum of one slice of compile-time width W <= 8 (real vectors): all column
+// loads, then all gathers, then the values and the ordered chain.  cb/vb are
+// the slice's column/value byte offsets in the block, l4 = 4*lane.
+template <int W, bool EXACT, bool FULL, class Blk>
+__device__ __forceinline__ double slice_real_w(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
+                                               const char* ybase, int len) {
+  constexpr int Q = W >> 2, PR = (W >> 1) & 1, SG = W & 1;
+  int32_t c[W];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int4 c4 = B.i4(cb + q * 512 + 4 * l4);
+    c[4 * q] = c4.x;
+    c[4 * q + 1] = c4.y;
+    c[4 * q + 2] = c4.z;
+    c[4 * q + 3] = c4.w;
   }
-  return ok;
+  if constexpr (PR) {
+    const int2 c2 = B.i2(cb + Q * 512 + 2 * l4);
+    c[4 * Q] = c2.x;
+    c[4 * Q + 1] = c2.y;
+  }
+  if constexpr (SG) c[W - 1] = B.i1(cb + Q * 512 + PR * 256 + l4);
+  double x[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) x[j] = ldg_f64(ybase + uint64_t(uint32_t(c[j])) * 8u);
+  double v[W];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double2 a = B.d2(vb + q * 1024 + 8 * l4), b = B.d2(vb + q * 1024 + 8 * l4 + 16);
+    v[4 * q] = a.x;
+    v[4 * q + 1] = a.y;
+    v[4 * q + 2] = b.x;
+    v[4 * q + 3] = b.y;
+  }
+  if constexpr (PR) {
+    const double2 a = B.d2(vb + Q * 1024 + 4 * l4);
+    v[4 * Q] = a.x;
+    v[4 * Q + 1] = a.y;
+  }
+  if constexpr (SG) v[W - 1] = B.d1(vb + Q * 1024 + PR * 512 + 2 * l4);
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    if constexpr (FULL)
+      t = madd<EXACT>(t, v[j], x[j]);
+    else
+      madd_if<EXACT>(t, v[j], x[j], j, len);
+  }
+  return t;
 }
 
-// One power step over a staged (or global) tile block: warps stride over the
-// 32-row slices, lane = row.  Entries j of the slice's rows are consecutive
-// in the block, so col/val reads are conflict-free 128/256-byte rows.
-template <bool CPLX>
-__device__ __forceinline__ void tile_power(const MpkParams& P, const PowerCfgDev& C,
-                                           const unsigned char* blk, int32_t r0, int32_t r1,
-                                           int32_t E, int p, int wid, int nwarps) {
-  const int pi = p - 1;
-  const int kern = C.kernel[pi];
-  const double cre = C.coef_re[pi], cim = C.coef_im[pi];
-  const int32_t ns = (r1 - r0 + 31) >> 5;
-  const int32_t* soff = reinterpret_cast<const int32_t*>(blk);
-  const uint16_t* lens = reinterpret_cast<const uint16_t*>(blk + ((ns + 3) & ~3) * 4);
-  const int64_t co = blk_col_off(ns);
-  const int32_t* cols = reinterpret_cast<const int32_t*>(blk + co);
-  const double* vals = reinterpret_cast<const double*>(blk + co + int64_t(E) * 4);
-  const double* yin = P.y + int64_t(C.in_slot[pi]) * P.ldy;
-  const double* ypv = P.y + int64_t(C.prev_slot[pi]) * P.ldy;
-  double* yout = P.y + int64_t(C.out_slot[pi]) * P.ldy;
+// Any width (real vectors): a loop over quads plus the pair/single tail.
+template <bool EXACT, class Blk>
+__device__ __noinline__ double slice_real_any(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
+                                              const char* ybase, int w, int len) {
+  const int Q = w >> 2;
+  double t = 0.0;
+  for (int q = 0; q < Q; ++q) {
+    const int4 c4 = B.i4(cb + q * 512 + 4 * l4);
+    const double x0 = ldg_f64(ybase + uint64_t(uint32_t(c4.x)) * 8u);
+    const double x1 = ldg_f64(ybase + uint64_t(uint32_t(c4.y)) * 8u);
+    const double x2 = ldg_f64(ybase + uint64_t(uint32_t(c4.z)) * 8u);
+    const double x3 = ldg_f64(ybase + uint64_t(uint32_t(c4.w)) * 8u);
+    const double2 a = B.d2(vb + q * 1024 + 8 * l4), b = B.d2(vb + q * 1024 + 8 * l4 + 16);
+    const int j = 4 * q;
+    madd_if<EXACT>(t, a.x, x0, j, len);
+    madd_if<EXACT>(t, a.y, x1, j + 1, len);
+    madd_if<EXACT>(t, b.x, x2, j + 2, len);
+    madd_if<EXACT>(t, b.y, x3, j + 3, len);
+  }
+  const int PR = (w >> 1) & 1;
+  if (PR) {
+    const int2 c2 = B.i2(cb + Q * 512 + 2 * l4);
+    const double x0 = ldg_f64(ybase + uint64_t(uint32_t(c2.x)) * 8u);
+    const double x1 = ldg_f64(ybase + uint64_t(uint32_t(c2.y)) * 8u);
+    const double2 a = B.d2(vb + Q * 1024 + 4 * l4);
+    madd_if<EXACT>(t, a.x, x0, 4 * Q, len);
+    madd_if<EXACT>(t, a.y, x1, 4 * Q + 1, len);
+  }
+  if (w & 1) {
+    const int32_t c = B.i1(cb + Q * 512 + PR * 256 + l4);
+    const double x0 = ldg_f64(ybase + uint64_t(uint32_t(c)) * 8u);
+    const double a = B.d1(vb + Q * 1024 + PR * 512 + 2 * l4);
+    madd_if<EXACT>(t, a, x0, w - 1, len);
+  }
+  return t;
+}
+
+// Complex vectors (real matrix): t += v * x per component, storage order.
+template <bool EXACT, class Blk>
+__device__ __forceinline__ double2 slice_cplx(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
+                                              const char* ybase, int w, int len) {
+  double tr = 0.0, ti = 0.0;
+  const int Q = w >> 2;
+  for (int q = 0; q < Q; ++q) {
+    const int4 c4 = B.i4(cb + q * 512 + 4 * l4);
+    const double2 x0 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.x)) * 16u);
+    const double2 x1 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.y)) * 16u);
+    const double2 x2 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.z)) * 16u);
+    const double2 x3 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.w)) * 16u);
+    const double2 a = B.d2(vb + q * 1024 + 8 * l4), b = B.d2(vb + q * 1024 + 8 * l4 + 16);
+    const int j = 4 * q;
+    madd_if<EXACT>(tr, a.x, x0.x, j, len);
+    madd_if<EXACT>(ti, a.x, x0.y, j, len);
+    madd_if<EXACT>(tr, a.y, x1.x, j + 1, len);
+    madd_if<EXACT>(ti, a.y, x1.y, j + 1, len);
+    madd_if<EXACT>(tr, b.x, x2.x, j + 2, len);
+    madd_if<EXACT>(ti, b.x, x2.y, j + 2, len);
+    madd_if<EXACT>(tr, b.y, x3.x, j + 3, len);
+    madd_if<EXACT>(ti, b.y, x3.y, j + 3, len);
+  }
+  const int PR = (w >> 1) & 1;
+  if (PR) {
+    const int2 c2 = B.i2(cb + Q * 512 + 2 * l4);
+    const double2 x0 = ldg_f64x2(ybase + uint64_t(uint32_t(c2.x)) * 16u);
+    const double2 x1 = ldg_f64x2(ybase + uint64_t(uint32_t(c2.y)) * 16u);
+    const double2 a = B.d2(vb + Q * 1024 + 4 * l4);
+    madd_if<EXACT>(tr, a.x, x0.x, 4 * Q, len);
+    madd_if<EXACT>(ti, a.x, x0.y, 4 * Q, len);
+    madd_if<EXACT>(tr, a.y, x1.x, 4 * Q + 1, len);
+    madd_if<EXACT>(ti, a.y, x1.y, 4 * Q + 1, len);
+  }
+  if (w & 1) {
+    const int32_t c = B.i1(cb + Q * 512 + PR * 256 + l4);
+    const double2 x0 = ldg_f64x2(ybase + uint64_t(uint32_t(c)) * 16u);
+    const double a = B.d1(vb + Q * 1024 + PR * 512 + 2 * l4);
+    madd_if<EXACT>(tr, a, x0.x, w - 1, len);
+    madd_if<EXACT>(ti, a, x0.y, w - 1, len);
+  }
+  return make_double2(tr, ti);
+}
+
+template <bool EXACT, bool FULL, class Blk>
+__device__ __forceinline__ double slice_real(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
+                                             const char* ybase, int w, int len) {
+  switch (w) {
+    case 1: return slice_real_w<1, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 2: return slice_real_w<2, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 3: return slice_real_w<3, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 4: return slice_real_w<4, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 5: return slice_real_w<5, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 6: return slice_real_w<6, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 7: return slice_real_w<7, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 8: return slice_real_w<8, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 0: return 0.0;
+    default: return slice_real_any<EXACT>(B, cb, vb, l4, ybase, w, FULL ? w : len);
+  }
+}
+
+// One power step of one tile (rows r0 .. r0+nrows-1, E block entries): warps
+// stride over the 32-row slices, lane = row.  GENERAL adds the Chebyshev
+// three-term step and the accumulation; plain SpMV powers skip both.
+template <bool CPLX, bool EXACT, bool GENERAL, class Blk>
+__device__ __forceinline__ void tile_power(const PowTab& pt, double* acc_base, bool use_acc, const Blk& B,
+                                           int32_t r0, int32_t nrows, uint32_t E, int wid, int nwarps) {
+  const int32_t ns = (nrows + 31) >> 5;
+  const uint32_t lens_o = uint32_t(ns) * 8;
+  const uint32_t col_o = uint32_t(blk_col_off(ns));
+  const uint32_t vdelta = col_o + E * 4 - 2 * col_o;  // vb = 2*cb + vdelta
   const int lane = threadIdx.x & 31;
-  if constexpr (!CPLX && kPairSlices) {
-    // Real vectors: a warp advances TWO slices (s, s + nwarps) at a time so
-    // twice as many independent gathers are in flight per lane; each row's
-    // sum is still the sequential storage-order chain.
-    auto finish = [&](int32_t row, double t) {
-      if (row < r1) {
-        if (kern == LMPK_KERNEL_CHEB) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(ypv + row));
-        yout[row] = t;
-        if (P.use_acc) P.acc[row] = __dadd_rn(ld_cg(P.acc + row), __dmul_rn(cre, t));
-      }
-    };
-    for (int32_t s = wid; s < ns; s += 2 * nwarps) {
-      const int32_t s2 = s + nwarps;
-      const bool has2 = s2 < ns;
-      const int la = lens[s * 32 + lane];
-      const int lb = has2 ? lens[s2 * 32 + lane] : 0;
-      const int w = __reduce_max_sync(0xffffffffu, max(la, lb));
-      const int32_t* ca = cols + soff[s] + lane;
-      const double* va = vals + soff[s] + lane;
-      const int32_t* cb = cols + (has2 ? soff[s2] : 0) + lane;
-      const double* vb = vals + (has2 ? soff[s2] : 0) + lane;
-      double ta = 0.0, tb = 0.0;
-      for (int j0 = 0; j0 < w; j0 += 8) {
-        double xa[8], xb[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < la) xa[j] = ld_weak(yin + ca[(j0 + j) * 32]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < lb) xb[j] = ld_weak(yin + cb[(j0 + j) * 32]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < la) ta = __dadd_rn(ta, __dmul_rn(va[(j0 + j) * 32], xa[j]));
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < lb) tb = __dadd_rn(tb, __dmul_rn(vb[(j0 + j) * 32], xb[j]));
-      }
-      finish(r0 + s * 32 + lane, ta);
-      if (has2) finish(r0 + s2 * 32 + lane, tb);
-    }
-    return;
-  }
+  const uint32_t l4 = uint32_t(lane) * 4;
+  constexpr int cw = CPLX ? 2 : 1;
+  const char* ybase = pt.yin;
+  double* yout = pt.yout + int64_t(r0) * cw;
+  const double* ypv = pt.ypv + int64_t(r0) * cw;
+  double* acc = acc_base + int64_t(r0) * cw;
   for (int32_t s = wid; s < ns; s += nwarps) {
-    const int32_t row = r0 + s * 32 + lane;
-    const int len = lens[s * 32 + lane];
-    const int w = __reduce_max_sync(0xffffffffu, len);
-    const int32_t* cs = cols + soff[s] + lane;
-    const double* vs = vals + soff[s] + lane;
+    const int2 rec = B.i2(uint32_t(s) * 8);
+    const uint32_t cb = uint32_t(rec.x);
+    const uint32_t vb = 2 * cb + vdelta;
+    const int w = rec.y & 0xffff;
+    const bool full = int(uint32_t(rec.y) >> 16) == w;
+    const int32_t lr = s * 32 + lane;
     if constexpr (!CPLX) {
-      double t = 0.0;
-      // columns first, all gathers in flight, values read only when the
-      // gathered operands return (keeps the register footprint small)
-      for (int j0 = 0; j0 < w; j0 += 8) {
-        int cc[8];
-        double xx[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < w) cc[j] = cs[(j0 + j) * 32];
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < len) xx[j] = ld_weak(yin + cc[j]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < len) t = __dadd_rn(t, __dmul_rn(vs[(j0 + j) * 32], xx[j]));
-      }
-      if (row < r1) {
-        if (kern == LMPK_KERNEL_CHEB) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(ypv + row));
-        yout[row] = t;
-        if (P.use_acc) P.acc[row] = __dadd_rn(ld_cg(P.acc + row), __dmul_rn(cre, t));
-      }
-    } else {
-      const double2* yin2 = reinterpret_cast<const double2*>(yin);
-      double tr = 0.0, ti = 0.0;
-      for (int j0 = 0; j0 < w; j0 += 4) {
-        int cc[4];
-        double vv[4];
-        double2 xx[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j0 + j < w) {
-            cc[j] = cs[(j0 + j) * 32];
-            vv[j] = vs[(j0 + j) * 32];
-          }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j0 + j < len) xx[j] = ld_weak2(yin2 + cc[j]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j0 + j < len) {
-            tr = __dadd_rn(tr, __dmul_rn(vv[j], xx[j].x));
-            ti = __dadd_rn(ti, __dmul_rn(vv[j], xx[j].y));
-          }
-      }
-      if (row < r1) {
-        const int64_t r2 = 2 * int64_t(row);
-        if (kern == LMPK_KERNEL_CHEB) {
-          tr = __dsub_rn(__dmul_rn(2.0, tr), ld_cg(ypv + r2));
-          ti = __dsub_rn(__dmul_rn(2.0, ti), ld_cg(ypv + r2 + 1));
-        }
-        reinterpret_cast<double2*>(yout)[row] = make_double2(tr, ti);
-        if (P.use_acc) {
-          // acc += (cre + i cim) * t with the products spelled out
-          const double ar = ld_cg(P.acc + r2), ai = ld_cg(P.acc + r2 + 1);
-          const double pr = __dsub_rn(__dmul_rn(cre, tr), __dmul_rn(cim, ti));
-          const double pim = __dadd_rn(__dmul_rn(cre, ti), __dmul_rn(cim, tr));
-          P.acc[r2] = __dadd_rn(ar, pr);
-          P.acc[r2 + 1] = __dadd_rn(ai, pim);
-        }
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void mpk_publish(const MpkParams& P, int32_t t, int p) {
-  __syncthreads();  // all rows of (t, p) stored
-  if (threadIdx.x == 0) st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
-}
-
-template <bool CPLX>
-__global__ void __launch_bounds__(kMaxThreads, 2) mpk_kernel(MpkParams P, PowerCfgDev C) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t bars[2];
-  __shared__ int32_t s_work[2];
-  __shared__ int32_t s_abort;
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-    s_abort = 0;
-  }
-  __syncthreads();
-  unsigned char* buf0 = smem_raw;
-  unsigned char* buf1 = smem_raw + P.smem_cap;
-
-  if (P.mode == 1) {
-    // ---------------- RESIDENT: one tile in smem across all powers
-    const uint64_t pol = policy_evict_first();
-    for (int it = 0;; ++it) {
-      if (threadIdx.x == 0) s_work[0] = int32_t(atomicAdd(P.queue, 1ull) - P.queue_base);
-      __syncthreads();
-      const int32_t t = s_work[0];
-      if (t >= P.n_tiles || s_abort) break;
-      const int32_t r0 = __ldg(P.tile_row + t), r1 = __ldg(P.tile_row + t + 1);
-      const int64_t ofs = __ldg(P.tile_ofs + t), bytes = __ldg(P.tile_ofs + t + 1) - ofs;
-      const int32_t E = __ldg(P.tile_E + t);
-      const bool staged = stage_block(P, buf0, &bars[0], ofs, bytes, pol);
-      const int32_t lo = __ldg(P.dep_lo + t), hi = __ldg(P.dep_hi + t);
-      mbar_wait(&bars[0], it & 1);
-      __syncthreads();
-      const unsigned char* blk = staged ? buf0 : P.blocks + ofs;
-      for (int p = 1; p <= P.n_powers; ++p) {
-        if (p > 1) {
-          const bool ok = mpk_wait(P, lo, hi, P.epoch_base + uint32_t(p - 1));
-          if (threadIdx.x == 0 && !ok) s_abort = 1;
-          __syncthreads();
-          if (s_abort) break;
-        }
-        tile_power<CPLX>(P, C, blk, r0, r1, E, p, threadIdx.x >> 5, blockDim.x >> 5);
-        mpk_publish(P, t, p);
-      }
-      __syncthreads();
-      if (s_abort) break;
-    }
-    return;
-  }
-  // ---------------- STREAMING / SWEEP: items in queue order, double-buffered
-  // Sweep items are assigned statically (blockIdx + it*grid).  Streaming
-  // grabs are issued two items ahead so the queue atomic's round trip
-  // overlaps the current item's work; a CTA always computes its oldest held
-  // item, which keeps the in-order deadlock argument intact.
-  const uint64_t pol_keep = policy_evict_last();
-  const uint64_t pol_drop = policy_evict_first();
-  const bool sweep = P.mode == 3;
-  auto decode = [&](int32_t i, int32_t& t, int32_t& p) {
-    if (sweep) {
-      t = i;
-      p = 1;
-    } else {
-      const int32_t code = __ldg(P.items + i);
-      t = code >> 7;
-      p = code & 127;
-    }
-  };
-  auto grab = [&]() -> int32_t { return int32_t(atomicAdd(P.queue, 1ull) - P.queue_base); };
-  int32_t i_cur, i_next;
-  if (sweep) {
-    i_cur = blockIdx.x;
-    i_next = blockIdx.x + gridDim.x;
-  } else {
-    if (threadIdx.x == 0) {
-      const int32_t a = grab();
-      s_work[0] = a;
-      s_work[1] = a < P.n_items ? grab() : P.n_items;
-    }
-    __syncthreads();
-    i_cur = s_work[0];
-    i_next = s_work[1];
-  }
-  if (i_cur >= P.n_items) return;
-  int32_t t, p;
-  decode(i_cur, t, p);
-  int64_t ofs = __ldg(P.tile_ofs + t);
-  bool staged = stage_block(P, buf0, &bars[0], ofs, __ldg(P.tile_ofs + t + 1) - ofs,
-                            (sweep || p == P.n_powers) ? pol_drop : pol_keep);
-  for (int it = 0;; ++it) {
-    const int b = it & 1;
-    unsigned char* cur = b ? buf1 : buf0;
-    unsigned char* nxt = b ? buf0 : buf1;
-    const bool has_next = i_next < P.n_items;
-    unsigned long long ticket = 0;
-    if (!sweep && threadIdx.x == 0 && has_next) ticket = atomicAdd(P.queue, 1ull);  // item it+2
-    int32_t tn = 0, pn = 0;
-    int64_t ofsn = 0;
-    bool staged_n = false;
-    if (has_next) {  // prefetch the next item's block into the other buffer
-      decode(i_next, tn, pn);
-      ofsn = __ldg(P.tile_ofs + tn);
-      staged_n = stage_block(P, nxt, &bars[b ^ 1], ofsn, __ldg(P.tile_ofs + tn + 1) - ofsn,
-                             (sweep || pn == P.n_powers) ? pol_drop : pol_keep);
-    }
-    if (p > 1) {
-      const bool ok = mpk_wait(P, __ldg(P.dep_lo + t), __ldg(P.dep_hi + t), P.epoch_base + uint32_t(p - 1));
-      if (threadIdx.x == 0 && !ok) s_abort = 1;
-    }
-    mbar_wait(&bars[b], (it >> 1) & 1);
-    __syncthreads();
-    if (s_abort) {
-      // never leave the CTA with a bulk copy still landing in its smem
-      if (has_next) mbar_wait(&bars[b ^ 1], ((it + 1) >> 1) & 1);
-      break;
-    }
-    const int32_t r0 = __ldg(P.tile_row + t), r1 = __ldg(P.tile_row + t + 1);
-    tile_power<CPLX>(P, C, staged ? cur : P.blocks + ofs, r0, r1, __ldg(P.tile_E + t), p, threadIdx.x >> 5,
-                     blockDim.x >> 5);
-    int32_t i_after;
-    if (sweep) {
-      i_after = i_next + gridDim.x;
-      __syncthreads();
-    } else {
-      if (threadIdx.x == 0) s_work[it & 1] = has_next ? int32_t(ticket - P.queue_base) : P.n_items;
-      mpk_publish(P, t, p);  // includes the __syncthreads that publishes s_work
-      i_after = s_work[it & 1];
-    }
-    if (!has_next) break;
-    i_cur = i_next;
-    i_next = i_after;
-    t = tn;
-    p = pn;
-    ofs = ofsn;
-    staged = staged_n;
-  }
-}
-
-// ---------------------------------------------------------------- pipelined streaming / sweep
-// One producer warp + NC consumer warps per CTA (one CTA per SM).  The
-// producer grabs items in queue order, stages each tile block into a ring
-// slot with one TMA bulk copy, waits for the item's dependencies (relaxed
-// polls + acquire fence, which also invalidates L1) and then arrives on the
-// slot's FULL mbarrier.  Consumer warps flow through the ring without any
-// CTA-wide barrier: each computes its share of the slices, and the last warp
-// to finish an item (acq_rel counter in smem) publishes the item's progress
-// word with a gpu-scope release; every warp arrives on the slot's EMPTY
-// mbarrier so the producer can refill it.  Deadlock freedom: a CTA's
-// consumers never wait on other CTAs, and the producer only waits for the
-// dependencies of the oldest item it has not yet released, whose
-// dependencies precede it in the global queue order.
-constexpr int kPipeMaxSlots = 8;
-#ifndef LMPK_NC
-#define LMPK_NC 24
-#endif
-constexpr int kPipeConsumers = LMPK_NC;
-
-__device__ __forceinline__ bool warp_wait_deps(const MpkParams& P, int32_t lo, int32_t hi,
-                                               uint32_t target) {
-  const int lane = threadIdx.x & 31;
-  bool ok = true;
-  unsigned long long t0 = 0;
-  for (int32_t i = lo + lane; i <= hi; i += 32) {
-    int spins = 0;
-    while (ld_relaxed_u32(P.progress + i) < target) {
-      if (++spins > 4) __nanosleep(32);
-      if ((spins & 255) == 0) {
-        if (t0 == 0) t0 = globaltimer();
-        const volatile unsigned long long* ab = P.queue + 1;
-        if (*ab != 0ull) {
-          ok = false;
-          break;
-        }
-        if (globaltimer() - t0 > kWatchdogNs) {
-          atomicExch(P.queue + 1, 1ull);
-          *P.err = 1;
-          ok = false;
-          break;
-        }
-      }
-    }
-    if (!ok) break;
-  }
-  ok = __all_sync(0xffffffffu, ok);
-  fence_acq_rel_gpu();  // acquire (and L1 invalidation) before the slot is released
-  return ok;
-}
-
-template <bool CPLX, int NC>
-__global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_pipe_kernel(MpkParams P, PowerCfgDev C) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full_bar[kPipeMaxSlots], empty_bar[kPipeMaxSlots];
-  __shared__ int64_t s_ofs[kPipeMaxSlots];
-  __shared__ int32_t s_t[kPipeMaxSlots], s_p[kPipeMaxSlots], s_staged[kPipeMaxSlots];
-  __shared__ uint32_t s_done[kPipeMaxSlots];
-  const int S = P.n_slots;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], NC);
-      s_done[i] = 0;
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const bool sweep = P.mode == 3;
-  if (warp == NC) {
-    // ------------------------------------------------ producer warp
-    const uint64_t pol_keep = policy_evict_last();
-    const uint64_t pol_drop = policy_evict_first();
-    bool abort = false;
-    for (int k = 0;; ++k) {
-      const int slot = k % S;
-      const uint32_t use = uint32_t(k / S);
-      int32_t item;
-      if (sweep) {
-        item = blockIdx.x + k * gridDim.x;
+      double t;
+      if (full) {
+        t = slice_real<EXACT, true>(B, cb, vb, l4, ybase, w, w);
       } else {
-        int32_t g = 0;
-        if (lane == 0) g = int32_t(atomicAdd(P.queue, 1ull) - P.queue_base);
-        item = __shfl_sync(0xffffffffu, g, 0);
+        const int len = int(B.u16(lens_o + uint32_t(s) * 64 + 2 * l4 / 4));
+        t = slice_real<EXACT, false>(B, cb, vb, l4, ybase, w, len);
       }
-      if (abort) item = P.n_items;
-      if (lane == 0 && use > 0) mbar_wait(&empty_bar[slot], (use - 1) & 1);
-      __syncwarp();
-      if (item >= P.n_items) {
-        if (lane == 0) {
-          s_t[slot] = -1;
-          mbar_arrive(&full_bar[slot]);
-        }
-        break;
-      }
-      int32_t t, p;
-      if (sweep) {
-        t = item;
-        p = 1;
-      } else {
-        const int32_t code = __ldg(P.items + item);
-        t = code >> 7;
-        p = code & 127;
-      }
-      const int64_t ofs = __ldg(P.tile_ofs + t);
-      const int64_t bytes = __ldg(P.tile_ofs + t + 1) - ofs;
-      const bool staged = bytes <= P.smem_cap;
-      if (lane == 0) {
-        s_t[slot] = t;
-        s_p[slot] = p;
-        s_ofs[slot] = ofs;
-        s_staged[slot] = staged ? 1 : 0;
-        if (staged) {
-          fence_proxy_async_smem();
-          mbar_expect_tx(&full_bar[slot], uint32_t(bytes));
-          bulk_g2s(smem_raw + int64_t(slot) * P.smem_cap, P.blocks + ofs, uint32_t(bytes),
-                   &full_bar[slot], (sweep || p == P.n_powers) ? pol_drop : pol_keep);
+      if (lr < nrows) {
+        if constexpr (GENERAL) {
+          if (pt.cheb) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(ypv + lr));
+          stg_f64(yout + lr, t);
+          if (use_acc) stg_f64(acc + lr, madd<EXACT>(ld_cg(acc + lr), pt.cre, t));
+        } else {
+          stg_f64(yout + lr, t);
         }
       }
-      if (p > 1) {
-        if (!warp_wait_deps(P, __ldg(P.dep_lo + t), __ldg(P.dep_hi + t), P.epoch_base + uint32_t(p - 1)))
-          abort = true;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full_bar[slot]);
-    }
-  } else {
-    // ------------------------------------------------ consumer warps
-    for (int k = 0;; ++k) {
-      const int slot = k % S;
-      mbar_wait(&full_bar[slot], uint32_t(k / S) & 1);
-      const int32_t t = s_t[slot];
-      if (t < 0) break;
-      const int p = s_p[slot];
-      const int32_t r0 = __ldg(P.tile_row + t), r1 = __ldg(P.tile_row + t + 1);
-      const unsigned char* blk =
-          s_staged[slot] ? smem_raw + int64_t(slot) * P.smem_cap : P.blocks + s_ofs[slot];
-      tile_power<CPLX>(P, C, blk, r0, r1, __ldg(P.tile_E + t), p, warp, NC);
-      __syncwarp();
-      if (lane == 0) {
-        if (!sweep) {
-          const uint32_t old = atom_add_acqrel_cta_smem(&s_done[slot], 1u);
-          if (old == NC - 1) {
-            s_done[slot] = 0;
-            st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
+    } else {
+      const int len = full ? w : int(B.u16(lens_o + uint32_t(s) * 64 + 2 * l4 / 4));
+      double2 t = slice_cplx<EXACT>(B, cb, vb, l4, ybase, w, len);
+      if (lr < nrows) {
+        const int64_t r2 = 2 * int64_t(lr);
+        if constexpr (GENERAL) {
+          if (pt.cheb) {
+            t.x = __dsub_rn(__dmul_rn(2.0, t.x), ld_cg(ypv + r2));
+            t.y = __dsub_rn(__dmul_rn(2.0, t.y), ld_cg(ypv + r2 + 1));
           }
         }
-        mbar_arrive(&empty_bar[slot]);
+        stg_f64x2(yout + r2, t);
+        if constexpr (GENERAL) {
+          if (use_acc) {
+            // acc += (cre + i cim) * t with the products spelled out
+            const double ar = ld_cg(acc + r2), ai = ld_cg(acc + r2 + 1);
+            const double pr = __dsub_rn(__dmul_rn(pt.cre, t.x), __dmul_rn(pt.cim, t.y));
+            const double pim = __dadd_rn(__dmul_rn(pt.cre, t.y), __dmul_rn(pt.cim, t.x));
+            stg_f64x2(acc + r2, make_double2(__dadd_rn(ar, pr), __dadd_rn(ai, pim)));
+          }
+        }
       }
     }
   }
 }
 
-// ---------------------------------------------------------------- pipelined resident mode
-// One producer warp + NC consumer warps per CTA (one CTA per SM).  The CTA
-// holds R tiles resident in shared memory (one TMA bulk copy each, so the
-// matrix is read from HBM once).  The producer polls the held tiles round
-// robin WITHOUT blocking on any single one: a tile whose next power p has
-// its dependencies satisfied (tiles dep_lo..dep_hi published p-1) is queued
-// as a work item (slot, p) in a small smem ring; consumer warps drain the
-// ring like the streaming pipeline (no CTA-wide barriers; the last warp of
-// an item publishes the tile's progress word).  A tile whose last power
-// completed frees its slot, which the producer refills with the next tile
-// of the global in-order queue.  Deadlock freedom: tiles are grabbed in
-// order, so the unfinished tiles [t0, t0 + 148*R) are always held; if the
-// (p_m-1)-step dependency chain reach is below 148*R (checked when the
-// tiling is built) the oldest held tile can always advance.
-constexpr int kResMaxSlots = 8;
-constexpr int kWorkRing = 8;
-
-__device__ __forceinline__ bool warp_deps_ready(const MpkParams& P, int32_t lo, int32_t hi,
-                                                uint32_t target) {
-  bool ok = true;
-  for (int32_t i = lo + int32_t(threadIdx.x & 31); i <= hi; i += 32)
-    ok = ok && (ld_relaxed_u32(P.progress + i) >= target);
-  return __all_sync(0xffffffffu, ok);
+// Fill the per-power table (all threads of the CTA, then __syncthreads).
+__device__ __forceinline__ void build_powtab(PowTab* tab, const MpkParams& P, const PowerCfgDev& C) {
+  for (int i = threadIdx.x; i < P.n_powers; i += blockDim.x) {
+    PowTab e;
+    e.yin = reinterpret_cast<const char*>(P.y + int64_t(C.in_slot[i]) * P.ldy);
+    e.yout = P.y + int64_t(C.out_slot[i]) * P.ldy;
+    e.ypv = P.y + int64_t(C.prev_slot[i]) * P.ldy;
+    e.cre = C.coef_re[i];
+    e.cim = C.coef_im[i];
+    e.cheb = C.kernel[i] == LMPK_KERNEL_CHEB;
+    e.general = e.cheb || P.use_acc;
+    tab[i] = e;
+  }
 }
 
-template <bool CPLX, int NC>
-__global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_res_kernel(MpkParams P, PowerCfgDev C) {
+// ---------------------------------------------------------------- group walk kernel
+// See the file header.  Shared state per held slot r: h_t (tile), h_last
+// (last power of the held item), h_glb (block read from global memory),
+// slot_free (set by the consumer that finished the item's last power).
+template <bool CPLX, bool EXACT, int NC>
+__global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_group_kernel(MpkParams P, PowerCfgDev C) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t tile_bar[kResMaxSlots];
+  __shared__ uint64_t tile_bar[kMaxSlots];
   __shared__ uint64_t full_bar[kWorkRing], empty_bar[kWorkRing];
   __shared__ int32_t w_slot[kWorkRing], w_p[kWorkRing];
   __shared__ uint32_t w_done[kWorkRing];
-  __shared__ int32_t h_t[kResMaxSlots];
-  __shared__ volatile int32_t slot_free[kResMaxSlots];
+  __shared__ int32_t h_t[kMaxSlots], h_last[kMaxSlots], h_glb[kMaxSlots];
+  __shared__ int32_t h_r0[kMaxSlots], h_rows[kMaxSlots], h_E[kMaxSlots];
+  __shared__ int64_t h_ofs[kMaxSlots];
+  __shared__ volatile int32_t slot_free[kMaxSlots];
+  __shared__ PowTab s_pow[LMPK_MAX_POWERS];
   const int R = P.n_slots;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  build_powtab(s_pow, P, C);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < R; ++i) {
+    for (int i = 0; i < kMaxSlots; ++i) {
       mbar_init(&tile_bar[i], 1);
       slot_free[i] = 0;
     }
@@ -639,81 +430,181 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_res_kernel(MpkParams P, 
   }
   __syncthreads();
   if (warp == NC) {
-    // ------------------------------------------------ producer warp
-    const uint64_t pol = policy_evict_first();
-    int32_t np[kResMaxSlots];      // next power to issue per held slot (lane-uniform)
-    uint32_t refills[kResMaxSlots];
-    int32_t lo[kResMaxSlots], hi[kResMaxSlots];
-    int live = 0;
-    auto refill = [&](int r) {
-      int32_t g = 0;
-      if (lane == 0) g = int32_t(atomicAdd(P.queue, 1ull) - P.queue_base);
-      const int32_t t = __shfl_sync(0xffffffffu, g, 0);
-      if (t >= P.n_tiles || t < 0) {
-        if (lane == 0) h_t[r] = -1;
+    // ------------------------------------------------ producer / scheduler warp
+    const int pol_mode = (P.flags >> 8) & 3;
+    const uint64_t pol_keep = pol_mode == 0 ? policy_evict_last()
+                                            : (pol_mode == 1 ? policy_evict_normal() : policy_evict_first());
+    const uint64_t pol_drop = policy_evict_first();
+    const bool no_tma = (P.flags & LMPK_FLAG_NO_TMA) != 0;
+    // per-slot state, register-resident (every loop below is unrolled)
+    int32_t np[kMaxSlots], pf[kMaxSlots], pl[kMaxSlots], lo[kMaxSlots], hi[kMaxSlots];
+    uint32_t fills[kMaxSlots];
+    unsigned long long p_polls = 0, p_idle = 0, p_t0 = P.prof ? globaltimer() : 0, p_items = 0;
+    // The next queue item (ticket + tile metadata) is fetched ahead, right
+    // after a slot was filled, so a freed slot only waits for its TMA.
+    struct Next {
+      int32_t t, first, last, r0, rows, E, lo, hi;
+      int64_t ofs, bytes;
+      bool valid;
+    } nx;
+    auto fetch_next = [&]() {
+      while (true) {
+        int32_t i = 0;
+        if (lane == 0) i = int32_t(atomicAdd(P.queue, 1ull) - P.queue_base);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= P.n_items || i < 0) {
+          nx.valid = false;
+          return;
+        }
+        int32_t t = i, g = 0;
+        if (P.items) {
+          const int32_t code = __ldg(P.items + i);
+          t = code >> 8;
+          g = code & 255;
+        }
+        const int first = g * P.q + 1;
+        if (first > P.n_powers) continue;  // fewer powers than planned
+        nx.t = t;
+        nx.first = first;
+        nx.last = min(first + P.q - 1, P.n_powers);
+        nx.ofs = __ldg(P.tile_ofs + t);
+        nx.bytes = __ldg(P.tile_ofs + t + 1) - nx.ofs;
+        nx.r0 = __ldg(P.tile_row + t);
+        nx.rows = __ldg(P.tile_row + t + 1) - nx.r0;
+        nx.E = __ldg(P.tile_E + t);
+        nx.lo = __ldg(P.dep_lo + t);
+        nx.hi = __ldg(P.dep_hi + t);
+        nx.valid = true;
+        return;
+      }
+    };
+    // q > 1: a grabbed item must be held at once (the deadlock-freedom window
+    // counts grabbed items as held), so no ticket is taken ahead of a slot.
+    // q == 1 items only wait for older items, so prefetching is safe.
+    const bool prefetch = P.q == 1;
+    auto refill = [&](int r) -> bool {
+      if (!prefetch) fetch_next();
+      if (!nx.valid) {
         np[r] = 0;
+        if (lane == 0) h_t[r] = -1;
         return false;
       }
-      const int64_t ofs = __ldg(P.tile_ofs + t);
-      const int64_t bytes = __ldg(P.tile_ofs + t + 1) - ofs;
+      const bool glb = no_tma || nx.bytes > P.smem_cap;
       if (lane == 0) {
-        h_t[r] = t;
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&tile_bar[r], uint32_t(bytes));
-        bulk_g2s(smem_raw + int64_t(r) * P.smem_cap, P.blocks + ofs, uint32_t(bytes), &tile_bar[r], pol);
+        h_t[r] = nx.t;
+        h_last[r] = nx.last;
+        h_ofs[r] = nx.ofs;
+        h_glb[r] = glb ? 1 : 0;
+        h_r0[r] = nx.r0;
+        h_rows[r] = nx.rows;
+        h_E[r] = nx.E;
+        if (!glb) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&tile_bar[r], uint32_t(nx.bytes));
+          bulk_g2s(smem_raw + int64_t(r) * P.smem_cap, P.blocks + nx.ofs, uint32_t(nx.bytes), &tile_bar[r],
+                   nx.last == P.n_powers ? pol_drop : pol_keep);
+        } else {
+          mbar_arrive(&tile_bar[r]);
+        }
       }
-      lo[r] = __ldg(P.dep_lo + t);
-      hi[r] = __ldg(P.dep_hi + t);
-      np[r] = 1;
+      pf[r] = nx.first;
+      pl[r] = nx.last;
+      np[r] = nx.first;
+      lo[r] = nx.lo;
+      hi[r] = nx.hi;
+      ++p_items;
+      if (prefetch) fetch_next();
       return true;
     };
-    for (int r = 0; r < R; ++r) {
-      refills[r] = 0;
-      if (refill(r)) ++live;
+    if (prefetch) fetch_next();
+    int live = 0;
+#pragma unroll
+    for (int r = 0; r < kMaxSlots; ++r) {
+      fills[r] = 0;
+      np[r] = 0;
+      pf[r] = pl[r] = lo[r] = hi[r] = 0;
+      if (r < R && refill(r)) ++live;
     }
     int k = 0;  // work items pushed
     unsigned long long idle_since = 0;
     bool abort = false;
     while (live > 0 && !abort) {
       bool progressed = false;
-      for (int r = 0; r < R; ++r) {
-        if (np[r] == 0) continue;  // retired slot
-        if (np[r] > P.n_powers) {
-          // all powers issued: refill once the last one completed
-          if (slot_free[r]) {
-            __syncwarp();
-            if (lane == 0) slot_free[r] = 0;
-            __threadfence_block();
-            ++refills[r];
-            if (!refill(r)) --live;
-            progressed = true;
+      // ---- refill slots whose item finished its last power
+#pragma unroll
+      for (int r = 0; r < kMaxSlots; ++r) {
+        if (r < R && np[r] != 0 && np[r] > pl[r] && slot_free[r]) {
+          __syncwarp();
+          if (lane == 0) slot_free[r] = 0;
+          __threadfence_block();
+          ++fills[r];
+          if (!refill(r)) --live;
+          progressed = true;
+        }
+      }
+      // ---- dependency polls of every held item, one batch of loads
+      uint32_t want = 0, tgt[kMaxSlots];
+#pragma unroll
+      for (int r = 0; r < kMaxSlots; ++r) {
+        tgt[r] = 0;
+        if (r < R && np[r] != 0 && np[r] <= pl[r]) {
+          const bool staged = np[r] != pf[r] || mbar_test(&tile_bar[r], fills[r] & 1);
+          if (staged) {
+            want |= 1u << r;
+            tgt[r] = np[r] > 1 ? P.epoch_base + uint32_t(np[r] - 1) : 0u;
           }
-          continue;
         }
-        const int p = np[r];
-        bool ready;
-        if (p == 1)
-          ready = mbar_test(&tile_bar[r], refills[r] & 1);
-        else
-          ready = warp_deps_ready(P, lo[r], hi[r], P.epoch_base + uint32_t(p - 1));
-        if (!ready) continue;
-        if (p > 1) fence_acq_rel_gpu();  // acquire + L1 invalidation before the gathers
-        const int ws = k % kWorkRing;
-        if (lane == 0) {
-          if (k >= kWorkRing) mbar_wait(&empty_bar[ws], uint32_t(k / kWorkRing - 1) & 1);
-          w_slot[ws] = r;
-          w_p[ws] = p;
-          mbar_arrive(&full_bar[ws]);
+      }
+      uint32_t ready = 0;
+      if (want) {
+        uint32_t v0[kMaxSlots], v1[kMaxSlots];
+#pragma unroll
+        for (int r = 0; r < kMaxSlots; ++r) {
+          v0[r] = v1[r] = 0xffffffffu;
+          if (((want >> r) & 1) && tgt[r] != 0) {
+            const int32_t i0 = lo[r] + lane, i1 = i0 + 32;
+            if (i0 <= hi[r]) v0[r] = ld_relaxed_u32(P.progress + i0);
+            if (i1 <= hi[r]) v1[r] = ld_relaxed_u32(P.progress + i1);
+          }
         }
-        __syncwarp();
-        ++k;
-        np[r] = p + 1;
+#pragma unroll
+        for (int r = 0; r < kMaxSlots; ++r) {
+          if ((want >> r) & 1) {
+            bool ok = v0[r] >= tgt[r] && v1[r] >= tgt[r];
+            if (tgt[r] != 0)
+              for (int32_t i = lo[r] + lane + 64; i <= hi[r]; i += 32)
+                ok = ok && ld_relaxed_u32(P.progress + i) >= tgt[r];
+            if (__all_sync(0xffffffffu, ok)) ready |= 1u << r;
+          }
+        }
+        if (P.prof) {
+          ++p_polls;
+          if (!ready) ++p_idle;
+        }
+      }
+      if (ready) {
+        fence_acq_rel_gpu();  // acquire + L1 invalidation before the gathers
+#pragma unroll
+        for (int r = 0; r < kMaxSlots; ++r) {
+          if ((ready >> r) & 1) {
+            const int ws = k % kWorkRing;
+            if (lane == 0) {
+              if (k >= kWorkRing) mbar_wait(&empty_bar[ws], uint32_t(k / kWorkRing - 1) & 1);
+              w_slot[ws] = r;
+              w_p[ws] = np[r];
+              mbar_arrive(&full_bar[ws]);
+            }
+            __syncwarp();
+            ++k;
+            ++np[r];
+          }
+        }
         progressed = true;
       }
       if (progressed) {
         idle_since = 0;
       } else {
-        __nanosleep(64);
+        __nanosleep(32);
         const unsigned long long now = globaltimer();
         if (idle_since == 0) idle_since = now;
         const volatile unsigned long long* ab = P.queue + 1;
@@ -727,6 +618,12 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_res_kernel(MpkParams P, 
         }
       }
     }
+    if (P.prof && lane == 0) {
+      atomicAdd(P.prof + 3, p_polls);
+      atomicAdd(P.prof + 4, p_idle);
+      atomicAdd(P.prof + 5, globaltimer() - p_t0);
+      atomicAdd(P.prof + 6, p_items);
+    }
     // terminator
     const int ws = k % kWorkRing;
     if (lane == 0) {
@@ -734,29 +631,51 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_res_kernel(MpkParams P, 
       w_slot[ws] = -1;
       mbar_arrive(&full_bar[ws]);
     }
-    // no TMA may still be landing when the CTA exits: held slots were either
-    // consumed (power >= 1 issued) or are waited for here
-    if (abort && lane == 0)
-      for (int r = 0; r < R; ++r)
-        if (np[r] == 1) mbar_wait(&tile_bar[r], refills[r] & 1);
+    // no TMA may still be landing when the CTA exits
+    if (abort && lane == 0) {
+#pragma unroll
+      for (int r = 0; r < kMaxSlots; ++r)
+        if (r < R && np[r] != 0 && np[r] == pf[r]) mbar_wait(&tile_bar[r], fills[r] & 1);
+    }
   } else {
-    // ------------------------------------------------ consumer warps
+    // ------------------------------------------------ consumer warps: compute only
+    unsigned long long t_wait = 0, t_comp = 0, n_it = 0;
     for (int k = 0;; ++k) {
       const int ws = k % kWorkRing;
+      const unsigned long long tw0 = P.prof ? globaltimer() : 0;
       mbar_wait(&full_bar[ws], uint32_t(k / kWorkRing) & 1);
+      const unsigned long long tw1 = P.prof ? globaltimer() : 0;
       const int r = w_slot[ws];
       if (r < 0) break;
       const int p = w_p[ws];
       const int32_t t = h_t[r];
-      const int32_t r0 = __ldg(P.tile_row + t), r1 = __ldg(P.tile_row + t + 1);
-      tile_power<CPLX>(P, C, smem_raw + int64_t(r) * P.smem_cap, r0, r1, __ldg(P.tile_E + t), p, warp, NC);
+      const int32_t r0 = h_r0[r], rows = h_rows[r];
+      const uint32_t E = uint32_t(h_E[r]);
+      const PowTab& pt = s_pow[p - 1];
+      const bool use_acc = P.use_acc != 0;
+      // separate inlined copies so each sees a known address space (LDS vs
+      // LDG); plain SpMV powers take the epilogue without Chebyshev/acc
+      if (!h_glb[r]) {
+        const SmemBlk B{smem_u32(smem_raw) + uint32_t(r) * uint32_t(P.smem_cap)};
+        if (pt.general)
+          tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, r0, rows, E, warp, NC);
+        else
+          tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, r0, rows, E, warp, NC);
+      } else {
+        tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, GlbBlk{P.blocks + h_ofs[r]}, r0, rows, E, warp, NC);
+      }
       __syncwarp();
+      if (P.prof) {
+        t_wait += tw1 - tw0;
+        t_comp += globaltimer() - tw1;
+        ++n_it;
+      }
       if (lane == 0) {
         const uint32_t old = atom_add_acqrel_cta_smem(&w_done[ws], 1u);
         if (old == NC - 1) {
           w_done[ws] = 0;
-          st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
-          if (p == P.n_powers) {
+          if (P.mode != 3) st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
+          if (p == h_last[r]) {
             __threadfence_block();
             slot_free[r] = 1;
           }
@@ -764,25 +683,36 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_res_kernel(MpkParams P, 
         mbar_arrive(&empty_bar[ws]);
       }
     }
+    if (P.prof && lane == 0) {
+      atomicAdd(P.prof + 0, t_wait);
+      atomicAdd(P.prof + 1, t_comp);
+      atomicAdd(P.prof + 2, n_it);
+    }
   }
 }
 
 // ---------------------------------------------------------------- tiling kernels
-__global__ void k_slice_width(const int32_t* row_ptr, int32_t n, int32_t n_slices, int32_t* width) {
+// per slice: longest row (width) and shortest row (padding-free prefix)
+__global__ void k_slice_width(const int32_t* row_ptr, int32_t n, int32_t n_slices, int32_t* width,
+                              int32_t* wmin) {
   const int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
   const int32_t r = s * 32 + lane;
   const int len = r < n ? __ldg(row_ptr + r + 1) - __ldg(row_ptr + r) : 0;
   const int w = __reduce_max_sync(0xffffffffu, len);
-  if (lane == 0) width[s] = w;
+  const int m = __reduce_min_sync(0xffffffffu, len);
+  if (lane == 0) {
+    width[s] = w;
+    wmin[s] = m;
+  }
 }
 
-// one warp per slice: write slice offset, row lengths and column-major entries
+// one warp per slice: slice record, row lengths and the chunked entries
 __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const double* val,
                               int32_t n_slices, const int32_t* slice_tile, const int32_t* slice_off,
-                              const int32_t* width, const int32_t* tile_row, const int64_t* tile_ofs,
-                              const int32_t* tile_E, unsigned char* blocks) {
+                              const int32_t* width, const int32_t* wmin, const int32_t* tile_row,
+                              const int64_t* tile_ofs, const int32_t* tile_E, unsigned char* blocks) {
   const int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
@@ -791,8 +721,8 @@ __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const 
   const int32_t ns = (r1 - r0 + 31) >> 5;
   const int32_t ls = s - (r0 >> 5);
   unsigned char* blk = blocks + tile_ofs[t];
-  int32_t* soff = reinterpret_cast<int32_t*>(blk);
-  uint16_t* lens = reinterpret_cast<uint16_t*>(blk + ((ns + 3) & ~3) * 4);
+  int2* rec = reinterpret_cast<int2*>(blk);
+  uint16_t* lens = reinterpret_cast<uint16_t*>(blk + int64_t(ns) * 8);
   const int64_t co = blk_col_off(ns);
   const int32_t E = tile_E[t];
   int32_t* cols = reinterpret_cast<int32_t*>(blk + co);
@@ -802,11 +732,11 @@ __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const 
   const bool valid = r < r1;
   const int32_t a = valid ? row_ptr[r] : 0;
   const int len = valid ? row_ptr[r + 1] - a : 0;
-  if (lane == 0) soff[ls] = base;
-  lens[ls * 32 + lane] = uint16_t(len);
   const int w = width[s];
+  if (lane == 0) rec[ls] = make_int2(int32_t(co + int64_t(base) * 4), w | (wmin[s] << 16));
+  lens[ls * 32 + lane] = uint16_t(len);
   for (int j = 0; j < w; ++j) {
-    const int64_t e = int64_t(base) + int64_t(j) * 32 + lane;
+    const int64_t e = chunk_entry(base, w, lane, j);
     if (j < len) {
       cols[e] = col[a + j];
       vals[e] = val[a + j];
@@ -866,91 +796,56 @@ static int dmalloc(T** p, size_t count) {
   return LMPK_OK;
 }
 
-template <bool CPLX>
-static cudaError_t occupancy_t(lmpk_ctx* ctx, int threads, int smem, int* occ) {
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, mpk_kernel<CPLX>);
-  if (e != cudaSuccess) return e;
-  const int max_dyn = ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes);
-  if (smem > max_dyn) {
-    *occ = 0;
-    return cudaSuccess;
-  }
-  // the attribute is only an upper bound: set it to the device maximum
-  e = cudaFuncSetAttribute(mpk_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, mpk_kernel<CPLX>, threads, smem);
+static const void* group_fn(bool cplx, bool exact) {
+  if (cplx)
+    return exact ? reinterpret_cast<const void*>(mpk_group_kernel<true, true, kConsumers>)
+                 : reinterpret_cast<const void*>(mpk_group_kernel<true, false, kConsumers>);
+  return exact ? reinterpret_cast<const void*>(mpk_group_kernel<false, true, kConsumers>)
+               : reinterpret_cast<const void*>(mpk_group_kernel<false, false, kConsumers>);
 }
 
-// occupancy valid for both instantiations (complex uses more registers)
-static int occupancy(lmpk_ctx* ctx, int threads, int smem, int* occ) {
-  int o1 = 0, o2 = 0;
-  cudaError_t e = occupancy_t<false>(ctx, threads, smem, &o1);
-  if (e == cudaSuccess) e = occupancy_t<true>(ctx, threads, smem, &o2);
-  if (e != cudaSuccess) {
-    cudaGetLastError();  // do not leave a sticky status for later checks
-    set_error("occupancy query failed: %s", cudaGetErrorString(e));
-    return LMPK_ERR_CUDA;
-  }
-  *occ = std::min(o1, o2);
+// Largest dynamic smem one group-kernel CTA may use (all instantiations), and
+// the occupancy at `smem` bytes (min over instantiations).
+static int group_occupancy(lmpk_ctx* ctx, int smem, int* occ) {
+  *occ = 1 << 20;
+  for (int c = 0; c < 2; ++c)
+    for (int x = 0; x < 2; ++x) {
+      const void* fn = group_fn(c != 0, x != 0);
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+      const int max_dyn = ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes);
+      if (e == cudaSuccess && smem > max_dyn) {
+        *occ = 0;
+        return LMPK_OK;
+      }
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+      int o = 0;
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kBlockThreads, smem);
+      if (e != cudaSuccess) {
+        cudaGetLastError();  // do not leave a sticky status for later checks
+        set_error("occupancy query failed: %s", cudaGetErrorString(e));
+        return LMPK_ERR_CUDA;
+      }
+      *occ = std::min(*occ, o);
+    }
   return LMPK_OK;
 }
 
-template <bool CPLX>
-static cudaError_t pipe_attr_t(lmpk_ctx* ctx, int smem, int* occ) {
-  auto fn = mpk_pipe_kernel<CPLX, kPipeConsumers>;
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-  if (e != cudaSuccess) return e;
-  const int max_dyn = ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes);
-  if (smem > max_dyn) {
-    *occ = 0;
-    return cudaSuccess;
-  }
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, 32 * (kPipeConsumers + 1), smem);
-}
-
-template <bool CPLX>
-static cudaError_t res_attr_t(lmpk_ctx* ctx, int smem, int* occ) {
-  auto fn = mpk_res_kernel<CPLX, kPipeConsumers>;
-  cudaFuncAttributes fa;
-  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-  if (e != cudaSuccess) return e;
-  const int max_dyn = ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes);
-  if (smem > max_dyn) {
-    *occ = 0;
-    return cudaSuccess;
-  }
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, fn, 32 * (kPipeConsumers + 1), smem);
-}
-
-static int res_occupancy(lmpk_ctx* ctx, int smem, int* occ) {
-  int o1 = 0, o2 = 0;
-  cudaError_t e = res_attr_t<false>(ctx, smem, &o1);
-  if (e == cudaSuccess) e = res_attr_t<true>(ctx, smem, &o2);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    set_error("occupancy query failed: %s", cudaGetErrorString(e));
-    return LMPK_ERR_CUDA;
-  }
-  *occ = std::min(o1, o2);
-  return LMPK_OK;
-}
-
-static int pipe_occupancy(lmpk_ctx* ctx, int smem, int* occ) {
-  int o1 = 0, o2 = 0;
-  cudaError_t e = pipe_attr_t<false>(ctx, smem, &o1);
-  if (e == cudaSuccess) e = pipe_attr_t<true>(ctx, smem, &o2);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    set_error("occupancy query failed: %s", cudaGetErrorString(e));
-    return LMPK_ERR_CUDA;
-  }
-  *occ = std::min(o1, o2);
+// Largest static shared memory over the group-kernel instantiations.
+static int group_static_smem(int* out) {
+  int mx = 0;
+  for (int c = 0; c < 2; ++c)
+    for (int x = 0; x < 2; ++x) {
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, group_fn(c != 0, x != 0));
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("cudaFuncGetAttributes failed: %s", cudaGetErrorString(e));
+        return LMPK_ERR_CUDA;
+      }
+      mx = std::max(mx, static_cast<int>(fa.sharedSizeBytes));
+    }
+  *out = mx;
   return LMPK_OK;
 }
 
@@ -980,9 +875,9 @@ static void partition_slices(const std::vector<int32_t>& width, int64_t cap,
   }
 }
 
-// max over t of the (p_m-1)-step forward dependency chain, via the prefix max
+// max over t of the (steps)-step forward dependency chain, via the prefix max
 // of dep_hi (monotone, conservative).
-static int32_t chain_reach(const std::vector<int32_t>& dep_hi, int32_t p_m, int32_t* max_fwd) {
+static int32_t chain_reach(const std::vector<int32_t>& dep_hi, int32_t steps, int32_t* max_fwd) {
   const int32_t nt = static_cast<int32_t>(dep_hi.size());
   std::vector<int32_t> H(nt);
   int32_t run = 0, mf = 0;
@@ -991,11 +886,11 @@ static int32_t chain_reach(const std::vector<int32_t>& dep_hi, int32_t p_m, int3
     H[t] = run;
     mf = std::max(mf, dep_hi[t] - t);
   }
-  *max_fwd = mf;
+  if (max_fwd) *max_fwd = mf;
   int32_t worst = 0;
   for (int32_t t = 0; t < nt; ++t) {
     int32_t c = t;
-    for (int32_t j = 1; j < p_m; ++j) {
+    for (int32_t j = 0; j < steps; ++j) {
       const int32_t nc = H[c];
       if (nc == c) break;
       c = nc;
@@ -1023,10 +918,10 @@ extern "C" int lmpk_tiling_destroy(lmpk_tiling* t) {
   return LMPK_OK;
 }
 
-// Tiles + tile-SELL-32 blocks + dependency ranges for block cap `cap` bytes.
+// Tiles + chunked tile-SELL-32 blocks + dependency ranges for block cap `cap` bytes.
 static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
                         const int32_t* col, const double* val, const std::vector<int32_t>& width,
-                        int64_t cap, cudaStream_t st) {
+                        const int32_t* d_wmin, int64_t cap, cudaStream_t st) {
   const int32_t S = static_cast<int32_t>(width.size());
   std::vector<int32_t> first;
   std::vector<int64_t> Es;
@@ -1055,7 +950,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   tile_ofs[nt] = ofs;
   T->h_tile_row = tile_row;
   T->block_bytes = ofs;
-  T->max_block = static_cast<int32_t>(maxb);
+  T->max_block = static_cast<int32_t>(std::min<int64_t>(maxb, INT32_MAX));
   LMPK_TRY(dmalloc(&T->d_tile_row, nt + 1));
   LMPK_TRY(dmalloc(&T->d_tile_ofs, nt + 1));
   LMPK_TRY(dmalloc(&T->d_tile_E, nt));
@@ -1078,7 +973,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   LMPK_CHECK_CUDA(cudaMemsetAsync(T->d_progress, 0, size_t(nt) * 4, st));
   if (S > 0) {
     k_fill_blocks<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_slice_tile, d_slice_off,
-                                                                 d_width, T->d_tile_row, T->d_tile_ofs,
+                                                                 d_width, d_wmin, T->d_tile_row, T->d_tile_ofs,
                                                                  T->d_tile_E, T->d_blocks);
     launch_count_add(ctx, 1);
   }
@@ -1107,99 +1002,125 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   LMPK_ARG_CHECK(n >= 0, "n must be >= 0");
   lmpk_tiling_params prm{};
   if (params) prm = *params;
+  LMPK_ARG_CHECK(prm.slots >= 0 && prm.slots <= kMaxSlots, "slots must be in [0, %d]", kMaxSlots);
+  LMPK_ARG_CHECK(prm.powers_per_item >= 0 && prm.powers_per_item <= p_m,
+                 "powers_per_item must be in [0, p_m]");
   *out = nullptr;
   cudaStream_t st = as_stream(stream);
   int32_t h_nnz = 0;
   LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_nnz, row_ptr + n, 4, cudaMemcpyDeviceToHost, st));
   const int32_t S = (n + 31) / 32;
   std::vector<int32_t> width(S);
+  int32_t* d_w = nullptr;
+  int32_t* d_wmin = nullptr;
+  LMPK_TRY(dmalloc(&d_w, std::max(S, 1)));
+  LMPK_TRY(dmalloc(&d_wmin, std::max(S, 1)));
+  struct Guard {
+    int32_t *a, *b;
+    ~Guard() {
+      cudaFree(a);
+      cudaFree(b);
+    }
+  } guard{d_w, d_wmin};
   if (S > 0) {
-    int32_t* d_w = nullptr;
-    LMPK_TRY(dmalloc(&d_w, S));
-    k_slice_width<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, n, S, d_w);
+    k_slice_width<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, n, S, d_w, d_wmin);
     launch_count_add(ctx, 1);
     LMPK_CHECK_CUDA(cudaMemcpyAsync(width.data(), d_w, size_t(S) * 4, cudaMemcpyDeviceToHost, st));
-    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_w);
-  } else {
-    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   }
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   int32_t max_row = 0;
   for (int32_t w : width) max_row = std::max(max_row, w);
   LMPK_ARG_CHECK(max_row <= 65535, "rows longer than 65535 entries are not supported by the tiled kernel");
 
   const bool want_stream = (prm.mode_flags & LMPK_FLAG_MODE_STREAM) != 0;
   const bool want_res = (prm.mode_flags & LMPK_FLAG_MODE_RESIDENT) != 0;
-  const int threads = prm.threads > 0 ? prm.threads : kMaxThreads;
-  LMPK_ARG_CHECK(threads % 32 == 0 && threads >= 64 && threads <= kMaxThreads,
-                 "threads must be a multiple of 32 in [64, %d]", kMaxThreads);
-  const int static_reserve = 1024 + 64;  // per-CTA driver reserve + static smem
-  // candidates: (mode, ring/resident slots); both pipelined kernels run one
-  // CTA per SM with one producer warp and kPipeConsumers consumer warps
+  LMPK_ARG_CHECK(!(want_stream && want_res), "MODE_STREAM and MODE_RESIDENT are exclusive");
+  // candidates (q powers per item, R slots), first feasible wins
   struct Cand {
-    int mode, slots;
+    int q, slots;
   };
   std::vector<Cand> cands;
-  if (!want_stream) {
-    if (prm.slots > 0)
-      cands.push_back({1, std::min(prm.slots, kResMaxSlots)});
+  const int R0 = prm.slots > 0 ? prm.slots : 0;
+  if (want_res) {
+    if (R0)
+      cands.push_back({p_m, R0});
     else
-      for (int r : {2, 3, 4, 6, 8}) cands.push_back({1, r});
+      for (int r : {2, 3, 4}) cands.push_back({p_m, r});
+  } else if (want_stream || prm.powers_per_item > 0) {
+    const int q = prm.powers_per_item > 0 ? prm.powers_per_item : 1;
+    cands.push_back({q, R0 ? R0 : 2});
+    if (!R0) cands.push_back({q, 3});
+  } else {
+    // default plan: pure streaming (measured fastest on the cfg2 stencil:
+    // 1.07 ms vs 1.46 ms for q = 2 and 1.80 ms fully resident)
+    cands.push_back({1, R0 ? R0 : 2});
   }
-  if (!want_res) cands.push_back({2, prm.slots > 0 ? std::min(prm.slots, kPipeMaxSlots) : 3});
   lmpk_tiling* T = nullptr;
-  int grid = 0, smem = 0, mode = 0, slots = 1;
+  int grid = 0, smem = 0, slots = 1, q_used = 1;
   int32_t mfwd = 0, creach = 0;
   int64_t cap_used = 0;
+  int static_smem = 0;
+  LMPK_TRY(group_static_smem(&static_smem));
+  // the driver reserves 1 KB per CTA; the rest of the SM's smem is the budget
+  const int64_t per_cta = std::min<int64_t>(ctx->max_smem_sm - 1024 - static_smem,
+                                            ctx->max_smem_block - static_smem);
+  // LMPK_FLAG_NO_TMA in the tiling's mode flags: blocks are streamed from
+  // global memory, so the slots need no shared memory and R is free
+  const bool unstaged = (prm.mode_flags & LMPK_FLAG_NO_TMA) != 0;
   for (const Cand& cd : cands) {
-    int64_t cap = (ctx->max_smem_block - 1024) / cd.slots;
+    int64_t cap = unstaged ? per_cta / 2 : per_cta / cd.slots;
     if (prm.tile_nnz_hint > 0) cap = std::min<int64_t>(cap, int64_t(prm.tile_nnz_hint) * 12 + 2048);
     cap &= ~int64_t(127);
     if (cap < 2048) continue;
-    const int smem_need = static_cast<int>(cap * cd.slots);
+    const int smem_need = unstaged ? 0 : static_cast<int>(cap * cd.slots);
     int occ = 0;
-    if (cd.mode == 1)
-      LMPK_TRY(res_occupancy(ctx, smem_need, &occ));
-    else
-      LMPK_TRY(pipe_occupancy(ctx, smem_need, &occ));
+    LMPK_TRY(group_occupancy(ctx, smem_need, &occ));
     if (occ < 1) continue;
     lmpk_tiling* cand = new lmpk_tiling();
     cand->ctx = ctx;
     cand->n = n;
-    const int rc = build_tiling(ctx, cand, n, row_ptr, col, val, width, cap, st);
+    const int rc = build_tiling(ctx, cand, n, row_ptr, col, val, width, d_wmin, cap, st);
     if (rc != LMPK_OK) {
       lmpk_tiling_destroy(cand);
       return rc;
     }
     int32_t mf = 0;
-    const int32_t cr = chain_reach(cand->h_dep_hi, p_m, &mf);
+    const int32_t cr = chain_reach(cand->h_dep_hi, cd.q - 1, &mf);
     const int g = ctx->sm_count;
-    // resident: every held tile must fit its slot, and the dependency chain
-    // of the oldest held tile must stay inside the held window
-    if (cd.mode == 1 && !(cr < g * cd.slots - 1 && cand->max_block <= cap)) {
+    const int64_t G = (p_m + cd.q - 1) / cd.q;
+    // the oldest unfinished item needs the next G*(cr+1) queue positions
+    // held (q > 1 grabs a ticket only for a free slot)
+    const bool ok = (cd.q == 1 || int64_t(g) * cd.slots >= G * (int64_t(cr) + 1) + 1) &&
+                    (cd.q == 1 || unstaged || cand->max_block <= cap);
+    if (!ok) {
       lmpk_tiling_destroy(cand);
       continue;
     }
     T = cand;
-    mode = cd.mode;
     grid = g;
     smem = smem_need;
     slots = cd.slots;
+    q_used = cd.q;
     mfwd = mf;
-    creach = cr;
+    creach = chain_reach(cand->h_dep_hi, p_m - 1, nullptr);
     cap_used = cap;
     break;
   }
   if (!T) {
-    set_error("lmpk_tiling_create: no feasible tiling (mode flags 0x%x)", prm.mode_flags);
+    set_error("lmpk_tiling_create: no feasible tiling (mode flags 0x%x, powers_per_item %d)", prm.mode_flags,
+              prm.powers_per_item);
     return want_res ? LMPK_ERR_UNSUPPORTED : LMPK_ERR_ARG;
   }
   const int32_t nt = T->info.n_tiles;
+  if (nt >= (1 << 23)) {
+    lmpk_tiling_destroy(T);
+    set_error("too many tiles (%d)", nt);
+    return LMPK_ERR_UNSUPPORTED;
+  }
   T->info.p_m = p_m;
-  T->info.mode = mode;
-  T->info.block = 32 * (kPipeConsumers + 1);
+  T->info.mode = q_used == p_m ? 1 : 2;
+  T->info.block = kBlockThreads;
   T->slots = slots;
-  (void)threads;
   T->info.smem_bytes = smem;
   T->info.tile_nnz_cap = static_cast<int32_t>(cap_used / 12);
   T->info.max_fwd_reach = mfwd;
@@ -1207,33 +1128,30 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   T->info.max_row_nnz = max_row;
   T->info.nnz = h_nnz;
   T->info.grid = grid;
-  if (mode == 2) {
-    // skewed diagonal order key (t + p*M, p), M = D + slack; dependent items
-    // land ~slack*p_m queue positions apart
-    const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (2 * grid + p_m - 1) / p_m);
-    T->info.queue_slack = slack;
-    const int64_t M = int64_t(std::max(mfwd, 0)) + slack;
-    std::vector<int64_t> keys;
-    keys.reserve(int64_t(nt) * p_m);
-    for (int32_t t = 0; t < nt; ++t)
-      for (int32_t p = 1; p <= p_m; ++p) keys.push_back(((t + p * M) << 8) | p);
-    std::vector<int32_t> order(keys.size());
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return keys[a] < keys[b]; });
-    std::vector<int32_t> items(order.size());
-    for (size_t i = 0; i < order.size(); ++i) {
-      const int32_t t = order[i] / p_m, p = order[i] % p_m + 1;
-      items[i] = (t << 7) | p;
-    }
-    LMPK_TRY(dmalloc(&T->d_items, items.size()));
-    LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_items, items.data(), items.size() * 4, cudaMemcpyHostToDevice, st));
-    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  T->info.powers_per_item = q_used;
+  T->info.slots = slots;
+  // skewed diagonal key (t + g*M, g), M = q*D + slack
+  const int32_t G = (p_m + q_used - 1) / q_used;
+  // default slack ~1.5 * (items in flight) / G: measured optimum on cfg2
+  const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (3 * grid * slots) / (2 * G));
+  T->info.queue_slack = G > 1 ? slack : 0;
+  const int64_t M = int64_t(q_used) * std::max(mfwd, 0) + slack;
+  std::vector<int64_t> keys;
+  keys.reserve(int64_t(nt) * G);
+  for (int32_t t = 0; t < nt; ++t)
+    for (int32_t g = 0; g < G; ++g) keys.push_back(((t + g * M) << 8) | g);
+  std::vector<int32_t> order(keys.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return keys[a] < keys[b]; });
+  std::vector<int32_t> items(order.size());
+  for (size_t i = 0; i < order.size(); ++i) {
+    const int32_t t = order[i] / G, g = order[i] % G;
+    items[i] = (t << 8) | g;
   }
-  if (nt >= (1 << 24)) {
-    lmpk_tiling_destroy(T);
-    set_error("too many tiles (%d)", nt);
-    return LMPK_ERR_UNSUPPORTED;
-  }
+  T->n_items = static_cast<int32_t>(items.size());
+  LMPK_TRY(dmalloc(&T->d_items, items.size()));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_items, items.data(), items.size() * 4, cudaMemcpyHostToDevice, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   if (info) *info = T->info;
   *out = T;
   return LMPK_OK;
@@ -1249,24 +1167,22 @@ extern "C" int lmpk_tiling_geometry(const lmpk_tiling* t, int32_t* tile_row, int
   return LMPK_OK;
 }
 
-static int launch_mpk(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev& C, bool cplx,
-                      bool coop, int grid, int smem, cudaStream_t st) {
+static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool coop,
+                        int grid, int smem, cudaStream_t st) {
   void* args[] = {&Pm, &C};
-  const bool pipe = Pm.mode != 1;
-  const void* fn = pipe ? (cplx ? reinterpret_cast<const void*>(mpk_pipe_kernel<true, kPipeConsumers>)
-                                : reinterpret_cast<const void*>(mpk_pipe_kernel<false, kPipeConsumers>))
-                        : (cplx ? reinterpret_cast<const void*>(mpk_res_kernel<true, kPipeConsumers>)
-                                : reinterpret_cast<const void*>(mpk_res_kernel<false, kPipeConsumers>));
-  const int block = 32 * (kPipeConsumers + 1);
-  cudaError_t e = coop ? cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, st)
-                       : cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, st);
+  const void* fn = group_fn(cplx, exact);
+  cudaError_t e = coop ? cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, smem, st)
+                       : cudaLaunchKernel(fn, dim3(grid), dim3(kBlockThreads), args, smem, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    set_error("mpk launch failed: %s (grid %d, block %d, smem %d)", cudaGetErrorString(e), grid, block,
-              smem);
+    set_error("mpk launch failed: %s (grid %d, block %d, smem %d)", cudaGetErrorString(e), grid,
+              kBlockThreads, smem);
     return LMPK_ERR_CUDA;
   }
   launch_count_add(ctx, 1);
+  // q == 1: every CTA ends its prefetching grab sequence with exactly one
+  // failing grab; q > 1: every slot does
+  ctx->queue_base += uint64_t(Pm.n_items) + uint64_t(grid) * uint64_t(Pm.q == 1 ? 1 : Pm.n_slots);
   return LMPK_OK;
 }
 
@@ -1279,6 +1195,7 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   LMPK_ARG_CHECK(P >= 1 && P <= LMPK_MAX_POWERS, "n_powers must be in [1, %d]", LMPK_MAX_POWERS);
   LMPK_ARG_CHECK(sweep || P <= T->info.p_m, "n_powers %d exceeds the tiling's p_m %d", P, T->info.p_m);
   const bool cplx = (flags & LMPK_FLAG_COMPLEX) != 0;
+  const bool exact = (flags & LMPK_FLAG_EXACT) != 0;
   LMPK_ARG_CHECK(ldy >= int64_t(T->n) * (cplx ? 2 : 1), "ldy too small");
   LMPK_ARG_CHECK(!use_acc || acc != nullptr, "use_acc requires acc");
   LMPK_ARG_CHECK(!cplx || (reinterpret_cast<uintptr_t>(y) & 15) == 0, "complex y must be 16-byte aligned");
@@ -1309,28 +1226,20 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   Pm.tile_row = T->d_tile_row;
   Pm.dep_lo = T->d_dep_lo;
   Pm.dep_hi = T->d_dep_hi;
-  Pm.items = T->d_items;
   Pm.y = y;
   Pm.ldy = ldy;
-  Pm.acc = acc;
+  Pm.acc = use_acc ? acc : y;  // never dereferenced without use_acc
   Pm.use_acc = use_acc ? 1 : 0;
   Pm.progress = Tm->d_progress;
   Pm.queue = reinterpret_cast<unsigned long long*>(ctx->queue_ctr);
-  Pm.n_tiles = T->info.n_tiles;
   Pm.n_slots = T->slots;
   Pm.smem_cap = T->info.smem_bytes / T->slots;
-  Pm.use_tma = (flags & LMPK_FLAG_NO_TMA) ? 0 : 1;
+  Pm.flags = flags;
   Pm.err = ctx->err.dev;
+  Pm.prof = ctx->prof;
+  const int grid = T->info.grid;
   if (sweep) {
     // n_powers back-to-back, dependency-free passes (one launch per power)
-    const int grid = std::min<int>(ctx->sm_count, T->info.n_tiles);
-    // ring slots of the tiling's block cap (at least 2 when they fit)
-    const int64_t avail = ctx->max_smem_block - 1024;
-    const int64_t cap = T->max_block;
-    int S = static_cast<int>(std::min<int64_t>(std::max<int64_t>(avail / std::max<int64_t>(cap, 1), 1), kPipeMaxSlots));
-    const int smem = static_cast<int>(std::min<int64_t>(S * cap, avail));
-    Pm.smem_cap = static_cast<int32_t>(smem / S) & ~127;
-    Pm.n_slots = S;
     for (int i = 0; i < P; ++i) {
       PowerCfgDev Ci;
       memset(&Ci, 0, sizeof(Ci));
@@ -1341,11 +1250,14 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
       Ci.coef_re[0] = C.coef_re[i];
       Ci.coef_im[0] = C.coef_im[i];
       Pm.mode = 3;
+      Pm.items = nullptr;
+      Pm.q = 1;
       Pm.n_powers = 1;
       Pm.n_items = T->info.n_tiles;
       Pm.queue_base = ctx->queue_base;
       Pm.epoch_base = 0;
-      LMPK_TRY(launch_mpk(ctx, T, Pm, Ci, cplx, false, grid, smem, st));
+      LMPK_TRY(launch_group(ctx, Pm, Ci, cplx, exact, false, std::min(grid, T->info.n_tiles),
+                            (flags & LMPK_FLAG_NO_TMA) ? 0 : T->info.smem_bytes, st));
     }
     return LMPK_OK;
   }
@@ -1357,18 +1269,55 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   Pm.epoch_base = ctx->epoch * kEpochStride;
   Pm.queue_base = ctx->queue_base;
   Pm.n_powers = P;
-  Pm.mode = T->info.mode;
-  Pm.n_items = T->info.n_tiles * T->info.p_m;
-  LMPK_ARG_CHECK(Pm.mode == 1 || P == T->info.p_m,
-                 "streaming tiling built for p_m=%d cannot run %d powers", T->info.p_m, P);
-  const int grid = Pm.mode == 1 ? T->info.grid : std::min<int>(T->info.grid, Pm.n_items);
-  LMPK_TRY(launch_mpk(ctx, T, Pm, C, cplx, Pm.mode == 1, grid, T->info.smem_bytes, st));
-  // every successful grab takes one work unit; every grab sequence ends with
-  // exactly one failing grab: one per CTA (streaming) or per resident slot
-  const int64_t work = (Pm.mode == 1) ? T->info.n_tiles : Pm.n_items;
-  const int64_t fails = (Pm.mode == 1) ? int64_t(grid) * T->slots : grid;
-  ctx->queue_base += uint64_t(work + fails);
-  return LMPK_OK;
+  Pm.mode = 1;
+  Pm.items = T->d_items;
+  Pm.q = T->info.powers_per_item;
+  Pm.n_items = T->n_items;
+  // co-residency of all CTAs is part of the deadlock-freedom argument.
+  // LMPK_FLAG_NO_TMA: blocks are streamed from global memory by the
+  // consumers, so no slot buffers -- the unified L1 is left to the gathers.
+  const bool no_tma = (flags & LMPK_FLAG_NO_TMA) != 0;
+  return launch_group(ctx, Pm, C, cplx, exact, true, grid, no_tma ? 0 : T->info.smem_bytes, st);
+}
+
+// ---------------------------------------------------------------- compute probe
+// Each CTA stages tile blockIdx.x once and runs the row kernel `iters` times
+// (power 1 into slot 1) with no cross-CTA synchronisation: the attainable
+// per-SM rate of the tile kernel itself.
+template <bool EXACT>
+__global__ void k_probe_compute(MpkParams P, PowerCfgDev C, int iters, int n_tiles) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t bar;
+  __shared__ PowTab s_pow[1];
+  build_powtab(s_pow, P, C);
+  const int32_t t = blockIdx.x % n_tiles;
+  const int64_t ofs = P.tile_ofs[t], bytes = P.tile_ofs[t + 1] - ofs;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const bool staged = bytes <= P.smem_cap;
+  if (threadIdx.x == 0) {
+    if (staged) {
+      mbar_arrive_expect_tx(&bar, uint32_t(bytes));
+      bulk_g2s(smem_raw, P.blocks + ofs, uint32_t(bytes), &bar, policy_evict_normal());
+    } else {
+      mbar_arrive_expect_tx(&bar, 0);
+    }
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  const int32_t r0 = P.tile_row[t], rows = P.tile_row[t + 1] - r0;
+  const uint32_t E = uint32_t(P.tile_E[t]);
+  for (int it = 0; it < iters; ++it) {
+    if (staged)
+      tile_power<false, EXACT, false>(s_pow[0], P.acc, false, SmemBlk{smem_u32(smem_raw)}, r0, rows, E,
+                                      threadIdx.x >> 5, blockDim.x >> 5);
+    else
+      tile_power<false, EXACT, true>(s_pow[0], P.acc, false, GlbBlk{P.blocks + ofs}, r0, rows, E,
+                                     threadIdx.x >> 5, blockDim.x >> 5);
+  }
 }
 
 // Host-side check after the caller synchronized the stream.
@@ -1383,4 +1332,50 @@ extern "C" int lmpk_ctx_check(lmpk_ctx* ctx, void* stream) {
     ctx->queue_base = 0;
   }
   return rc;
+}
+
+// ns per 1000 nonzeros per SM of the tile kernel alone (see k_probe_compute).
+// flags: LMPK_FLAG_EXACT selects the separately rounded chain.
+extern "C" int lmpk_probe_tile_compute(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int64_t ldy,
+                                       int iters, int threads, int ctas_per_sm, double* ns_per_knnz) {
+  LMPK_ARG_CHECK(ctx && T && y && ns_per_knnz, "probe: NULL argument");
+  const bool exact = (ctas_per_sm & 0x100) != 0;
+  ctas_per_sm &= 0xff;
+  MpkParams Pm;
+  memset(&Pm, 0, sizeof(Pm));
+  Pm.blocks = T->d_blocks;
+  Pm.tile_ofs = T->d_tile_ofs;
+  Pm.tile_E = T->d_tile_E;
+  Pm.tile_row = T->d_tile_row;
+  Pm.y = y;
+  Pm.acc = y;
+  Pm.ldy = ldy;
+  Pm.smem_cap = T->max_block;
+  Pm.n_powers = 1;
+  PowerCfgDev C;
+  memset(&C, 0, sizeof(C));
+  C.out_slot[0] = 1;
+  C.in_slot[0] = 0;
+  const int smem = T->max_block;
+  auto fn = exact ? k_probe_compute<true> : k_probe_compute<false>;
+  LMPK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->max_smem_block - 1024));
+  const int grid = ctx->sm_count * ctas_per_sm;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  fn<<<grid, threads, smem>>>(Pm, C, 1, T->info.n_tiles);
+  cudaEventRecord(a);
+  fn<<<grid, threads, smem>>>(Pm, C, iters, T->info.n_tiles);
+  cudaEventRecord(b);
+  LMPK_CHECK_CUDA(cudaEventSynchronize(b));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  // nnz processed: each CTA one tile per iteration
+  const double avg_nnz = double(T->info.nnz) / std::max(1, T->info.n_tiles);
+  const double nnz = avg_nnz * grid * iters;
+  *ns_per_knnz = (ms * 1e6) * ctx->sm_count / (nnz / 1000.0);
+  return LMPK_OK;
 }

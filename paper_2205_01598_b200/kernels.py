@@ -8,6 +8,7 @@ library or a CUDA device is missing.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -68,14 +69,14 @@ class Tiling:
     """Tile geometry of one device matrix for the level-blocked kernel."""
 
     def __init__(self, a: DeviceCsr, p_m, tile_nnz=0, ctas_per_sm=0, mode_flags=0, threads=0,
-                 queue_slack=0, slots=0, stream=None):
+                 queue_slack=0, slots=0, group=0, stream=None):
         self.ctx = context()
         self.a = a
         self.p_m = int(p_m)
         h = ctypes.c_void_p()
         info = _lib.TilingInfo()
         prm = _lib.TilingParams(int(tile_nnz), int(ctas_per_sm), int(threads), int(queue_slack),
-                                int(mode_flags), int(slots))
+                                int(mode_flags), int(slots), int(group))
         check(self.ctx.lib.lmpk_tiling_create(
             self.ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val), int(p_m),
             ctypes.byref(prm), ctypes.byref(h), ctypes.byref(info), stream_handle(stream)),
@@ -86,6 +87,11 @@ class Tiling:
     @property
     def mode(self) -> str:
         return {1: "resident", 2: "streaming"}[self.info["mode"]]
+
+    @property
+    def group(self) -> int:
+        """Powers computed per staged tile block (q)."""
+        return self.info["powers_per_item"]
 
     def geometry(self):
         nt = self.info["n_tiles"]
@@ -130,12 +136,21 @@ def mpk_power_cfg(p_m):
     return power_cfg(p_m, p, p - 1, np.maximum(p - 2, 0), np.zeros(p_m, dtype=int))
 
 
+# Row sums of the level-blocked kernel: True = separately rounded multiply and
+# add (bitwise identical to the reference), False = fused multiply-add chain
+# (same order; relative error far inside the 1e-12 contract).  LMPK_EXACT=0/1
+# overrides the default.
+EXACT_DEFAULT = os.environ.get("LMPK_EXACT", "1") != "0"
+
+
 def mpk_run(tiling: Tiling, y, cfg, acc=None, use_acc=False, complex_state=False, flags=0,
-            stream=None, check_errors=True):
+            stream=None, check_errors=True, exact=None):
     """Level-blocked MPK over the slots of y (torch float64, [n_slots, n] or
     [n_slots, 2n] for complex state viewed as float64)."""
     ctx = tiling.ctx
-    f = int(flags) | (_lib.FLAG_COMPLEX if complex_state else 0)
+    if exact is None:
+        exact = EXACT_DEFAULT
+    f = int(flags) | (_lib.FLAG_COMPLEX if complex_state else 0) | (_lib.FLAG_EXACT if exact else 0)
     check(ctx.lib.lmpk_mpk_run(ctx.handle, tiling.handle, ptr(y), int(y.stride(0)), int(y.shape[0]),
                                ctypes.byref(cfg), ptr(acc), 1 if use_acc else 0, f,
                                stream_handle(stream)), "mpk_run")

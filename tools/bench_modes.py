@@ -1,4 +1,5 @@
-"""cfg2 timing of the MPK modes for the library selected by LMPK_LIB."""
+"""cfg2 timing of MPK plans: SPECS is a JSON list of
+[q, slots, tile_nnz, slack, policy, exact]; q = 0 -> sweep (k x SpMV)."""
 import os, sys, json, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2205_01598_b200 import kernels as K, _lib
@@ -18,20 +19,24 @@ def ev_time(fn, reps=10, warm=3):
         e0.record(); fn(); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1))
     return min(ts), sum(ts) / len(ts)
 ref = None
-specs = json.loads(os.environ.get("SPECS", '[["res",2,0],["stream",2,0],["sweep",2,0]]'))
-for mode, slots, tile in specs:
-    fl = _lib.FLAG_MODE_RESIDENT if mode == "res" else _lib.FLAG_MODE_STREAM
+specs = json.loads(os.environ.get("SPECS", '[[1,2,0,0,0,0],[2,2,0,0,0,0],[8,2,0,0,0,0],[0,2,0,0,0,0]]'))
+for spec in specs:
+    q, slots, tile, slack, polf, exact, notma = (list(spec) + [0] * 7)[:7]
     try:
-        t = K.Tiling(b, k, tile_nnz=tile, slots=slots, mode_flags=fl)
+        fl = (_lib.FLAG_MODE_RESIDENT if q == k else _lib.FLAG_MODE_STREAM) | (_lib.FLAG_NO_TMA if notma else 0)
+        t = K.Tiling(b, k, tile_nnz=tile, slots=slots, mode_flags=fl, queue_slack=slack, group=max(q, 1))
         cfg = K.mpk_power_cfg(k)
         y = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); y[0] = x
-        f = _lib.FLAG_SWEEP if mode == "sweep" else 0
-        tmin, tmean = ev_time(lambda: K.mpk_run(t, y, cfg, flags=f, check_errors=False))
-        K.mpk_run(t, y, cfg, flags=f)
+        f = (_lib.FLAG_SWEEP if q == 0 else 0) | (polf << 8) | (_lib.FLAG_NO_TMA if notma else 0)
+        run = lambda: K.mpk_run(t, y, cfg, flags=f, check_errors=False, exact=bool(exact))
+        tmin, tmean = ev_time(run)
+        K.mpk_run(t, y, cfg, flags=f, exact=True)
         if ref is None: ref = y.clone()
-        print(json.dumps(dict(lib=os.path.basename(os.environ.get("LMPK_LIB", "default")), mode=mode, slots=slots,
-              tile=t.info["tile_nnz_cap"], n_tiles=t.info["n_tiles"], ms=round(tmin, 4), ms_mean=round(tmean, 4),
-              gflops=round(F / tmin / 1e6), ro_frac=round(Q_ro / (tmin * 1e-3) / 6531.6e9, 4),
-              bitwise=bool(torch.equal(y, ref)))), flush=True)
+        K.mpk_run(t, y, cfg, flags=f, exact=bool(exact))
+        err = float(max(((y[i] - ref[i]).norm() / ref[i].norm()).item() for i in range(1, k + 1)))
+        print(json.dumps(dict(q=q, notma=notma, slots=t.info["slots"], pol=polf, exact=exact, slack=t.info["queue_slack"],
+              tile=t.info["tile_nnz_cap"], n_tiles=t.info["n_tiles"], D=t.info["max_fwd_reach"],
+              ms=round(tmin, 4), ms_mean=round(tmean, 4), gflops=round(F / tmin / 1e6),
+              ro_frac=round(Q_ro / (tmin * 1e-3) / 6531.6e9, 4), rel_err=err)), flush=True)
     except Exception as e:
-        print(json.dumps(dict(mode=mode, slots=slots, err=str(e)[:200])), flush=True)
+        print(json.dumps(dict(spec=spec, err=str(e)[:300])), flush=True)

@@ -1,0 +1,32 @@
+"""Phase counters of the group-walk kernel on cfg2 (LMPK_PROFILE=1).
+SPECS: JSON list of [q, slots, tile_nnz, slack]; q = 0 -> sweep."""
+import ctypes, json, os, sys
+os.environ["LMPK_PROFILE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2205_01598_b200 import kernels as K, _lib
+from oracle import levelmpk_oracle as O
+N = int(os.environ.get("N", "200")); k = 8
+rp, c, v = O.gen_stencil_3d(N); n = rp.shape[0] - 1
+a = K.DeviceCsr.from_host(rp, c, v)
+perm, inv, lp = K.bfs_levels(a, 0)
+b = K.permute_symmetric(a, perm, inv)
+ctx = _lib.context()
+buf = (ctypes.c_ulonglong * 16)()
+for q, slots, tile, slack in json.loads(os.environ.get("SPECS", '[[1,2,0,0],[2,2,0,0],[0,2,0,0]]')):
+    fl = _lib.FLAG_MODE_RESIDENT if q == k else _lib.FLAG_MODE_STREAM
+    t = K.Tiling(b, k, tile_nnz=tile, slots=slots, mode_flags=fl, group=max(q, 1), queue_slack=slack)
+    y = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); y[0] = 1.0
+    cfg = K.mpk_power_cfg(k); f = _lib.FLAG_SWEEP if q == 0 else 0
+    K.mpk_run(t, y, cfg, flags=f); torch.cuda.synchronize()
+    ctx.lib.lmpk_ctx_profile(ctx.handle, buf, 1)
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(); K.mpk_run(t, y, cfg, flags=f); e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ctx.lib.lmpk_ctx_profile(ctx.handle, buf, 1)
+    v = list(buf)
+    nw = v[2] or 1
+    print(json.dumps(dict(q=q, slots=slots, tiles=t.info["n_tiles"], ms=round(ms, 3),
+        cons_wait_frac=round(v[0] / max(v[0] + v[1], 1), 3), cons_compute_us_per_item_warp=round(v[1] / nw / 1e3, 3),
+        cons_wait_us_per_item_warp=round(v[0] / nw / 1e3, 3), polls=v[3], notready_frac=round(v[4] / max(v[3], 1), 3),
+        prod_alive_ms_per_cta=round(v[5] / 148 / 1e6, 3), items_grabbed=v[6])), flush=True)
