@@ -1,0 +1,229 @@
+"""Multi-GPU MPK: contiguous level-range shards with a depth-k halo.
+
+The reference has no multi-process code; this module
+is the greenfield multi-GPU layer north_star asks for.  It rests on level
+confinement (Eq. 4 of the paper; pkg/src/levelmpk/levels.py, test_levels.py:
+58-88): in the level-permuted matrix a row of level l only couples to levels
+l-1..l+1.  Hence:
+
+  * rank g owns a contiguous LEVEL range [a_g, b_g), balanced by nnz, i.e. a
+    contiguous row range of the permuted matrix;
+  * its WINDOW is levels [a_g - k, b_g + k) (clamped): to produce y_1..y_k on
+    the owned rows it needs y_0 on the window only, and the window matrix is
+    the contiguous row block of the permuted matrix with the columns outside
+    the window dropped.  Rows whose entries were dropped sit in the outermost
+    window levels; their error moves inward one level per power, so after p
+    powers levels [a_g - k + p, b_g + k - p) are exact -- the owned rows at
+    every power p <= k (bitwise identical to the single-GPU result: same
+    rows, same entries in the same order);
+  * y_0 halos are exchanged ONCE per MPK call: the left halo [win_lo, own_lo)
+    comes from rank g-1, the right halo [own_hi, win_hi) from rank g+1, as one
+    batched NCCL send/recv group over NVLink (torch.distributed P2P ops);
+  * the redundant work is the halo rows computed at every power:
+    2 * k * (nnz(window) - nnz(owned)) flops per call, reported by
+    ``LevelShards.redundant_flops``.
+
+Each rank needs at least k levels so the halo comes from direct neighbours
+only; ``LevelShards`` raises ValueError otherwise.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    level_lo: int  # owned levels [level_lo, level_hi)
+    level_hi: int
+    own_lo: int    # owned rows (permuted order)
+    own_hi: int
+    win_lo: int    # window rows: levels [level_lo - k, level_hi + k) clamped
+    win_hi: int
+
+    @property
+    def n_own(self) -> int:
+        return self.own_hi - self.own_lo
+
+    @property
+    def n_win(self) -> int:
+        return self.win_hi - self.win_lo
+
+    @property
+    def own_offset(self) -> int:
+        """First owned row inside the window."""
+        return self.own_lo - self.win_lo
+
+    @property
+    def left_halo(self) -> int:
+        return self.own_lo - self.win_lo
+
+    @property
+    def right_halo(self) -> int:
+        return self.win_hi - self.own_hi
+
+
+class LevelShards:
+    """Partition of a level-permuted matrix into `world` level ranges."""
+
+    def __init__(self, level_ptr, level_nnz, world: int, k: int):
+        level_ptr = np.asarray(level_ptr, dtype=np.int64)
+        level_nnz = np.asarray(level_nnz, dtype=np.int64)
+        L = int(level_ptr.shape[0] - 1)
+        if world < 1:
+            raise ValueError("world must be >= 1")
+        if k < 1:
+            raise ValueError("p_m must be >= 1")
+        if level_nnz.shape[0] != L:
+            raise ValueError("level_nnz length must equal the number of levels")
+        if world > 1 and L < world * k:
+            raise ValueError(f"{L} levels cannot give {world} shards of >= k={k} levels "
+                             "(depth-k halos must come from direct neighbours)")
+        self.world, self.k, self.n_levels = world, k, L
+        self.level_ptr = level_ptr
+        self.level_nnz = level_nnz
+        bounds = self._balanced_bounds(level_nnz, world, k)
+        self.level_bounds = bounds
+        self.shards = []
+        for g in range(world):
+            a, b = int(bounds[g]), int(bounds[g + 1])
+            wa, wb = max(0, a - k), min(L, b + k)
+            self.shards.append(Shard(g, a, b, int(level_ptr[a]), int(level_ptr[b]),
+                                     int(level_ptr[wa]), int(level_ptr[wb])))
+
+    @staticmethod
+    def _balanced_bounds(level_nnz, world, k):
+        """Level boundaries with ~equal owned nnz and >= k levels per shard."""
+        L = level_nnz.shape[0]
+        if world == 1:
+            return np.array([0, L], dtype=np.int64)
+        csum = np.concatenate([[0], np.cumsum(level_nnz)])
+        total = csum[-1]
+        bounds = [0]
+        for g in range(1, world):
+            target = total * g / world
+            b = int(np.searchsorted(csum, target, side="left"))
+            lo = bounds[-1] + k                # >= k levels for shard g-1
+            hi = L - (world - g) * k           # leave >= k levels for the rest
+            bounds.append(int(min(max(b, lo), hi)))
+        bounds.append(L)
+        return np.array(bounds, dtype=np.int64)
+
+    def __getitem__(self, g) -> Shard:
+        return self.shards[g]
+
+    def nnz_range(self, lo_level, hi_level) -> int:
+        return int(self.level_nnz[lo_level:hi_level].sum())
+
+    def window_nnz(self, g) -> int:
+        s = self.shards[g]
+        return self.nnz_range(max(0, s.level_lo - self.k), min(self.n_levels, s.level_hi + self.k))
+
+    def owned_nnz(self, g) -> int:
+        s = self.shards[g]
+        return self.nnz_range(s.level_lo, s.level_hi)
+
+    def redundant_flops(self, g=None) -> int:
+        """2*k*(window nnz - owned nnz): halo rows recomputed at every power
+        (an upper bound: dropped out-of-window entries are not computed)."""
+        gs = range(self.world) if g is None else [g]
+        return int(sum(2 * self.k * (self.window_nnz(i) - self.owned_nnz(i)) for i in gs))
+
+    def halo_bytes(self, g, width=1) -> int:
+        s = self.shards[g]
+        return 8 * width * (s.left_halo + s.right_halo)
+
+
+def window_csr(row_ptr, col, val, lo: int, hi: int):
+    """Rows [lo, hi) of a CRS matrix with columns shifted by -lo and the
+    entries whose column falls outside [lo, hi) dropped (entry order kept)."""
+    row_ptr = np.asarray(row_ptr)
+    col = np.asarray(col)
+    val = np.asarray(val)
+    e0, e1 = int(row_ptr[lo]), int(row_ptr[hi])
+    c = col[e0:e1].astype(np.int64)
+    keep = (c >= lo) & (c < hi)
+    lens = np.diff(row_ptr[lo:hi + 1].astype(np.int64))
+    row_id = np.repeat(np.arange(hi - lo), lens)
+    kept_per_row = np.bincount(row_id[keep], minlength=hi - lo)
+    rp = np.zeros(hi - lo + 1, dtype=np.int32)
+    np.cumsum(kept_per_row, out=rp[1:])
+    return rp, (c[keep] - lo).astype(np.int32), np.ascontiguousarray(val[e0:e1][keep])
+
+
+class CudaWindowMpk:
+    """Local MPK on one rank's window: the single-GPU level-blocked kernel."""
+
+    def __init__(self, rp, col, val, k, **tiling_kw):
+        from . import kernels as K
+
+        self.K = K
+        self.k = k
+        self.a = K.DeviceCsr.from_host(rp, col, val)
+        self.tiling = K.Tiling(self.a, k, **tiling_kw)
+        self.cfg = K.mpk_power_cfg(k)
+
+    def __call__(self, y, check_errors=True):
+        self.K.mpk_run(self.tiling, y, self.cfg, check_errors=check_errors)
+        return y
+
+
+class DistMpk:
+    """Level-range sharded MPK on one rank of a torch.distributed group.
+
+    ``run(x_own)`` takes y_0 on the owned rows (permuted order) and returns
+    the [k+1, n_own] block of y_0..y_k for those rows.  ``local`` computes the
+    window MPK in place on a [k+1, n_win] tensor; the default is the CUDA
+    kernel (CudaWindowMpk); tests inject a CPU computation with gloo.
+    """
+
+    def __init__(self, row_ptr, col, val, level_ptr, level_nnz, k, rank, world, group=None,
+                 device=None, local=None, **tiling_kw):
+        import torch
+
+        self.torch = torch
+        self.rank, self.world, self.k, self.group = rank, world, k, group
+        self.shards = LevelShards(level_ptr, level_nnz, world, k)
+        self.shard = self.shards[rank]
+        s = self.shard
+        rp, c, v = window_csr(row_ptr, col, val, s.win_lo, s.win_hi)
+        self.window = (rp, c, v)
+        self.device = torch.device("cpu") if device is None else torch.device(device)
+        self.local = local if local is not None else CudaWindowMpk(rp, c, v, k, **tiling_kw)
+        self.y = torch.zeros((k + 1, s.n_win), dtype=torch.float64, device=self.device)
+
+    def exchange(self, y0):
+        """Fill the halo rows of y0 (window-local) from the neighbour ranks."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+
+        s, shards = self.shard, self.shards
+        ops = []
+        o0, o1 = s.own_offset, s.own_offset + s.n_own
+        if self.rank > 0:
+            left = shards[self.rank - 1]
+            # my first rows are rank-1's right halo; rank-1's last rows are my left halo
+            ops.append(dist.P2POp(dist.isend, y0[o0:o0 + left.right_halo], self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, y0[0:s.left_halo], self.rank - 1, self.group))
+        if self.rank < self.world - 1:
+            right = shards[self.rank + 1]
+            ops.append(dist.P2POp(dist.isend, y0[o1 - right.left_halo:o1], self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, y0[o1:o1 + s.right_halo], self.rank + 1, self.group))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def run(self, x_own, check_errors=True):
+        s = self.shard
+        y = self.y
+        y[0, s.own_offset:s.own_offset + s.n_own].copy_(self.torch.as_tensor(x_own, device=self.device))
+        self.exchange(y[0])
+        self.local(y, check_errors=check_errors)
+        return y[:, s.own_offset:s.own_offset + s.n_own]
+
+    @property
+    def redundant_flops(self) -> int:
+        return self.shards.redundant_flops(self.rank)

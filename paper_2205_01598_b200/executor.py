@@ -143,6 +143,34 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
     return e0.elapsed_time(e1) * 1e-3
 
 
+_PLAN_FIELDS = ("variant", "p_m", "workers", "n_rows", "items", "barrier", "row_start", "row_end",
+                "power", "chunks", "bnd_point", "check_ptr", "check_item", "check_kind",
+                "out_slot", "in_slot", "prev_slot", "kernel", "acc_coef")
+
+
+def adopt_plan(ref_plan) -> ExecPlan:
+    """An ExecPlan of this package from a reference ``levelmpk.plan.ExecPlan``
+    (plan.py:41-49 fields) -- the adapter behind a ``LEVELMPK_BACKEND=cuda``
+    seam in the reference.  The permuted matrix is re-wrapped
+    (validated) and uploaded on first use; preprocessing objects are dropped."""
+    if isinstance(ref_plan, ExecPlan):
+        return ref_plan
+    kw = {f: getattr(ref_plan, f) for f in _PLAN_FIELDS}
+    a = ref_plan.a
+    kw["a"] = CsrMatrix(a.n_rows, a.row_ptr, a.col, a.val)
+    for f in ("out_slot", "in_slot", "prev_slot", "kernel", "acc_coef"):
+        if kw[f] is not None:
+            kw[f] = np.asarray(kw[f])
+    n_items = len(kw["items"])
+    defaults = {"out_slot": np.asarray(kw["power"]), "in_slot": np.asarray(kw["power"]) - 1,
+                "prev_slot": np.maximum(np.asarray(kw["power"]) - 2, 0),
+                "kernel": np.zeros(n_items, dtype=np.int64), "acc_coef": np.zeros(n_items)}
+    for f, v in defaults.items():
+        if kw[f] is None:
+            kw[f] = v
+    return ExecPlan(**kw)
+
+
 def run_plan(plan: ExecPlan, x=None, y=None, acc=None, use_acc=False, timeout=None):
     """Execute a plan on the GPU; returns an MpkResult with the power vectors.
 

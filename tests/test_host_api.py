@@ -241,3 +241,25 @@ def test_gershgorin_and_scaling():
 
 def test_backend_seam():
     assert lm.backend_name() == "cuda" and not lm.USING_NUMBA and lm.USING_CUDA
+
+
+def test_adopt_reference_plan_fields():
+    """executor.adopt_plan: the adapter behind a LEVELMPK_BACKEND=cuda seam in
+    the reference copies a reference ExecPlan (plan.py:41-49)
+    field by field, filling the reference's None kernel-slot defaults."""
+    from types import SimpleNamespace
+
+    from paper_2205_01598_b200.executor import _PLAN_FIELDS, adopt_plan, build_baseline_plan
+
+    a = lm.gen_stencil_2d7pt(6, 5)
+    ours = build_baseline_plan(a, 3, 2)
+    ref_like = SimpleNamespace(**{f: getattr(ours, f) for f in _PLAN_FIELDS})
+    ref_like.a = SimpleNamespace(n_rows=a.n_rows, row_ptr=a.row_ptr, col=a.col, val=a.val)
+    for f in ("out_slot", "in_slot", "prev_slot", "kernel", "acc_coef"):
+        setattr(ref_like, f, None)
+    p = adopt_plan(ref_like)
+    assert p.a == a and p.variant == ours.variant and p.n_items == ours.n_items
+    assert np.array_equal(p.out_slot, ours.power) and np.array_equal(p.in_slot, ours.power - 1)
+    assert np.array_equal(p.prev_slot, np.maximum(ours.power - 2, 0))
+    assert not np.any(p.kernel) and not np.any(p.acc_coef)
+    assert adopt_plan(p) is p
