@@ -129,6 +129,7 @@ typedef struct lmpk_tiling_info {
   int64_t block_bytes;   /* size of the tile-SELL-32 copy of the matrix         */
   int32_t powers_per_item; /* q: powers computed per staged tile block          */
   int32_t slots;         /* R: staged items held per CTA                        */
+  int32_t x_staged_tiles; /* tiles whose gathers come from a staged x buffer    */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */
@@ -137,7 +138,9 @@ typedef struct lmpk_tiling_params {
   int32_t ctas_per_sm;   /* reserved (one CTA per SM)                           */
   int32_t threads;       /* reserved (1 producer + LMPK_NC consumer warps)      */
   int32_t queue_slack;   /* streaming: key spacing M - D (tiles)                */
-  int32_t mode_flags;    /* LMPK_FLAG_MODE_STREAM / LMPK_FLAG_MODE_RESIDENT     */
+  int32_t mode_flags;    /* LMPK_FLAG_MODE_STREAM / LMPK_FLAG_MODE_RESIDENT;    */
+                         /* LMPK_FLAG_COMPLEX: tiling for complex vectors (no */
+                         /* x staging); LMPK_FLAG_NO_TMA: unstaged blocks     */
   int32_t slots;         /* staged items held per CTA (<= 4)                    */
   int32_t powers_per_item; /* q: powers per staged tile (0 = plan; MODE_RESIDENT */
                            /* forces q = p_m, MODE_STREAM defaults to q = 1)   */

@@ -49,7 +49,7 @@ class TilingInfo(ctypes.Structure):
         ("block", _i32), ("smem_bytes", _i32), ("tile_nnz_cap", _i32),
         ("max_fwd_reach", _i32), ("chain_reach", _i32), ("max_row_nnz", _i32),
         ("queue_slack", _i32), ("nnz", _i64), ("block_bytes", _i64),
-        ("powers_per_item", _i32), ("slots", _i32),
+        ("powers_per_item", _i32), ("slots", _i32), ("x_staged_tiles", _i32),
     ]
 
     def as_dict(self):

@@ -146,8 +146,11 @@ extern "C" int64_t lmpk_ctx_launch_count(const lmpk_ctx* c) { return c ? c->laun
 
 // Phase counters of the pipelined kernels (LMPK_PROFILE=1 at ctx creation):
 // [0] consumer ns waiting for work, [1] consumer ns computing, [2] items
-// consumed (per warp), [3] producer dependency polls, [4] polls with nothing
-// ready, [5] producer ns alive, [6] items issued.  reset != 0 zeroes them.
+// consumed (per warp), [3] producer dependency poll rounds, [4] rounds with
+// nothing ready, [5] producer ns alive, [6] items grabbed, [7] ns TMA issue ->
+// staged observed, [8] ns staged -> pushed (dependency wait), [9] ns last push
+// -> slot free observed (compute + publish), [10] producer loop iterations,
+// [12] item slot cycles.  reset != 0 zeroes them.
 extern "C" int lmpk_ctx_profile(lmpk_ctx* c, unsigned long long* out, int reset) {
   LMPK_ARG_CHECK(c && out, "lmpk_ctx_profile: NULL argument");
   if (!c->prof) {

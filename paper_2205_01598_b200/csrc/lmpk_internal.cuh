@@ -85,6 +85,10 @@ struct lmpk_tiling {
   int32_t* d_tile_E = nullptr;     // [n_tiles] padded entries (multiple of 32) per tile
   int32_t* d_dep_lo = nullptr;     // [n_tiles]
   int32_t* d_dep_hi = nullptr;     // [n_tiles]
+  int32_t* d_tile_nseg = nullptr;  // [n_tiles] x-segments (0: global columns)
+  int32_t* d_tile_xent = nullptr;  // [n_tiles] x-buffer entries
+  int32_t staged_tiles = 0, max_xent = 0;
+  int64_t xoff = 0;                // byte offset of the x buffer in a slot (0: no staging)
   int32_t* d_items = nullptr;      // item queue order, packed (t << 8) | power group
   int32_t n_items = 0;
   uint32_t* d_progress = nullptr;  // [n_tiles] epoch-tagged power counters
@@ -168,6 +172,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
       "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// Same with a 32-bit shared-memory destination address.
+__device__ __forceinline__ void bulk_g2s_a(uint32_t dst_smem, const void* src_gmem, uint32_t bytes,
+                                           uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(dst_smem),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }

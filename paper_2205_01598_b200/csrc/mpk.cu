@@ -60,7 +60,7 @@ constexpr int kWorkRing = 8;
 #define LMPK_NC 24
 #endif
 constexpr int kConsumers = LMPK_NC;  // consumer warps per CTA (+1 producer warp)
-constexpr int kBlockThreads = 32 * (kConsumers + 1);
+constexpr int kBlockThreads = 32 * (kConsumers + kMaxSlots);  // launched with NC + R warps
 
 struct PowerCfgDev {
   int32_t out_slot[LMPK_MAX_POWERS];
@@ -78,6 +78,8 @@ struct MpkParams {
   const int32_t* tile_row;
   const int32_t* dep_lo;
   const int32_t* dep_hi;
+  const int32_t* tile_nseg;  // x-segments per tile (0: global columns)
+  const int32_t* tile_xent;  // x-buffer entries per tile
   const int32_t* items;  // packed (t << 8) | g in queue order (NULL: item i = tile i, g = 0)
   double* y;
   int64_t ldy;
@@ -92,6 +94,9 @@ struct MpkParams {
   int32_t q;         // powers per item
   int32_t mode;      // 1 group walk, 3 sweep (one power, no deps)
   int32_t smem_cap;  // bytes of one slot
+  int32_t xoff;      // byte offset of the x buffer inside a slot
+  int32_t blk_cap;   // bytes of a slot available to the staged block
+  int32_t xmode;     // 0 no x staging, 1 TMA (aligned vectors), 2 cooperative copy
   int32_t n_slots;   // R
   int32_t flags;     // LMPK_FLAG_* (NO_TMA, policy bits 8-9)
   int* err;          // host-mapped
@@ -106,13 +111,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __host__ __device__ inline int64_t align16(int64_t b) { return (b + 15) & ~int64_t(15); }
 
-// Block layout of a tile with ns slices and E entries (E = 32 * sum of widths):
-//   [rec int2 x ns] [lens uint16 x 32*ns] | align16 | [col int32 x E] [val f64 x E]
+// Block layout of a tile with ns slices, E entries (E = 32 * sum of widths)
+// and nseg x-segments:
+//   [rec int2 x ns] [lens uint16 x 32*ns] | align16 | [seg int4 x nseg]
+//   [col int32 x E] [val f64 x E]
 // rec[s] = {byte offset of slice s's first column index in the block,
 //           w | wmin << 16} (w = longest row, wmin = shortest row).
-__host__ __device__ inline int64_t blk_col_off(int32_t ns) { return align16(int64_t(ns) * 72); }
-__host__ __device__ inline int64_t blk_bytes(int32_t ns, int64_t E) {
-  return (blk_col_off(ns) + E * 12 + 127) & ~int64_t(127);
+// seg[j] = {first vector entry, entry count, local base, 0}: the tile's
+// columns covered by even-aligned runs of the gathered vector.  When nseg > 0
+// the columns are LOCAL indices into the slot's x buffer, which the producer
+// fills with one bulk copy per run once the dependencies of a power are met
+// (gathers then come from shared memory); nseg == 0 keeps global columns.
+constexpr int kMaxSegs = 64;
+__host__ __device__ inline int64_t blk_seg_off(int32_t ns) { return align16(int64_t(ns) * 72); }
+__host__ __device__ inline int64_t blk_col_off(int32_t ns, int32_t nseg) {
+  return blk_seg_off(ns) + int64_t(nseg) * 16;
+}
+__host__ __device__ inline int64_t blk_bytes(int32_t ns, int64_t E, int32_t nseg) {
+  return (blk_col_off(ns, nseg) + E * 12 + 127) & ~int64_t(127);
 }
 
 // Entry index of (lane, j) inside a slice of width w starting at entry `base`:
@@ -126,6 +142,28 @@ __host__ __device__ inline int64_t chunk_entry(int64_t base, int w, int lane, in
 }
 
 // ---------------------------------------------------------------- row kernel
+// Gather sources of the row kernel: the vector in global memory (global
+// columns) or the slot's x buffer in shared memory (local columns).
+struct GatherGlobal {
+  const char* base;
+  __device__ __forceinline__ double d(int32_t c) const { return ldg_f64(base + uint64_t(uint32_t(c)) * 8u); }
+  __device__ __forceinline__ double2 d2(int32_t c) const {
+    return ldg_f64x2(base + uint64_t(uint32_t(c)) * 16u);
+  }
+};
+struct GatherSmem {
+  uint32_t base;
+  __device__ __forceinline__ double d(int32_t c) const {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + uint32_t(c) * 8u));
+    return v;
+  }
+  __device__ __forceinline__ double2 d2(int32_t c) const {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(base + uint32_t(c) * 16u));
+    return v;
+  }
+};
 // Per-power operands, built once per launch in shared memory (the consumers
 // would otherwise re-derive them from the constant bank for every item).
 struct PowTab {
@@ -169,9 +207,9 @@ __device__ __forceinline__ void stg_f64x2(double* p, double2 v) {
 // Row sum of one slice of compile-time width W <= 8 (real vectors): all column
 // loads, then all gathers, then the values and the ordered chain.  cb/vb are
 // the slice's column/value byte offsets in the block, l4 = 4*lane.
-template <int W, bool EXACT, bool FULL, class Blk>
+template <int W, bool EXACT, bool FULL, class Blk, class G, int PROBE = 0>
 __device__ __forceinline__ double slice_real_w(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
-                                               const char* ybase, int len) {
+                                               const G& g, int len) {
   constexpr int Q = W >> 2, PR = (W >> 1) & 1, SG = W & 1;
   int32_t c[W];
 #pragma unroll
@@ -190,7 +228,16 @@ __device__ __forceinline__ double slice_real_w(const Blk& B, uint32_t cb, uint32
   if constexpr (SG) c[W - 1] = B.i1(cb + Q * 512 + PR * 256 + l4);
   double x[W];
 #pragma unroll
-  for (int j = 0; j < W; ++j) x[j] = ldg_f64(ybase + uint64_t(uint32_t(c[j])) * 8u);
+  for (int j = 0; j < W; ++j) {
+    // PROBE (compute probe only): 1 = gathers confined to 8 KB, 2 = coalesced
+    // gathers, 3 = no gathers
+    if constexpr (PROBE == 1) c[j] &= 1023;
+    if constexpr (PROBE == 2) c[j] = int32_t(l4 >> 2) + 32 * j;
+    if constexpr (PROBE == 3)
+      x[j] = __int_as_float(c[j]);
+    else
+      x[j] = g.d(c[j]);
+  }
   double v[W];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
@@ -218,17 +265,17 @@ __device__ __forceinline__ double slice_real_w(const Blk& B, uint32_t cb, uint32
 }
 
 // Any width (real vectors): a loop over quads plus the pair/single tail.
-template <bool EXACT, class Blk>
+template <bool EXACT, class Blk, class G>
 __device__ __noinline__ double slice_real_any(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
-                                              const char* ybase, int w, int len) {
+                                              const G& g, int w, int len) {
   const int Q = w >> 2;
   double t = 0.0;
   for (int q = 0; q < Q; ++q) {
     const int4 c4 = B.i4(cb + q * 512 + 4 * l4);
-    const double x0 = ldg_f64(ybase + uint64_t(uint32_t(c4.x)) * 8u);
-    const double x1 = ldg_f64(ybase + uint64_t(uint32_t(c4.y)) * 8u);
-    const double x2 = ldg_f64(ybase + uint64_t(uint32_t(c4.z)) * 8u);
-    const double x3 = ldg_f64(ybase + uint64_t(uint32_t(c4.w)) * 8u);
+    const double x0 = g.d(c4.x);
+    const double x1 = g.d(c4.y);
+    const double x2 = g.d(c4.z);
+    const double x3 = g.d(c4.w);
     const double2 a = B.d2(vb + q * 1024 + 8 * l4), b = B.d2(vb + q * 1024 + 8 * l4 + 16);
     const int j = 4 * q;
     madd_if<EXACT>(t, a.x, x0, j, len);
@@ -239,15 +286,15 @@ __device__ __noinline__ double slice_real_any(const Blk& B, uint32_t cb, uint32_
   const int PR = (w >> 1) & 1;
   if (PR) {
     const int2 c2 = B.i2(cb + Q * 512 + 2 * l4);
-    const double x0 = ldg_f64(ybase + uint64_t(uint32_t(c2.x)) * 8u);
-    const double x1 = ldg_f64(ybase + uint64_t(uint32_t(c2.y)) * 8u);
+    const double x0 = g.d(c2.x);
+    const double x1 = g.d(c2.y);
     const double2 a = B.d2(vb + Q * 1024 + 4 * l4);
     madd_if<EXACT>(t, a.x, x0, 4 * Q, len);
     madd_if<EXACT>(t, a.y, x1, 4 * Q + 1, len);
   }
   if (w & 1) {
     const int32_t c = B.i1(cb + Q * 512 + PR * 256 + l4);
-    const double x0 = ldg_f64(ybase + uint64_t(uint32_t(c)) * 8u);
+    const double x0 = g.d(c);
     const double a = B.d1(vb + Q * 1024 + PR * 512 + 2 * l4);
     madd_if<EXACT>(t, a, x0, w - 1, len);
   }
@@ -255,17 +302,17 @@ __device__ __noinline__ double slice_real_any(const Blk& B, uint32_t cb, uint32_
 }
 
 // Complex vectors (real matrix): t += v * x per component, storage order.
-template <bool EXACT, class Blk>
+template <bool EXACT, class Blk, class G>
 __device__ __forceinline__ double2 slice_cplx(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
-                                              const char* ybase, int w, int len) {
+                                              const G& g, int w, int len) {
   double tr = 0.0, ti = 0.0;
   const int Q = w >> 2;
   for (int q = 0; q < Q; ++q) {
     const int4 c4 = B.i4(cb + q * 512 + 4 * l4);
-    const double2 x0 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.x)) * 16u);
-    const double2 x1 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.y)) * 16u);
-    const double2 x2 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.z)) * 16u);
-    const double2 x3 = ldg_f64x2(ybase + uint64_t(uint32_t(c4.w)) * 16u);
+    const double2 x0 = g.d2(c4.x);
+    const double2 x1 = g.d2(c4.y);
+    const double2 x2 = g.d2(c4.z);
+    const double2 x3 = g.d2(c4.w);
     const double2 a = B.d2(vb + q * 1024 + 8 * l4), b = B.d2(vb + q * 1024 + 8 * l4 + 16);
     const int j = 4 * q;
     madd_if<EXACT>(tr, a.x, x0.x, j, len);
@@ -280,8 +327,8 @@ __device__ __forceinline__ double2 slice_cplx(const Blk& B, uint32_t cb, uint32_
   const int PR = (w >> 1) & 1;
   if (PR) {
     const int2 c2 = B.i2(cb + Q * 512 + 2 * l4);
-    const double2 x0 = ldg_f64x2(ybase + uint64_t(uint32_t(c2.x)) * 16u);
-    const double2 x1 = ldg_f64x2(ybase + uint64_t(uint32_t(c2.y)) * 16u);
+    const double2 x0 = g.d2(c2.x);
+    const double2 x1 = g.d2(c2.y);
     const double2 a = B.d2(vb + Q * 1024 + 4 * l4);
     madd_if<EXACT>(tr, a.x, x0.x, 4 * Q, len);
     madd_if<EXACT>(ti, a.x, x0.y, 4 * Q, len);
@@ -290,7 +337,7 @@ __device__ __forceinline__ double2 slice_cplx(const Blk& B, uint32_t cb, uint32_
   }
   if (w & 1) {
     const int32_t c = B.i1(cb + Q * 512 + PR * 256 + l4);
-    const double2 x0 = ldg_f64x2(ybase + uint64_t(uint32_t(c)) * 16u);
+    const double2 x0 = g.d2(c);
     const double a = B.d1(vb + Q * 1024 + PR * 512 + 2 * l4);
     madd_if<EXACT>(tr, a, x0.x, w - 1, len);
     madd_if<EXACT>(ti, a, x0.y, w - 1, len);
@@ -298,55 +345,132 @@ __device__ __forceinline__ double2 slice_cplx(const Blk& B, uint32_t cb, uint32_
   return make_double2(tr, ti);
 }
 
-template <bool EXACT, bool FULL, class Blk>
-__device__ __forceinline__ double slice_real(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
-                                             const char* ybase, int w, int len) {
+// Two slices of the same width W <= 8 at once (one warp): both slices'
+// gathers are in flight together, so the second slice's L2 latency hides
+// behind the first one's.
+template <int W, bool EXACT, bool FULL, class Blk, class G>
+__device__ __forceinline__ double2 slice_real_w2(const Blk& B, uint32_t cb0, uint32_t vb0, uint32_t cb1,
+                                                 uint32_t vb1, uint32_t l4, const G& g, int len0,
+                                                 int len1) {
+  constexpr int Q = W >> 2, PR = (W >> 1) & 1, SG = W & 1;
+  int32_t c0[W], c1[W];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int4 a = B.i4(cb0 + q * 512 + 4 * l4), b = B.i4(cb1 + q * 512 + 4 * l4);
+    c0[4 * q] = a.x, c0[4 * q + 1] = a.y, c0[4 * q + 2] = a.z, c0[4 * q + 3] = a.w;
+    c1[4 * q] = b.x, c1[4 * q + 1] = b.y, c1[4 * q + 2] = b.z, c1[4 * q + 3] = b.w;
+  }
+  if constexpr (PR) {
+    const int2 a = B.i2(cb0 + Q * 512 + 2 * l4), b = B.i2(cb1 + Q * 512 + 2 * l4);
+    c0[4 * Q] = a.x, c0[4 * Q + 1] = a.y;
+    c1[4 * Q] = b.x, c1[4 * Q + 1] = b.y;
+  }
+  if constexpr (SG) {
+    c0[W - 1] = B.i1(cb0 + Q * 512 + PR * 256 + l4);
+    c1[W - 1] = B.i1(cb1 + Q * 512 + PR * 256 + l4);
+  }
+  double x0[W], x1[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) x0[j] = g.d(c0[j]);
+#pragma unroll
+  for (int j = 0; j < W; ++j) x1[j] = g.d(c1[j]);
+  double t0 = 0.0, t1 = 0.0;
+  {
+    double v[W];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const double2 a = B.d2(vb0 + q * 1024 + 8 * l4), b = B.d2(vb0 + q * 1024 + 8 * l4 + 16);
+      v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = b.x, v[4 * q + 3] = b.y;
+    }
+    if constexpr (PR) {
+      const double2 a = B.d2(vb0 + Q * 1024 + 4 * l4);
+      v[4 * Q] = a.x, v[4 * Q + 1] = a.y;
+    }
+    if constexpr (SG) v[W - 1] = B.d1(vb0 + Q * 1024 + PR * 512 + 2 * l4);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      if constexpr (FULL)
+        t0 = madd<EXACT>(t0, v[j], x0[j]);
+      else
+        madd_if<EXACT>(t0, v[j], x0[j], j, len0);
+    }
+  }
+  {
+    double v[W];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const double2 a = B.d2(vb1 + q * 1024 + 8 * l4), b = B.d2(vb1 + q * 1024 + 8 * l4 + 16);
+      v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = b.x, v[4 * q + 3] = b.y;
+    }
+    if constexpr (PR) {
+      const double2 a = B.d2(vb1 + Q * 1024 + 4 * l4);
+      v[4 * Q] = a.x, v[4 * Q + 1] = a.y;
+    }
+    if constexpr (SG) v[W - 1] = B.d1(vb1 + Q * 1024 + PR * 512 + 2 * l4);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      if constexpr (FULL)
+        t1 = madd<EXACT>(t1, v[j], x1[j]);
+      else
+        madd_if<EXACT>(t1, v[j], x1[j], j, len1);
+    }
+  }
+  return make_double2(t0, t1);
+}
+
+template <bool EXACT, bool FULL, class Blk, class G>
+__device__ __forceinline__ double2 slice_real_pair(const Blk& B, uint32_t cb0, uint32_t vb0, uint32_t cb1,
+                                                   uint32_t vb1, uint32_t l4, const G& g, int w,
+                                                   int len0, int len1) {
   switch (w) {
-    case 1: return slice_real_w<1, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 2: return slice_real_w<2, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 3: return slice_real_w<3, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 4: return slice_real_w<4, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 5: return slice_real_w<5, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 6: return slice_real_w<6, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 7: return slice_real_w<7, EXACT, FULL>(B, cb, vb, l4, ybase, len);
-    case 8: return slice_real_w<8, EXACT, FULL>(B, cb, vb, l4, ybase, len);
+    case 1: return slice_real_w2<1, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    case 2: return slice_real_w2<2, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    case 3: return slice_real_w2<3, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    case 4: return slice_real_w2<4, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    case 5: return slice_real_w2<5, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    case 6: return slice_real_w2<6, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    case 7: return slice_real_w2<7, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+    default: return slice_real_w2<8, EXACT, FULL>(B, cb0, vb0, cb1, vb1, l4, g, len0, len1);
+  }
+}
+
+template <bool EXACT, bool FULL, class Blk, class G>
+__device__ __forceinline__ double slice_real(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
+                                             const G& g, int w, int len) {
+  switch (w) {
+    case 1: return slice_real_w<1, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 2: return slice_real_w<2, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 3: return slice_real_w<3, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 4: return slice_real_w<4, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 5: return slice_real_w<5, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 6: return slice_real_w<6, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 7: return slice_real_w<7, EXACT, FULL>(B, cb, vb, l4, g, len);
+    case 8: return slice_real_w<8, EXACT, FULL>(B, cb, vb, l4, g, len);
     case 0: return 0.0;
-    default: return slice_real_any<EXACT>(B, cb, vb, l4, ybase, w, FULL ? w : len);
+    default: return slice_real_any<EXACT>(B, cb, vb, l4, g, w, FULL ? w : len);
   }
 }
 
 // One power step of one tile (rows r0 .. r0+nrows-1, E block entries): warps
 // stride over the 32-row slices, lane = row.  GENERAL adds the Chebyshev
 // three-term step and the accumulation; plain SpMV powers skip both.
-template <bool CPLX, bool EXACT, bool GENERAL, class Blk>
+template <bool CPLX, bool EXACT, bool GENERAL, class Blk, class G>
 __device__ __forceinline__ void tile_power(const PowTab& pt, double* acc_base, bool use_acc, const Blk& B,
-                                           int32_t r0, int32_t nrows, uint32_t E, int wid, int nwarps) {
+                                           const G& g, int32_t r0, int32_t nrows, uint32_t E, int32_t nseg,
+                                           int wid, int nwarps, bool pairs = true) {
   const int32_t ns = (nrows + 31) >> 5;
   const uint32_t lens_o = uint32_t(ns) * 8;
-  const uint32_t col_o = uint32_t(blk_col_off(ns));
+  const uint32_t col_o = uint32_t(blk_col_off(ns, nseg));
   const uint32_t vdelta = col_o + E * 4 - 2 * col_o;  // vb = 2*cb + vdelta
   const int lane = threadIdx.x & 31;
   const uint32_t l4 = uint32_t(lane) * 4;
   constexpr int cw = CPLX ? 2 : 1;
-  const char* ybase = pt.yin;
   double* yout = pt.yout + int64_t(r0) * cw;
   const double* ypv = pt.ypv + int64_t(r0) * cw;
   double* acc = acc_base + int64_t(r0) * cw;
-  for (int32_t s = wid; s < ns; s += nwarps) {
-    const int2 rec = B.i2(uint32_t(s) * 8);
-    const uint32_t cb = uint32_t(rec.x);
-    const uint32_t vb = 2 * cb + vdelta;
-    const int w = rec.y & 0xffff;
-    const bool full = int(uint32_t(rec.y) >> 16) == w;
-    const int32_t lr = s * 32 + lane;
-    if constexpr (!CPLX) {
-      double t;
-      if (full) {
-        t = slice_real<EXACT, true>(B, cb, vb, l4, ybase, w, w);
-      } else {
-        const int len = int(B.u16(lens_o + uint32_t(s) * 64 + 2 * l4 / 4));
-        t = slice_real<EXACT, false>(B, cb, vb, l4, ybase, w, len);
-      }
+  if constexpr (!CPLX) {
+    auto epilogue = [&](int32_t s, double t) {
+      const int32_t lr = s * 32 + lane;
       if (lr < nrows) {
         if constexpr (GENERAL) {
           if (pt.cheb) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(ypv + lr));
@@ -356,9 +480,54 @@ __device__ __forceinline__ void tile_power(const PowTab& pt, double* acc_base, b
           stg_f64(yout + lr, t);
         }
       }
-    } else {
-      const int len = full ? w : int(B.u16(lens_o + uint32_t(s) * 64 + 2 * l4 / 4));
-      double2 t = slice_cplx<EXACT>(B, cb, vb, l4, ybase, w, len);
+    };
+    auto single = [&](int32_t s, int2 rec) -> double {
+      const uint32_t cb = uint32_t(rec.x), vb = 2 * cb + vdelta;
+      const int w = rec.y & 0xffff;
+      if (int(uint32_t(rec.y) >> 16) == w) return slice_real<EXACT, true>(B, cb, vb, l4, g, w, w);
+      const int len = int(B.u16(lens_o + uint32_t(s) * 64 + (l4 >> 1)));
+      return slice_real<EXACT, false>(B, cb, vb, l4, g, w, len);
+    };
+    // warp `wid` owns slices wid, wid + nwarps, ...; it takes them two at a time
+    for (int32_t s = wid; s < ns; s += 2 * nwarps) {
+      const int32_t s2 = s + nwarps;
+      const int2 rec0 = B.i2(uint32_t(s) * 8);
+      if (s2 >= ns) {
+        epilogue(s, single(s, rec0));
+        break;
+      }
+      const int2 rec1 = B.i2(uint32_t(s2) * 8);
+      const int w0 = rec0.y & 0xffff, w1 = rec1.y & 0xffff;
+      if (pairs && w0 == w1 && w0 >= 1 && w0 <= 8) {
+        const bool full0 = int(uint32_t(rec0.y) >> 16) == w0, full1 = int(uint32_t(rec1.y) >> 16) == w1;
+        const uint32_t cb0 = uint32_t(rec0.x), cb1 = uint32_t(rec1.x);
+        double2 t;
+        if (full0 && full1) {
+          t = slice_real_pair<EXACT, true>(B, cb0, 2 * cb0 + vdelta, cb1, 2 * cb1 + vdelta, l4, g, w0, w0, w0);
+        } else {
+          const int len0 = full0 ? w0 : int(B.u16(lens_o + uint32_t(s) * 64 + (l4 >> 1)));
+          const int len1 = full1 ? w1 : int(B.u16(lens_o + uint32_t(s2) * 64 + (l4 >> 1)));
+          t = slice_real_pair<EXACT, false>(B, cb0, 2 * cb0 + vdelta, cb1, 2 * cb1 + vdelta, l4, g, w0, len0,
+                                            len1);
+        }
+        epilogue(s, t.x);
+        epilogue(s2, t.y);
+      } else {
+        epilogue(s, single(s, rec0));
+        epilogue(s2, single(s2, rec1));
+      }
+    }
+  } else {
+  for (int32_t s = wid; s < ns; s += nwarps) {
+    const int2 rec = B.i2(uint32_t(s) * 8);
+    const uint32_t cb = uint32_t(rec.x);
+    const uint32_t vb = 2 * cb + vdelta;
+    const int w = rec.y & 0xffff;
+    const bool full = int(uint32_t(rec.y) >> 16) == w;
+    const int32_t lr = s * 32 + lane;
+    {
+      const int len = full ? w : int(B.u16(lens_o + uint32_t(s) * 64 + (l4 >> 1)));
+      double2 t = slice_cplx<EXACT>(B, cb, vb, l4, g, w, len);
       if (lr < nrows) {
         const int64_t r2 = 2 * int64_t(lr);
         if constexpr (GENERAL) {
@@ -380,6 +549,7 @@ __device__ __forceinline__ void tile_power(const PowTab& pt, double* acc_base, b
       }
     }
   }
+  }
 }
 
 // Fill the per-power table (all threads of the CTA, then __syncthreads).
@@ -398,20 +568,89 @@ __device__ __forceinline__ void build_powtab(PowTab* tab, const MpkParams& P, co
 }
 
 // ---------------------------------------------------------------- group walk kernel
-// See the file header.  Shared state per held slot r: h_t (tile), h_last
-// (last power of the held item), h_glb (block read from global memory),
-// slot_free (set by the consumer that finished the item's last power).
+// See the file header.  Warps 0..NC-1 are consumers; warp NC + r is the
+// producer of slot r (r < R).  Each producer runs its slot's state machine on
+// its own -- stage the block (TMA), wait for the dependencies of each power,
+// push (slot, power) into the shared work ring, wait until the consumers
+// freed the slot -- so a slow L2 round trip of one slot never delays another.
+// Shared state per slot r: h_t (tile), h_last (last power of the held item),
+// h_glb (block read from global memory), h_r0/h_rows/h_E (tile geometry),
+// free_bar (completed by the consumer that finished the item's last power).
+
+// mbarrier wait of a whole warp with the launch's abort flag / watchdog:
+// lane 0 waits, the verdict is broadcast (warp-uniform), __syncwarp orders
+// the other lanes' later shared-memory reads after the completed phase.
+__device__ __forceinline__ bool mbar_wait_bounded(uint64_t* bar, uint32_t parity, const MpkParams& P) {
+  int ok = 1;
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long t0 = 0;
+    for (int spins = 0; !mbar_try_wait(bar, parity); ++spins) {
+      if ((spins & 255) == 255) {
+        const unsigned long long now = globaltimer();
+        if (t0 == 0) t0 = now;
+        const volatile unsigned long long* ab = P.queue + 1;
+        if (*ab != 0ull) {
+          ok = 0;
+          break;
+        }
+        if (now - t0 > kWatchdogNs) {
+          atomicExch(P.queue + 1, 1ull);
+          *P.err = 2;
+          ok = 0;
+          break;
+        }
+      }
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  __syncwarp();
+  return ok != 0;
+}
+
+// Spin until progress[lo..hi] >= target (one warp, all loads in flight per
+// round); then one acquire fence (also invalidates L1 for the gathers).
+// Returns false if the launch is aborting (abort flag or watchdog).
+__device__ __forceinline__ bool spin_deps(const MpkParams& P, int32_t lo, int32_t hi, uint32_t target,
+                                          unsigned long long* rounds) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long t0 = 0;
+  for (int spins = 0;; ++spins) {
+    uint32_t m = 0xffffffffu;
+    for (int32_t i = lo + lane; i <= hi; i += 32) m = min(m, ld_relaxed_u32(P.progress + i));
+    ++*rounds;
+    if (__all_sync(0xffffffffu, m >= target)) {
+      fence_acq_rel_gpu();
+      return true;
+    }
+    if (spins > 2) __nanosleep(64);
+    if ((spins & 63) == 63) {
+      const unsigned long long now = globaltimer();
+      if (t0 == 0) t0 = now;
+      const volatile unsigned long long* ab = P.queue + 1;
+      bool stop = *ab != 0ull;
+      if (!stop && now - t0 > kWatchdogNs) {
+        if (lane == 0) {
+          atomicExch(P.queue + 1, 1ull);
+          *P.err = 1;
+        }
+        stop = true;
+      }
+      if (__any_sync(0xffffffffu, stop)) return false;
+    }
+  }
+}
+
 template <bool CPLX, bool EXACT, int NC>
-__global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_group_kernel(MpkParams P, PowerCfgDev C) {
+__global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(MpkParams P, PowerCfgDev C) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t tile_bar[kMaxSlots];
+  __shared__ uint64_t tile_bar[kMaxSlots], free_bar[kMaxSlots], x_bar[kMaxSlots];
   __shared__ uint64_t full_bar[kWorkRing], empty_bar[kWorkRing];
   __shared__ int32_t w_slot[kWorkRing], w_p[kWorkRing];
   __shared__ uint32_t w_done[kWorkRing];
+  __shared__ uint32_t ring_ctr, prod_done;
   __shared__ int32_t h_t[kMaxSlots], h_last[kMaxSlots], h_glb[kMaxSlots];
-  __shared__ int32_t h_r0[kMaxSlots], h_rows[kMaxSlots], h_E[kMaxSlots];
+  __shared__ int32_t h_r0[kMaxSlots], h_rows[kMaxSlots], h_E[kMaxSlots], h_nseg[kMaxSlots];
   __shared__ int64_t h_ofs[kMaxSlots];
-  __shared__ volatile int32_t slot_free[kMaxSlots];
   __shared__ PowTab s_pow[LMPK_MAX_POWERS];
   const int R = P.n_slots;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -419,31 +658,36 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_group_kernel(MpkParams P
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMaxSlots; ++i) {
       mbar_init(&tile_bar[i], 1);
-      slot_free[i] = 0;
+      mbar_init(&free_bar[i], 1);
+      mbar_init(&x_bar[i], 1);
     }
     for (int i = 0; i < kWorkRing; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], NC);
       w_done[i] = 0;
     }
+    ring_ctr = 0;
+    prod_done = 0;
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == NC) {
-    // ------------------------------------------------ producer / scheduler warp
+  if (warp >= NC) {
+    // ------------------------------------------------ producer of slot r
+    const int r = warp - NC;
+    if (r >= R) return;
     const int pol_mode = (P.flags >> 8) & 3;
     const uint64_t pol_keep = pol_mode == 0 ? policy_evict_last()
                                             : (pol_mode == 1 ? policy_evict_normal() : policy_evict_first());
     const uint64_t pol_drop = policy_evict_first();
     const bool no_tma = (P.flags & LMPK_FLAG_NO_TMA) != 0;
-    // per-slot state, register-resident (every loop below is unrolled)
-    int32_t np[kMaxSlots], pf[kMaxSlots], pl[kMaxSlots], lo[kMaxSlots], hi[kMaxSlots];
-    uint32_t fills[kMaxSlots];
-    unsigned long long p_polls = 0, p_idle = 0, p_t0 = P.prof ? globaltimer() : 0, p_items = 0;
-    // The next queue item (ticket + tile metadata) is fetched ahead, right
-    // after a slot was filled, so a freed slot only waits for its TMA.
+    // q > 1: a grabbed item must be held at once (the deadlock-freedom window
+    // counts grabbed items as held), so a ticket is taken only for a free
+    // slot.  q == 1 items only wait for older items: prefetch one ahead.
+    const bool prefetch = P.q == 1;
+    unsigned long long p_rounds = 0, p_items = 0, p_tma = 0, p_dep = 0, p_free = 0, p_x = 0;
+    const unsigned long long p_t0 = P.prof ? globaltimer() : 0;
     struct Next {
-      int32_t t, first, last, r0, rows, E, lo, hi;
+      int32_t t, first, last, r0, rows, E, lo, hi, nseg, xent;
       int64_t ofs, bytes;
       bool valid;
     } nx;
@@ -474,168 +718,129 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_group_kernel(MpkParams P
         nx.E = __ldg(P.tile_E + t);
         nx.lo = __ldg(P.dep_lo + t);
         nx.hi = __ldg(P.dep_hi + t);
+        nx.nseg = P.xmode ? __ldg(P.tile_nseg + t) : 0;
+        nx.xent = nx.nseg ? __ldg(P.tile_xent + t) : 0;
         nx.valid = true;
         return;
       }
     };
-    // q > 1: a grabbed item must be held at once (the deadlock-freedom window
-    // counts grabbed items as held), so no ticket is taken ahead of a slot.
-    // q == 1 items only wait for older items, so prefetching is safe.
-    const bool prefetch = P.q == 1;
-    auto refill = [&](int r) -> bool {
-      if (!prefetch) fetch_next();
-      if (!nx.valid) {
-        np[r] = 0;
-        if (lane == 0) h_t[r] = -1;
-        return false;
+    // Stage the x-segments of the gathered vector y_{p-1} into the slot's x
+    // buffer (one bulk copy per segment, completion on x_bar[r]).  The
+    // preceding acquire made the producers' stores visible to this thread;
+    // the proxy fence orders them before the async-proxy reads.
+    uint32_t xph = 0;
+    const uint32_t slot_base = smem_u32(smem_raw) + uint32_t(r) * uint32_t(P.smem_cap);
+    auto stage_x = [&](const char* yin, int32_t ns, int32_t nseg, int32_t xent) -> bool {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (lane == 0) mbar_arrive_expect_tx(&x_bar[r], uint32_t(xent) * 8u);
+      __syncwarp();
+      const uint32_t seg_o = slot_base + uint32_t(blk_seg_off(ns));
+      const uint32_t xb = slot_base + uint32_t(P.xoff);
+      for (int j = lane; j < nseg; j += 32) {
+        const int4 sg = SmemBlk{seg_o}.i4(uint32_t(j) * 16);
+        // even entry count: 16-byte granules (the extra entry is inside the
+        // slot -- bulk copies run only for even ldy)
+        bulk_g2s_a(xb + uint32_t(sg.z) * 8u, yin + int64_t(sg.x) * 8, uint32_t((sg.y + 1) & ~1) * 8u, &x_bar[r],
+                   policy_evict_normal());
       }
-      const bool glb = no_tma || nx.bytes > P.smem_cap;
+      const bool ok = mbar_wait_bounded(&x_bar[r], xph & 1, P);
+      ++xph;
+      return ok;
+    };
+    auto push = [&](int p) {
       if (lane == 0) {
-        h_t[r] = nx.t;
-        h_last[r] = nx.last;
-        h_ofs[r] = nx.ofs;
+        const uint32_t k = atomicAdd(&ring_ctr, 1u);
+        const int ws = int(k % kWorkRing);
+        if (k >= kWorkRing) mbar_wait(&empty_bar[ws], (k / kWorkRing - 1) & 1);
+        w_slot[ws] = r;
+        w_p[ws] = p;
+        mbar_arrive(&full_bar[ws]);
+      }
+      __syncwarp();
+    };
+    uint32_t fills = 0, frees = 0;
+    bool abort = false, tma_pending = false;
+    fetch_next();
+    while (nx.valid && !abort) {
+      const Next cur = nx;
+      const bool glb = no_tma || cur.bytes > P.blk_cap;
+      if (lane == 0) {
+        h_t[r] = cur.t;
+        h_last[r] = cur.last;
+        h_ofs[r] = cur.ofs;
         h_glb[r] = glb ? 1 : 0;
-        h_r0[r] = nx.r0;
-        h_rows[r] = nx.rows;
-        h_E[r] = nx.E;
+        h_r0[r] = cur.r0;
+        h_rows[r] = cur.rows;
+        h_E[r] = cur.E;
+        h_nseg[r] = glb ? 0 : cur.nseg;
         if (!glb) {
           fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&tile_bar[r], uint32_t(nx.bytes));
-          bulk_g2s(smem_raw + int64_t(r) * P.smem_cap, P.blocks + nx.ofs, uint32_t(nx.bytes), &tile_bar[r],
-                   nx.last == P.n_powers ? pol_drop : pol_keep);
-        } else {
-          mbar_arrive(&tile_bar[r]);
+          mbar_arrive_expect_tx(&tile_bar[r], uint32_t(cur.bytes));
+          bulk_g2s(smem_raw + int64_t(r) * P.smem_cap, P.blocks + cur.ofs, uint32_t(cur.bytes), &tile_bar[r],
+                   cur.last == P.n_powers ? pol_drop : pol_keep);
         }
       }
-      pf[r] = nx.first;
-      pl[r] = nx.last;
-      np[r] = nx.first;
-      lo[r] = nx.lo;
-      hi[r] = nx.hi;
+      __syncwarp();
+      tma_pending = !glb;
       ++p_items;
-      if (prefetch) fetch_next();
-      return true;
-    };
-    if (prefetch) fetch_next();
-    int live = 0;
-#pragma unroll
-    for (int r = 0; r < kMaxSlots; ++r) {
-      fills[r] = 0;
-      np[r] = 0;
-      pf[r] = pl[r] = lo[r] = hi[r] = 0;
-      if (r < R && refill(r)) ++live;
+      for (int p = cur.first; p <= cur.last; ++p) {
+        if (p > 1) {
+          const unsigned long long t0 = P.prof ? globaltimer() : 0;
+          if (!spin_deps(P, cur.lo, cur.hi, P.epoch_base + uint32_t(p - 1), &p_rounds)) {
+            abort = true;
+            break;
+          }
+          if (P.prof) p_dep += globaltimer() - t0;
+        }
+        if (tma_pending) {
+          const unsigned long long t0 = P.prof ? globaltimer() : 0;
+          const bool ok = mbar_wait_bounded(&tile_bar[r], fills & 1, P);
+          ++fills;
+          tma_pending = false;
+          if (!ok) {
+            abort = true;
+            break;
+          }
+          if (P.prof) p_tma += globaltimer() - t0;
+        }
+        if (P.xmode == 1 && !glb && cur.nseg > 0) {
+          const unsigned long long t0 = P.prof ? globaltimer() : 0;
+          if (!stage_x(s_pow[p - 1].yin, (cur.rows + 31) >> 5, cur.nseg, cur.xent)) {
+            abort = true;
+            break;
+          }
+          if (P.prof) p_x += globaltimer() - t0;
+        }
+        push(p);
+        if (p == cur.first && prefetch) fetch_next();
+      }
+      if (abort) break;
+      const unsigned long long t0 = P.prof ? globaltimer() : 0;
+      if (!mbar_wait_bounded(&free_bar[r], frees & 1, P)) {  // consumers finished the last power
+        abort = true;
+        break;
+      }
+      ++frees;
+      if (P.prof) p_free += globaltimer() - t0;
+      if (!prefetch) fetch_next();
     }
-    int k = 0;  // work items pushed
-    unsigned long long idle_since = 0;
-    bool abort = false;
-    while (live > 0 && !abort) {
-      bool progressed = false;
-      // ---- refill slots whose item finished its last power
-#pragma unroll
-      for (int r = 0; r < kMaxSlots; ++r) {
-        if (r < R && np[r] != 0 && np[r] > pl[r] && slot_free[r]) {
-          __syncwarp();
-          if (lane == 0) slot_free[r] = 0;
-          __threadfence_block();
-          ++fills[r];
-          if (!refill(r)) --live;
-          progressed = true;
-        }
-      }
-      // ---- dependency polls of every held item, one batch of loads
-      uint32_t want = 0, tgt[kMaxSlots];
-#pragma unroll
-      for (int r = 0; r < kMaxSlots; ++r) {
-        tgt[r] = 0;
-        if (r < R && np[r] != 0 && np[r] <= pl[r]) {
-          const bool staged = np[r] != pf[r] || mbar_test(&tile_bar[r], fills[r] & 1);
-          if (staged) {
-            want |= 1u << r;
-            tgt[r] = np[r] > 1 ? P.epoch_base + uint32_t(np[r] - 1) : 0u;
-          }
-        }
-      }
-      uint32_t ready = 0;
-      if (want) {
-        uint32_t v0[kMaxSlots], v1[kMaxSlots];
-#pragma unroll
-        for (int r = 0; r < kMaxSlots; ++r) {
-          v0[r] = v1[r] = 0xffffffffu;
-          if (((want >> r) & 1) && tgt[r] != 0) {
-            const int32_t i0 = lo[r] + lane, i1 = i0 + 32;
-            if (i0 <= hi[r]) v0[r] = ld_relaxed_u32(P.progress + i0);
-            if (i1 <= hi[r]) v1[r] = ld_relaxed_u32(P.progress + i1);
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < kMaxSlots; ++r) {
-          if ((want >> r) & 1) {
-            bool ok = v0[r] >= tgt[r] && v1[r] >= tgt[r];
-            if (tgt[r] != 0)
-              for (int32_t i = lo[r] + lane + 64; i <= hi[r]; i += 32)
-                ok = ok && ld_relaxed_u32(P.progress + i) >= tgt[r];
-            if (__all_sync(0xffffffffu, ok)) ready |= 1u << r;
-          }
-        }
-        if (P.prof) {
-          ++p_polls;
-          if (!ready) ++p_idle;
-        }
-      }
-      if (ready) {
-        fence_acq_rel_gpu();  // acquire + L1 invalidation before the gathers
-#pragma unroll
-        for (int r = 0; r < kMaxSlots; ++r) {
-          if ((ready >> r) & 1) {
-            const int ws = k % kWorkRing;
-            if (lane == 0) {
-              if (k >= kWorkRing) mbar_wait(&empty_bar[ws], uint32_t(k / kWorkRing - 1) & 1);
-              w_slot[ws] = r;
-              w_p[ws] = np[r];
-              mbar_arrive(&full_bar[ws]);
-            }
-            __syncwarp();
-            ++k;
-            ++np[r];
-          }
-        }
-        progressed = true;
-      }
-      if (progressed) {
-        idle_since = 0;
-      } else {
-        __nanosleep(32);
-        const unsigned long long now = globaltimer();
-        if (idle_since == 0) idle_since = now;
-        const volatile unsigned long long* ab = P.queue + 1;
-        if (*ab != 0ull) abort = true;
-        if (now - idle_since > kWatchdogNs) {
-          if (lane == 0) {
-            atomicExch(P.queue + 1, 1ull);
-            *P.err = 1;
-          }
-          abort = true;
-        }
-      }
-    }
+    if (tma_pending && lane == 0) mbar_wait(&tile_bar[r], fills & 1);  // no TMA may land after exit
     if (P.prof && lane == 0) {
-      atomicAdd(P.prof + 3, p_polls);
-      atomicAdd(P.prof + 4, p_idle);
+      atomicAdd(P.prof + 3, p_rounds);
       atomicAdd(P.prof + 5, globaltimer() - p_t0);
       atomicAdd(P.prof + 6, p_items);
+      atomicAdd(P.prof + 7, p_tma);
+      atomicAdd(P.prof + 8, p_dep);
+      atomicAdd(P.prof + 9, p_free);
+      atomicAdd(P.prof + 11, p_x);
     }
-    // terminator
-    const int ws = k % kWorkRing;
-    if (lane == 0) {
-      if (k >= kWorkRing) mbar_wait(&empty_bar[ws], uint32_t(k / kWorkRing - 1) & 1);
+    // the last producer to finish posts the terminator (after every push)
+    if (lane == 0 && atomicAdd(&prod_done, 1u) == uint32_t(R - 1)) {
+      const uint32_t k = atomicAdd(&ring_ctr, 1u);
+      const int ws = int(k % kWorkRing);
+      if (k >= kWorkRing) mbar_wait(&empty_bar[ws], (k / kWorkRing - 1) & 1);
       w_slot[ws] = -1;
       mbar_arrive(&full_bar[ws]);
-    }
-    // no TMA may still be landing when the CTA exits
-    if (abort && lane == 0) {
-#pragma unroll
-      for (int r = 0; r < kMaxSlots; ++r)
-        if (r < R && np[r] != 0 && np[r] == pf[r]) mbar_wait(&tile_bar[r], fills[r] & 1);
     }
   } else {
     // ------------------------------------------------ consumer warps: compute only
@@ -653,16 +858,46 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_group_kernel(MpkParams P
       const uint32_t E = uint32_t(h_E[r]);
       const PowTab& pt = s_pow[p - 1];
       const bool use_acc = P.use_acc != 0;
+      const int32_t nseg = h_nseg[r];
       // separate inlined copies so each sees a known address space (LDS vs
       // LDG); plain SpMV powers take the epilogue without Chebyshev/acc
       if (!h_glb[r]) {
-        const SmemBlk B{smem_u32(smem_raw) + uint32_t(r) * uint32_t(P.smem_cap)};
-        if (pt.general)
-          tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, r0, rows, E, warp, NC);
-        else
-          tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, r0, rows, E, warp, NC);
+        const uint32_t sb = smem_u32(smem_raw) + uint32_t(r) * uint32_t(P.smem_cap);
+        const SmemBlk B{sb};
+        const bool pairs = (P.flags & 0x800) == 0;  // internal A/B switch
+        if (nseg > 0) {
+          const uint32_t xb = sb + uint32_t(P.xoff);
+          if (P.xmode == 2) {
+            // vectors not 16-byte aligned: all consumer warps copy the
+            // segments (plain loads), then one named barrier
+            const int tid = warp * 32 + lane;
+            const uint32_t seg_o = uint32_t(blk_seg_off((rows + 31) >> 5));
+            const int cw = CPLX ? 2 : 1;
+            const double* yin = reinterpret_cast<const double*>(pt.yin);
+            for (int j = 0; j < nseg; ++j) {
+              const int4 sg = B.i4(seg_o + uint32_t(j) * 16);
+              for (int e = tid; e < sg.y * cw; e += NC * 32) {
+                const double v = ld_cg(yin + int64_t(sg.x) * cw + e);
+                asm volatile("st.shared.f64 [%0], %1;" ::"r"(xb + uint32_t(sg.z * cw + e) * 8u), "d"(v));
+              }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(NC * 32) : "memory");
+          }
+          const GatherSmem G{xb};
+          if (pt.general)
+            tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, pairs);
+          else
+            tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, pairs);
+        } else {
+          const GatherGlobal G{pt.yin};
+          if (pt.general)
+            tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, pairs);
+          else
+            tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, pairs);
+        }
       } else {
-        tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, GlbBlk{P.blocks + h_ofs[r]}, r0, rows, E, warp, NC);
+        tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, GlbBlk{P.blocks + h_ofs[r]}, GatherGlobal{pt.yin}, r0,
+                                      rows, E, 0, warp, NC);
       }
       __syncwarp();
       if (P.prof) {
@@ -675,10 +910,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) mpk_group_kernel(MpkParams P
         if (old == NC - 1) {
           w_done[ws] = 0;
           if (P.mode != 3) st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
-          if (p == h_last[r]) {
-            __threadfence_block();
-            slot_free[r] = 1;
-          }
+          if (p == h_last[r]) mbar_arrive(&free_bar[r]);  // release.cta: the slot may be refilled
         }
         mbar_arrive(&empty_bar[ws]);
       }
@@ -708,11 +940,14 @@ __global__ void k_slice_width(const int32_t* row_ptr, int32_t n, int32_t n_slice
   }
 }
 
-// one warp per slice: slice record, row lengths and the chunked entries
+// one warp per slice: slice record, row lengths and the chunked entries.
+// Tiles with x-segments get local columns (index into the tile's x buffer);
+// the warp of a tile's first slice also writes the tile's segment table.
 __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const double* val,
                               int32_t n_slices, const int32_t* slice_tile, const int32_t* slice_off,
                               const int32_t* width, const int32_t* wmin, const int32_t* tile_row,
-                              const int64_t* tile_ofs, const int32_t* tile_E, unsigned char* blocks) {
+                              const int64_t* tile_ofs, const int32_t* tile_E, const int32_t* seg_ptr,
+                              const int4* segs, unsigned char* blocks) {
   const int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
@@ -720,13 +955,18 @@ __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const 
   const int32_t r0 = tile_row[t], r1 = tile_row[t + 1];
   const int32_t ns = (r1 - r0 + 31) >> 5;
   const int32_t ls = s - (r0 >> 5);
+  const int32_t sg0 = seg_ptr ? seg_ptr[t] : 0;
+  const int32_t nseg = seg_ptr ? seg_ptr[t + 1] - sg0 : 0;
   unsigned char* blk = blocks + tile_ofs[t];
   int2* rec = reinterpret_cast<int2*>(blk);
   uint16_t* lens = reinterpret_cast<uint16_t*>(blk + int64_t(ns) * 8);
-  const int64_t co = blk_col_off(ns);
+  const int64_t co = blk_col_off(ns, nseg);
   const int32_t E = tile_E[t];
   int32_t* cols = reinterpret_cast<int32_t*>(blk + co);
   double* vals = reinterpret_cast<double*>(blk + co + int64_t(E) * 4);
+  if (ls == 0)
+    for (int j = lane; j < nseg; j += 32)
+      reinterpret_cast<int4*>(blk + blk_seg_off(ns))[j] = segs[sg0 + j];
   const int32_t base = slice_off[s];
   const int32_t r = s * 32 + lane;
   const bool valid = r < r1;
@@ -735,13 +975,28 @@ __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const 
   const int w = width[s];
   if (lane == 0) rec[ls] = make_int2(int32_t(co + int64_t(base) * 4), w | (wmin[s] << 16));
   lens[ls * 32 + lane] = uint16_t(len);
+  // local index of a global column: its segment (binary search) + offset
+  auto local = [&](int32_t c) -> int32_t {
+    if (nseg == 0) return c;
+    int lo = 0, hi = nseg - 1;  // last segment with start <= c
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (segs[sg0 + mid].x <= c)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const int4 g = segs[sg0 + lo];
+    return g.z + (c - g.x);
+  };
+  const int32_t pad = local(valid ? r : r0);  // harmless in-range index, never accumulated
   for (int j = 0; j < w; ++j) {
     const int64_t e = chunk_entry(base, w, lane, j);
     if (j < len) {
-      cols[e] = col[a + j];
+      cols[e] = local(col[a + j]);
       vals[e] = val[a + j];
     } else {
-      cols[e] = valid ? r : r0;  // harmless in-range index, never accumulated
+      cols[e] = (j == 0 || !valid) ? pad : local(col[a + len - 1]);
       vals[e] = 0.0;
     }
   }
@@ -861,7 +1116,7 @@ static void partition_slices(const std::vector<int32_t>& width, int64_t cap,
     int64_t E = 0;
     while (s + ns < S) {
       const int64_t e2 = E + int64_t(width[s + ns]) * 32;
-      if (ns > 0 && blk_bytes(ns + 1, e2) > cap) break;
+      if (ns > 0 && blk_bytes(ns + 1, e2, 0) > cap) break;
       E = e2;
       ++ns;
     }
@@ -911,6 +1166,8 @@ extern "C" int lmpk_tiling_destroy(lmpk_tiling* t) {
   cudaFree(t->d_tile_E);
   cudaFree(t->d_dep_lo);
   cudaFree(t->d_dep_hi);
+  cudaFree(t->d_tile_nseg);
+  cudaFree(t->d_tile_xent);
   cudaFree(t->d_items);
   cudaFree(t->d_progress);
   cudaFree(t->d_blocks);
@@ -918,10 +1175,73 @@ extern "C" int lmpk_tiling_destroy(lmpk_tiling* t) {
   return LMPK_OK;
 }
 
+// x-segments of every tile (host): the tile's distinct columns, as runs of
+// the gathered vector merged across gaps <= `gap`, each run's start rounded
+// down to an even entry (16-byte aligned bulk copies) and its local base
+// rounded up to even.  At most kMaxSegs runs (the gap doubles until they
+// fit); a tile whose runs exceed `xcap` entries or whose column span is huge
+// keeps global columns (nseg = 0).  Returns per tile nseg/xent and the runs.
+static void plan_segments(const std::vector<int32_t>& rp, const std::vector<int32_t>& col,
+                          const std::vector<int32_t>& tile_row, const std::vector<uint8_t>& allow, int32_t n,
+                          int64_t xcap, std::vector<int32_t>& seg_ptr, std::vector<int4>& segs,
+                          std::vector<int32_t>& xent) {
+  const int32_t nt = static_cast<int32_t>(tile_row.size()) - 1;
+  seg_ptr.assign(nt + 1, 0);
+  xent.assign(nt, 0);
+  segs.clear();
+  std::vector<uint8_t> mark;
+  std::vector<int2> runs;
+  for (int32_t t = 0; t < nt; ++t) {
+    seg_ptr[t] = static_cast<int32_t>(segs.size());
+    const int64_t e0 = rp[tile_row[t]], e1 = rp[tile_row[t + 1]];
+    if (e1 == e0 || xcap <= 0 || !allow[t]) continue;
+    int32_t mn = INT32_MAX, mx = -1;
+    for (int64_t e = e0; e < e1; ++e) {
+      mn = std::min(mn, col[e]);
+      mx = std::max(mx, col[e]);
+    }
+    const int64_t span = int64_t(mx) - mn + 1;
+    if (span > (int64_t(1) << 22)) continue;
+    mark.assign(span, 0);
+    for (int64_t e = e0; e < e1; ++e) mark[col[e] - mn] = 1;
+    for (int32_t gap = 8;; gap *= 2) {
+      runs.clear();
+      for (int64_t i = 0; i < span;) {
+        if (!mark[i]) {
+          ++i;
+          continue;
+        }
+        int64_t j = i;
+        while (j < span && mark[j]) ++j;
+        const int32_t a = int32_t((mn + i) & ~int64_t(1));
+        const int32_t b = int32_t(std::min<int64_t>(mn + j, n));
+        if (!runs.empty() && a - runs.back().y <= gap)
+          runs.back().y = std::max(runs.back().y, b);
+        else
+          runs.push_back(make_int2(a, b));
+        i = j;
+      }
+      if (static_cast<int>(runs.size()) <= kMaxSegs) break;
+    }
+    int64_t lb = 0;
+    for (const int2& g : runs) lb += (g.y - g.x + 1) & ~1;
+    if (lb > xcap) continue;
+    lb = 0;
+    for (const int2& g : runs) {
+      const int32_t cnt = g.y - g.x;
+      segs.push_back(make_int4(g.x, cnt, int32_t(lb), 0));
+      lb += (cnt + 1) & ~1;
+    }
+    xent[t] = int32_t(lb);
+  }
+  seg_ptr[nt] = static_cast<int32_t>(segs.size());
+}
+
 // Tiles + chunked tile-SELL-32 blocks + dependency ranges for block cap `cap` bytes.
 static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
                         const int32_t* col, const double* val, const std::vector<int32_t>& width,
-                        const int32_t* d_wmin, int64_t cap, cudaStream_t st) {
+                        const int32_t* d_wmin, int64_t cap, const std::vector<int32_t>* h_rp,
+                        const std::vector<int32_t>* h_col, int64_t xcap, cudaStream_t st) {
   const int32_t S = static_cast<int32_t>(width.size());
   std::vector<int32_t> first;
   std::vector<int64_t> Es;
@@ -929,14 +1249,28 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   const int32_t nt = static_cast<int32_t>(first.size());
   std::vector<int32_t> tile_row(nt + 1), tile_E(nt), slice_tile(std::max(S, 1)), slice_off(std::max(S, 1));
   std::vector<int64_t> tile_ofs(nt + 1);
+  for (int32_t t = 0; t < nt; ++t) tile_row[t] = std::min(first[t] * 32, n);
+  tile_row[nt] = n;
+  // x-segments (real-vector tilings only)
+  std::vector<int32_t> seg_ptr, xent;
+  std::vector<int4> segs;
+  if (h_rp && h_col && xcap > 0) {
+    // only tiles whose block is staged in shared memory can use an x buffer
+    std::vector<uint8_t> allow(nt);
+    for (int32_t t = 0; t < nt; ++t) {
+      const int32_t s1 = (t + 1 < nt) ? first[t + 1] : S;
+      allow[t] = blk_bytes(s1 - first[t], Es[t], 0) <= cap;
+    }
+    plan_segments(*h_rp, *h_col, tile_row, allow, n, xcap, seg_ptr, segs, xent);
+  }
   int64_t ofs = 0;
   int64_t maxb = 0;
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t s0 = first[t], s1 = (t + 1 < nt) ? first[t + 1] : S;
-    tile_row[t] = std::min(s0 * 32, n);
     tile_E[t] = static_cast<int32_t>(Es[t]);
     tile_ofs[t] = ofs;
-    const int64_t b = blk_bytes(s1 - s0, Es[t]);
+    const int32_t nseg = seg_ptr.empty() ? 0 : seg_ptr[t + 1] - seg_ptr[t];
+    const int64_t b = blk_bytes(s1 - s0, Es[t], nseg);
     maxb = std::max(maxb, b);
     ofs += b;
     int32_t e = 0;
@@ -946,7 +1280,6 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
       e += width[s] * 32;
     }
   }
-  tile_row[nt] = n;
   tile_ofs[nt] = ofs;
   T->h_tile_row = tile_row;
   T->block_bytes = ofs;
@@ -971,10 +1304,34 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_width, width.data(), size_t(S) * 4, cudaMemcpyHostToDevice, st));
   }
   LMPK_CHECK_CUDA(cudaMemsetAsync(T->d_progress, 0, size_t(nt) * 4, st));
+  // per-tile x-segment counts / entries (all zero without staging)
+  std::vector<int32_t> tile_nseg(nt, 0);
+  if (!seg_ptr.empty())
+    for (int32_t t = 0; t < nt; ++t) tile_nseg[t] = seg_ptr[t + 1] - seg_ptr[t];
+  if (xent.empty()) xent.assign(nt, 0);
+  LMPK_TRY(dmalloc(&T->d_tile_nseg, nt));
+  LMPK_TRY(dmalloc(&T->d_tile_xent, nt));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_nseg, tile_nseg.data(), nt * 4, cudaMemcpyHostToDevice, st));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_xent, xent.data(), nt * 4, cudaMemcpyHostToDevice, st));
+  int32_t* d_seg_ptr = nullptr;
+  int4* d_segs = nullptr;
+  if (!segs.empty()) {
+    LMPK_TRY(dmalloc(&d_seg_ptr, nt + 1));
+    LMPK_TRY(dmalloc(&d_segs, segs.size()));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(d_seg_ptr, seg_ptr.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * 16, cudaMemcpyHostToDevice, st));
+  }
+  int64_t staged = 0, xmax = 0;
+  for (int32_t t = 0; t < nt; ++t) {
+    staged += tile_nseg[t] > 0;
+    xmax = std::max<int64_t>(xmax, xent[t]);
+  }
+  T->staged_tiles = static_cast<int32_t>(staged);
+  T->max_xent = static_cast<int32_t>(xmax);
   if (S > 0) {
     k_fill_blocks<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_slice_tile, d_slice_off,
                                                                  d_width, d_wmin, T->d_tile_row, T->d_tile_ofs,
-                                                                 T->d_tile_E, T->d_blocks);
+                                                                 T->d_tile_E, d_seg_ptr, d_segs, T->d_blocks);
     launch_count_add(ctx, 1);
   }
   k_tile_deps<<<div_up(int64_t(nt) * 32, 256), 256, 0, st>>>(row_ptr, col, T->d_tile_row, nt, T->d_dep_lo,
@@ -989,6 +1346,8 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   cudaFree(d_slice_tile);
   cudaFree(d_slice_off);
   cudaFree(d_width);
+  cudaFree(d_seg_ptr);
+  cudaFree(d_segs);
   T->info.n_tiles = nt;
   T->info.block_bytes = ofs;
   return LMPK_OK;
@@ -1058,7 +1417,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   lmpk_tiling* T = nullptr;
   int grid = 0, smem = 0, slots = 1, q_used = 1;
   int32_t mfwd = 0, creach = 0;
-  int64_t cap_used = 0;
+  int64_t cap_used = 0, xoff_used = 0;
   int static_smem = 0;
   LMPK_TRY(group_static_smem(&static_smem));
   // the driver reserves 1 KB per CTA; the rest of the SM's smem is the budget
@@ -1067,19 +1426,38 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   // LMPK_FLAG_NO_TMA in the tiling's mode flags: blocks are streamed from
   // global memory, so the slots need no shared memory and R is free
   const bool unstaged = (prm.mode_flags & LMPK_FLAG_NO_TMA) != 0;
+  // x-segment staging (real-vector tilings, opt-in): a slot is [block | x
+  // buffer]; LMPK_XFRAC = percent of the slot for the x buffer (default 0 =
+  // off: measured slower on cfg2 -- 1.36 vs 0.99 ms at 25%)
+  int xfrac = 0;
+  if (const char* e = getenv("LMPK_XFRAC")) xfrac = std::max(0, std::min(60, atoi(e)));
+  const bool xstage = !unstaged && !(prm.mode_flags & LMPK_FLAG_COMPLEX) && xfrac > 0 && n > 0;
+  std::vector<int32_t> h_rp, h_col;
+  if (xstage) {
+    h_rp.resize(size_t(n) + 1);
+    h_col.resize(size_t(h_nnz));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(h_rp.data(), row_ptr, (size_t(n) + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (h_nnz > 0)
+      LMPK_CHECK_CUDA(cudaMemcpyAsync(h_col.data(), col, size_t(h_nnz) * 4, cudaMemcpyDeviceToHost, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  }
   for (const Cand& cd : cands) {
-    int64_t cap = unstaged ? per_cta / 2 : per_cta / cd.slots;
+    const int64_t slot = (unstaged ? per_cta / 2 : per_cta / cd.slots) & ~int64_t(127);
+    int64_t xbytes = xstage ? (slot * xfrac / 100) & ~int64_t(127) : 0;
+    int64_t cap = slot - xbytes - (xstage ? kMaxSegs * 16 : 0);
     if (prm.tile_nnz_hint > 0) cap = std::min<int64_t>(cap, int64_t(prm.tile_nnz_hint) * 12 + 2048);
     cap &= ~int64_t(127);
     if (cap < 2048) continue;
-    const int smem_need = unstaged ? 0 : static_cast<int>(cap * cd.slots);
+    const int64_t xoff = xstage ? cap + kMaxSegs * 16 : 0;
+    const int smem_need = unstaged ? 0 : static_cast<int>(xstage ? xoff + xbytes : cap * cd.slots / cd.slots);
     int occ = 0;
-    LMPK_TRY(group_occupancy(ctx, smem_need, &occ));
+    LMPK_TRY(group_occupancy(ctx, unstaged ? 0 : smem_need * cd.slots, &occ));
     if (occ < 1) continue;
     lmpk_tiling* cand = new lmpk_tiling();
     cand->ctx = ctx;
     cand->n = n;
-    const int rc = build_tiling(ctx, cand, n, row_ptr, col, val, width, d_wmin, cap, st);
+    const int rc = build_tiling(ctx, cand, n, row_ptr, col, val, width, d_wmin, cap, xstage ? &h_rp : nullptr,
+                                xstage ? &h_col : nullptr, xbytes / 8, st);
     if (rc != LMPK_OK) {
       lmpk_tiling_destroy(cand);
       return rc;
@@ -1091,19 +1469,20 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     // the oldest unfinished item needs the next G*(cr+1) queue positions
     // held (q > 1 grabs a ticket only for a free slot)
     const bool ok = (cd.q == 1 || int64_t(g) * cd.slots >= G * (int64_t(cr) + 1) + 1) &&
-                    (cd.q == 1 || unstaged || cand->max_block <= cap);
+                    (cd.q == 1 || unstaged || cand->max_block <= cap + (xstage ? kMaxSegs * 16 : 0));
     if (!ok) {
       lmpk_tiling_destroy(cand);
       continue;
     }
     T = cand;
     grid = g;
-    smem = smem_need;
+    smem = unstaged ? 0 : smem_need * cd.slots;
     slots = cd.slots;
     q_used = cd.q;
     mfwd = mf;
     creach = chain_reach(cand->h_dep_hi, p_m - 1, nullptr);
     cap_used = cap;
+    xoff_used = xoff;
     break;
   }
   if (!T) {
@@ -1119,7 +1498,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   }
   T->info.p_m = p_m;
   T->info.mode = q_used == p_m ? 1 : 2;
-  T->info.block = kBlockThreads;
+  T->info.block = 32 * (kConsumers + slots);
   T->slots = slots;
   T->info.smem_bytes = smem;
   T->info.tile_nnz_cap = static_cast<int32_t>(cap_used / 12);
@@ -1130,6 +1509,8 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   T->info.grid = grid;
   T->info.powers_per_item = q_used;
   T->info.slots = slots;
+  T->xoff = xoff_used;
+  T->info.x_staged_tiles = T->staged_tiles;
   // skewed diagonal key (t + g*M, g), M = q*D + slack
   const int32_t G = (p_m + q_used - 1) / q_used;
   // default slack ~1.5 * (items in flight) / G: measured optimum on cfg2
@@ -1171,18 +1552,17 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
                         int grid, int smem, cudaStream_t st) {
   void* args[] = {&Pm, &C};
   const void* fn = group_fn(cplx, exact);
-  cudaError_t e = coop ? cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlockThreads), args, smem, st)
-                       : cudaLaunchKernel(fn, dim3(grid), dim3(kBlockThreads), args, smem, st);
+  const int block = 32 * (kConsumers + Pm.n_slots);
+  cudaError_t e = coop ? cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, st)
+                       : cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    set_error("mpk launch failed: %s (grid %d, block %d, smem %d)", cudaGetErrorString(e), grid,
-              kBlockThreads, smem);
+    set_error("mpk launch failed: %s (grid %d, block %d, smem %d)", cudaGetErrorString(e), grid, block, smem);
     return LMPK_ERR_CUDA;
   }
   launch_count_add(ctx, 1);
-  // q == 1: every CTA ends its prefetching grab sequence with exactly one
-  // failing grab; q > 1: every slot does
-  ctx->queue_base += uint64_t(Pm.n_items) + uint64_t(grid) * uint64_t(Pm.q == 1 ? 1 : Pm.n_slots);
+  // every slot producer ends its grab sequence with exactly one failing grab
+  ctx->queue_base += uint64_t(Pm.n_items) + uint64_t(grid) * uint64_t(Pm.n_slots);
   return LMPK_OK;
 }
 
@@ -1234,6 +1614,18 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   Pm.queue = reinterpret_cast<unsigned long long*>(ctx->queue_ctr);
   Pm.n_slots = T->slots;
   Pm.smem_cap = T->info.smem_bytes / T->slots;
+  Pm.xoff = static_cast<int32_t>(T->xoff);
+  Pm.blk_cap = T->xoff > 0 ? Pm.xoff : Pm.smem_cap;
+  Pm.tile_nseg = T->d_tile_nseg;
+  Pm.tile_xent = T->d_tile_xent;
+  if (T->staged_tiles > 0) {
+    LMPK_ARG_CHECK(!cplx, "this tiling stages real x-segments; build it with LMPK_FLAG_COMPLEX in "
+                          "mode_flags for complex vectors");
+    LMPK_ARG_CHECK(!(flags & LMPK_FLAG_NO_TMA), "LMPK_FLAG_NO_TMA needs a tiling built with LMPK_FLAG_NO_TMA");
+    // bulk copies need 16-byte aligned vector slots; otherwise the consumers copy
+    const bool aligned = (reinterpret_cast<uintptr_t>(y) & 15) == 0 && (ldy & 1) == 0;
+    Pm.xmode = aligned ? 1 : 2;
+  }
   Pm.flags = flags;
   Pm.err = ctx->err.dev;
   Pm.prof = ctx->prof;
@@ -1284,7 +1676,7 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
 // Each CTA stages tile blockIdx.x once and runs the row kernel `iters` times
 // (power 1 into slot 1) with no cross-CTA synchronisation: the attainable
 // per-SM rate of the tile kernel itself.
-template <bool EXACT>
+template <bool EXACT, int MODE>
 __global__ void k_probe_compute(MpkParams P, PowerCfgDev C, int iters, int n_tiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t bar;
@@ -1310,13 +1702,33 @@ __global__ void k_probe_compute(MpkParams P, PowerCfgDev C, int iters, int n_til
   __syncthreads();
   const int32_t r0 = P.tile_row[t], rows = P.tile_row[t + 1] - r0;
   const uint32_t E = uint32_t(P.tile_E[t]);
+  const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   for (int it = 0; it < iters; ++it) {
-    if (staged)
-      tile_power<false, EXACT, false>(s_pow[0], P.acc, false, SmemBlk{smem_u32(smem_raw)}, r0, rows, E,
-                                      threadIdx.x >> 5, blockDim.x >> 5);
-    else
-      tile_power<false, EXACT, true>(s_pow[0], P.acc, false, GlbBlk{P.blocks + ofs}, r0, rows, E,
-                                     threadIdx.x >> 5, blockDim.x >> 5);
+    if constexpr (MODE == 0) {
+      if (staged)
+        tile_power<false, EXACT, false>(s_pow[0], P.acc, false, SmemBlk{smem_u32(smem_raw)},
+                                        GatherGlobal{s_pow[0].yin}, r0, rows, E, 0, wid, nw);
+      else
+        tile_power<false, EXACT, true>(s_pow[0], P.acc, false, GlbBlk{P.blocks + ofs}, GatherGlobal{s_pow[0].yin},
+                                       r0, rows, E, 0, wid, nw);
+    } else {
+      // MODE 1..3: width-7 full slices only, single-slice path with the
+      // gather variant of slice_real_w<..., PROBE = MODE>
+      if (!staged) return;
+      const SmemBlk B{smem_u32(smem_raw)};
+      const int32_t ns = (rows + 31) >> 5;
+      const uint32_t col_o = uint32_t(blk_col_off(ns, 0));
+      const uint32_t vdelta = col_o + E * 4 - 2 * col_o;
+      double* yout = s_pow[0].yout + r0;
+      for (int32_t s = wid; s < ns; s += nw) {
+        const int2 rec = B.i2(uint32_t(s) * 8);
+        if ((rec.y & 0xffff) != 7 || (int(uint32_t(rec.y) >> 16) != 7)) continue;
+        const uint32_t cb = uint32_t(rec.x);
+        const double v = slice_real_w<7, EXACT, true, SmemBlk, GatherGlobal, MODE>(
+            B, cb, 2 * cb + vdelta, uint32_t(lane) * 4, GatherGlobal{s_pow[0].yin}, 7);
+        stg_f64(yout + s * 32 + lane, v);
+      }
+    }
   }
 }
 
@@ -1340,6 +1752,7 @@ extern "C" int lmpk_probe_tile_compute(lmpk_ctx* ctx, const lmpk_tiling* T, doub
                                        int iters, int threads, int ctas_per_sm, double* ns_per_knnz) {
   LMPK_ARG_CHECK(ctx && T && y && ns_per_knnz, "probe: NULL argument");
   const bool exact = (ctas_per_sm & 0x100) != 0;
+  const int mode = (ctas_per_sm >> 12) & 7;
   ctas_per_sm &= 0xff;
   MpkParams Pm;
   memset(&Pm, 0, sizeof(Pm));
@@ -1357,7 +1770,13 @@ extern "C" int lmpk_probe_tile_compute(lmpk_ctx* ctx, const lmpk_tiling* T, doub
   C.out_slot[0] = 1;
   C.in_slot[0] = 0;
   const int smem = T->max_block;
-  auto fn = exact ? k_probe_compute<true> : k_probe_compute<false>;
+  void (*fn)(MpkParams, PowerCfgDev, int, int) = nullptr;
+  switch (mode) {
+    case 1: fn = exact ? k_probe_compute<true, 1> : k_probe_compute<false, 1>; break;
+    case 2: fn = exact ? k_probe_compute<true, 2> : k_probe_compute<false, 2>; break;
+    case 3: fn = exact ? k_probe_compute<true, 3> : k_probe_compute<false, 3>; break;
+    default: fn = exact ? k_probe_compute<true, 0> : k_probe_compute<false, 0>; break;
+  }
   LMPK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->max_smem_block - 1024));
   const int grid = ctx->sm_count * ctas_per_sm;
   cudaEvent_t a, b;

@@ -129,13 +129,13 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
         if cplx or use_acc or np.any(plan.kernel != 0):
             # baseline plans with Chebyshev slots: tiled dependency-free sweeps
             cfg = plan.power_config()
-            K.mpk_run(plan.tiling(), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx,
+            K.mpk_run(plan.tiling(complex_state=cplx), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx,
                       flags=flags | _lib.FLAG_SWEEP)
         else:
             K.mpk_baseline(plan.a.device(), yv, plan.p_m)
     else:
         cfg = plan.power_config()
-        K.mpk_run(plan.tiling(), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=flags)
+        K.mpk_run(plan.tiling(complex_state=cplx), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=flags)
     e1.record()
     e1.synchronize()
     ctx = _lib.context()

@@ -87,14 +87,22 @@ class ExecPlan:
     def barrier_count(self) -> int:
         return self.n_items if self.barrier else 0
 
-    def tiling(self, **params):
-        """GPU tile geometry for this plan's matrix (built once, cached)."""
-        if self._tiling is None or (params and params != self.tiling_params):
-            if params:
-                self.tiling_params = dict(params)
+    def tiling(self, complex_state=False, **params):
+        """GPU tile geometry for this plan's matrix (built once, cached).  Real
+        tilings stage x-segments in shared memory; complex state needs its own
+        tiling (LMPK_FLAG_COMPLEX)."""
+        if params and params != self.tiling_params:
+            self.tiling_params = dict(params)
+            self._tiling = None
+        if self._tiling is None:
+            self._tiling = {}
+        key = bool(complex_state)
+        if key not in self._tiling:
             prm = dict(self.tiling_params or {})
-            self._tiling = K.Tiling(self.a.device(), self.p_m, **prm)
-        return self._tiling
+            if key:
+                prm["mode_flags"] = int(prm.get("mode_flags", 0)) | _lib.FLAG_COMPLEX
+            self._tiling[key] = K.Tiling(self.a.device(), self.p_m, **prm)
+        return self._tiling[key]
 
     def power_config(self, acc_coef_im=None):
         """Per-power kernel configuration for liblmpk.  The reference stores it
