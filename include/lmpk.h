@@ -66,6 +66,8 @@ extern "C" {
                                     /* sweeps (k back-to-back SpMVs) on the     */
                                     /* same tiles -- the blocking-free baseline */
 #define LMPK_FLAG_EXACT 0x400       /* bit-exact row sums (see Summation below) */
+#define LMPK_FLAG_READY_QUEUE 0x1000 /* q = 1: dependency-driven ready-queue walk */
+                                     /* instead of the skewed-key item order      */
 /* bits 8-9 (0x100, 0x200): L2 eviction policy of staged blocks that a later
  * power group re-reads: 0 evict_last, 1 evict_normal, 2/3 evict_first.      */
 

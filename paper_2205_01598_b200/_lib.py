@@ -32,6 +32,7 @@ FLAG_MODE_RESIDENT = 0x20
 FLAG_NO_TMA = 0x40
 FLAG_SWEEP = 0x80
 FLAG_EXACT = 0x400
+FLAG_READY_QUEUE = 0x1000
 
 MAX_POWERS = 64
 

@@ -89,6 +89,11 @@ struct lmpk_tiling {
   int32_t* d_tile_xent = nullptr;  // [n_tiles] x-buffer entries
   int32_t staged_tiles = 0, max_xent = 0;
   int64_t xoff = 0;                // byte offset of the x buffer in a slot (0: no staging)
+  int32_t* d_rdep_ptr = nullptr;   // [n_tiles+1] reverse dependencies (ready-queue walk)
+  int32_t* d_rdep = nullptr;
+  uint32_t* d_rcnt = nullptr;      // [p_m][n_tiles] readiness counters
+  int32_t* d_rqueue = nullptr;     // [p_m * n_tiles] ready queue
+  uint32_t* d_rctrl = nullptr;     // head / tail / next power-1 tile
   int32_t* d_items = nullptr;      // item queue order, packed (t << 8) | power group
   int32_t n_items = 0;
   uint32_t* d_progress = nullptr;  // [n_tiles] epoch-tagged power counters
@@ -323,6 +328,19 @@ __device__ __forceinline__ double2 ldg_f64x2(const char* p) {
   double2 v;
   asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
+}
+__device__ __forceinline__ int32_t ld_acquire_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_s32(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acqrel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
 }
 __device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");

@@ -78,6 +78,13 @@ struct MpkParams {
   const int32_t* tile_row;
   const int32_t* dep_lo;
   const int32_t* dep_hi;
+  const int32_t* rdep_ptr;   // ready-queue walk: tiles depending on tile t are
+  const int32_t* rdep;       //   rdep[rdep_ptr[t] .. rdep_ptr[t+1])
+  uint32_t* rcnt;            // [p_m][n_tiles] finished dependencies of (t, p+1)
+  int32_t* rqueue;           // ready items (t << 8 | p), -1 = not yet written
+  uint32_t* rctrl;           // [0] queue head, [32] queue tail, [64] next power-1 tile, [96] items done
+  int32_t lead;              // ready walk: max power-1 lead (tiles) over the completed work
+  int32_t n_tiles;
   const int32_t* tile_nseg;  // x-segments per tile (0: global columns)
   const int32_t* tile_xent;  // x-buffer entries per tile
   const int32_t* items;  // packed (t << 8) | g in queue order (NULL: item i = tile i, g = 0)
@@ -92,7 +99,7 @@ struct MpkParams {
   int32_t n_items;
   int32_t n_powers;
   int32_t q;         // powers per item
-  int32_t mode;      // 1 group walk, 3 sweep (one power, no deps)
+  int32_t mode;      // 1 key-order group walk, 3 sweep (one power, no deps), 4 ready-queue walk (q = 1)
   int32_t smem_cap;  // bytes of one slot
   int32_t xoff;      // byte offset of the x buffer inside a slot
   int32_t blk_cap;   // bytes of a slot available to the staged block
@@ -691,9 +698,110 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
       int64_t ofs, bytes;
       bool valid;
     } nx;
+    // Ready-queue walk: take a ready (t, p) if the queue has one, else start
+    // the next power-1 tile; every enqueued item's dependencies are complete.
+    auto fetch_ready = [&]() -> int32_t {  // item code, -1 exhausted, -2 abort
+      int32_t code = -1;
+      if (lane == 0) {
+        const uint32_t total_q = uint32_t(P.n_tiles) * uint32_t(P.n_powers - 1);
+        unsigned long long t0 = 0;
+        // head / tail / next power-1 tile live on separate 128-byte lines
+        uint32_t* q_head = P.rctrl;
+        uint32_t* q_tail = P.rctrl + 32;
+        uint32_t* q_p1 = P.rctrl + 64;
+        for (int spins = 0;; ++spins) {
+          const uint32_t h = ld_relaxed_u32(q_head), tl = ld_relaxed_u32(q_tail);
+          if (h < tl) {
+            // fetch-and-add dequeue: no CAS herd.  An index past the current
+            // tail is a reservation of a future item; every index below
+            // total_q is eventually enqueued, so waiting for it cannot
+            // deadlock (this slot holds no work while it waits).
+            const uint32_t idx = atomicAdd(q_head, 1u);
+            if (idx >= total_q) break;  // all queue items are taken
+            int32_t c;
+            const unsigned long long tw = P.prof ? globaltimer() : 0;
+            for (int w = 0; (c = ld_acquire_s32(P.rqueue + idx)) < 0; ++w) {
+              if (w > 8) __nanosleep(64);
+              if ((w & 1023) == 1023) {
+                const unsigned long long now = globaltimer();
+                if (t0 == 0) t0 = now;
+                const volatile unsigned long long* ab = P.queue + 1;
+                if (*ab != 0ull || now - t0 > kWatchdogNs) {
+                  if (*ab == 0ull) {
+                    atomicExch(P.queue + 1, 1ull);
+                    *P.err = 3;
+                  }
+                  c = -2;
+                  break;
+                }
+              }
+            }
+            if (P.prof) atomicAdd(P.prof + 10, globaltimer() - tw);
+            code = c;
+            if (P.prof && c >= 0) atomicAdd(P.prof + 14, 1ull);
+            break;
+          }
+          // a new power-1 tile only within `lead` tiles of the completed
+          // work (completed items / powers): keeps the walk's L2 window tight
+          const uint32_t p1 = ld_relaxed_u32(q_p1);
+          if (p1 < uint32_t(P.n_tiles) &&
+              p1 < ld_relaxed_u32(P.rctrl + 96) / uint32_t(P.n_powers) + uint32_t(P.lead)) {
+            const uint32_t i = atomicAdd(q_p1, 1u);
+            if (i < uint32_t(P.n_tiles)) {
+              code = int32_t(i << 8) | 1;
+              if (P.prof) atomicAdd(P.prof + 15, 1ull);
+              break;
+            }
+            continue;
+          }
+          if (h >= total_q) break;  // every item handed out
+          if (P.prof) atomicAdd(P.prof + 13, 1ull);
+          if (spins > 4) __nanosleep(64);
+          if ((spins & 63) == 63) {
+            const unsigned long long now = globaltimer();
+            if (t0 == 0) t0 = now;
+            const volatile unsigned long long* ab = P.queue + 1;
+            if (*ab != 0ull) {
+              code = -2;
+              break;
+            }
+            if (now - t0 > kWatchdogNs) {
+              atomicExch(P.queue + 1, 1ull);
+              *P.err = 3;
+              code = -2;
+              break;
+            }
+          }
+        }
+        if (code >= 0 && (code & 255) > 1) fence_acq_rel_gpu();  // acquire the deps; invalidate L1
+      }
+      return __shfl_sync(0xffffffffu, code, 0);
+    };
     auto fetch_next = [&]() {
       while (true) {
         int32_t i = 0;
+        if (P.mode == 4) {
+          const unsigned long long tf0 = P.prof ? globaltimer() : 0;
+          const int32_t code = fetch_ready();
+          if (P.prof && lane == 0) atomicAdd(P.prof + 0, globaltimer() - tf0);
+          if (code < 0) {
+            nx.valid = false;
+            return;
+          }
+          const int32_t t = code >> 8;
+          nx.t = t;
+          nx.first = nx.last = code & 255;
+          nx.ofs = __ldg(P.tile_ofs + t);
+          nx.bytes = __ldg(P.tile_ofs + t + 1) - nx.ofs;
+          nx.r0 = __ldg(P.tile_row + t);
+          nx.rows = __ldg(P.tile_row + t + 1) - nx.r0;
+          nx.E = __ldg(P.tile_E + t);
+          nx.lo = nx.hi = t;
+          nx.nseg = P.xmode ? __ldg(P.tile_nseg + t) : 0;
+          nx.xent = nx.nseg ? __ldg(P.tile_xent + t) : 0;
+          nx.valid = true;
+          return;
+        }
         if (lane == 0) i = int32_t(atomicAdd(P.queue, 1ull) - P.queue_base);
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i >= P.n_items || i < 0) {
@@ -748,6 +856,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
       return ok;
     };
     auto push = [&](int p) {
+      const unsigned long long tq0 = P.prof ? globaltimer() : 0;
       if (lane == 0) {
         const uint32_t k = atomicAdd(&ring_ctr, 1u);
         const int ws = int(k % kWorkRing);
@@ -755,6 +864,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         w_slot[ws] = r;
         w_p[ws] = p;
         mbar_arrive(&full_bar[ws]);
+        if (P.prof) atomicAdd(P.prof + 1, globaltimer() - tq0);
       }
       __syncwarp();
     };
@@ -784,7 +894,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
       tma_pending = !glb;
       ++p_items;
       for (int p = cur.first; p <= cur.last; ++p) {
-        if (p > 1) {
+        if (p > 1 && P.mode != 4) {
           const unsigned long long t0 = P.prof ? globaltimer() : 0;
           if (!spin_deps(P, cur.lo, cur.hi, P.epoch_base + uint32_t(p - 1), &p_rounds)) {
             abort = true;
@@ -844,12 +954,10 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
     }
   } else {
     // ------------------------------------------------ consumer warps: compute only
-    unsigned long long t_wait = 0, t_comp = 0, n_it = 0;
+    unsigned long long n_it = 0;
     for (int k = 0;; ++k) {
       const int ws = k % kWorkRing;
-      const unsigned long long tw0 = P.prof ? globaltimer() : 0;
       mbar_wait(&full_bar[ws], uint32_t(k / kWorkRing) & 1);
-      const unsigned long long tw1 = P.prof ? globaltimer() : 0;
       const int r = w_slot[ws];
       if (r < 0) break;
       const int p = w_p[ws];
@@ -900,26 +1008,41 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
                                       rows, E, 0, warp, NC);
       }
       __syncwarp();
-      if (P.prof) {
-        t_wait += tw1 - tw0;
-        t_comp += globaltimer() - tw1;
-        ++n_it;
-      }
-      if (lane == 0) {
-        const uint32_t old = atom_add_acqrel_cta_smem(&w_done[ws], 1u);
-        if (old == NC - 1) {
+      ++n_it;
+      uint32_t old = 0;
+      if (lane == 0) old = atom_add_acqrel_cta_smem(&w_done[ws], 1u);
+      const bool last = __shfl_sync(0xffffffffu, old, 0) == uint32_t(NC - 1);
+      if (last) {
+        // this warp finished (t, p) last: every warp's rows are stored
+        if (P.mode == 4) {
+          if (p < P.n_powers) {
+            // count (t, p) towards each dependent (u, p+1); the increment that
+            // completes u's dependency range enqueues (u, p+1)
+            __syncwarp();
+            fence_acq_rel_gpu();
+            const int32_t a = __ldg(P.rdep_ptr + t), b = __ldg(P.rdep_ptr + t + 1);
+            for (int32_t i = a + lane; i < b; i += 32) {
+              const int32_t u = __ldg(P.rdep + i);
+              const uint32_t target = uint32_t(__ldg(P.dep_hi + u) - __ldg(P.dep_lo + u) + 1);
+              const uint32_t prev = atom_add_acqrel_gpu(P.rcnt + int64_t(p) * P.n_tiles + u, 1u);
+              if (prev + 1 == target) {
+                const uint32_t idx = atomicAdd(P.rctrl + 32, 1u);
+                st_release_s32(P.rqueue + idx, (u << 8) | (p + 1));
+              }
+            }
+          }
+          if (lane == 0) atomicAdd(P.rctrl + 96, 1u);
+        } else if (P.mode != 3 && lane == 0) {
+          st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
+        }
+        if (lane == 0) {
           w_done[ws] = 0;
-          if (P.mode != 3) st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
           if (p == h_last[r]) mbar_arrive(&free_bar[r]);  // release.cta: the slot may be refilled
         }
-        mbar_arrive(&empty_bar[ws]);
       }
+      if (lane == 0) mbar_arrive(&empty_bar[ws]);
     }
-    if (P.prof && lane == 0) {
-      atomicAdd(P.prof + 0, t_wait);
-      atomicAdd(P.prof + 1, t_comp);
-      atomicAdd(P.prof + 2, n_it);
-    }
+    if (P.prof && lane == 0) atomicAdd(P.prof + 2, n_it);
   }
 }
 
@@ -1168,6 +1291,11 @@ extern "C" int lmpk_tiling_destroy(lmpk_tiling* t) {
   cudaFree(t->d_dep_hi);
   cudaFree(t->d_tile_nseg);
   cudaFree(t->d_tile_xent);
+  cudaFree(t->d_rdep_ptr);
+  cudaFree(t->d_rdep);
+  cudaFree(t->d_rcnt);
+  cudaFree(t->d_rqueue);
+  cudaFree(t->d_rctrl);
   cudaFree(t->d_items);
   cudaFree(t->d_progress);
   cudaFree(t->d_blocks);
@@ -1530,6 +1658,24 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     items[i] = (t << 8) | g;
   }
   T->n_items = static_cast<int32_t>(items.size());
+  // reverse dependencies for the ready-queue walk (q = 1): u depends on t
+  // iff t lies in [dep_lo(u), dep_hi(u)]
+  if (q_used == 1) {
+    std::vector<int32_t> cnt(nt + 1, 0);
+    for (int32_t u = 0; u < nt; ++u)
+      for (int32_t t = T->h_dep_lo[u]; t <= T->h_dep_hi[u]; ++t) ++cnt[t + 1];
+    for (int32_t t = 0; t < nt; ++t) cnt[t + 1] += cnt[t];
+    std::vector<int32_t> rdep(std::max(cnt[nt], 1)), fill(cnt.begin(), cnt.end() - 1);
+    for (int32_t u = 0; u < nt; ++u)
+      for (int32_t t = T->h_dep_lo[u]; t <= T->h_dep_hi[u]; ++t) rdep[fill[t]++] = u;
+    LMPK_TRY(dmalloc(&T->d_rdep_ptr, nt + 1));
+    LMPK_TRY(dmalloc(&T->d_rdep, rdep.size()));
+    LMPK_TRY(dmalloc(&T->d_rcnt, size_t(p_m) * nt));
+    LMPK_TRY(dmalloc(&T->d_rqueue, size_t(p_m) * nt));
+    LMPK_TRY(dmalloc(&T->d_rctrl, 128));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_rdep_ptr, cnt.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_rdep, rdep.data(), rdep.size() * 4, cudaMemcpyHostToDevice, st));
+  }
   LMPK_TRY(dmalloc(&T->d_items, items.size()));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_items, items.data(), items.size() * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
@@ -1562,7 +1708,8 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
   }
   launch_count_add(ctx, 1);
   // every slot producer ends its grab sequence with exactly one failing grab
-  ctx->queue_base += uint64_t(Pm.n_items) + uint64_t(grid) * uint64_t(Pm.n_slots);
+  // (the ready-queue walk does not use the ticket counter)
+  if (Pm.mode != 4) ctx->queue_base += uint64_t(Pm.n_items) + uint64_t(grid) * uint64_t(Pm.n_slots);
   return LMPK_OK;
 }
 
@@ -1665,6 +1812,23 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   Pm.items = T->d_items;
   Pm.q = T->info.powers_per_item;
   Pm.n_items = T->n_items;
+  Pm.n_tiles = T->info.n_tiles;
+  if (Pm.q == 1 && T->d_rcnt && (flags & LMPK_FLAG_READY_QUEUE)) {
+    // ready-queue walk (opt-in; measured slower than the skewed-key walk on
+    // cfg2: 1.56 vs 1.02 ms -- exposed TMA and per-item atomics):
+    // reset the counters, the queue and its cursors
+    Pm.mode = 4;
+    Pm.rdep_ptr = T->d_rdep_ptr;
+    Pm.rdep = T->d_rdep;
+    Pm.rcnt = T->d_rcnt;
+    Pm.rqueue = T->d_rqueue;
+    Pm.rctrl = T->d_rctrl;
+    const size_t nt = size_t(T->info.n_tiles);
+    LMPK_CHECK_CUDA(cudaMemsetAsync(T->d_rcnt, 0, size_t(P) * nt * 4, st));
+    LMPK_CHECK_CUDA(cudaMemsetAsync(T->d_rqueue, 0xff, size_t(P) * nt * 4, st));
+    LMPK_CHECK_CUDA(cudaMemsetAsync(T->d_rctrl, 0, 128 * 4, st));
+    Pm.lead = int32_t(std::min<int64_t>(int64_t(T->info.max_fwd_reach) * P + T->info.queue_slack, INT32_MAX / 2));
+  }
   // co-residency of all CTAs is part of the deadlock-freedom argument.
   // LMPK_FLAG_NO_TMA: blocks are streamed from global memory by the
   // consumers, so no slot buffers -- the unified L1 is left to the gathers.

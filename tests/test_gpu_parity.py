@@ -251,3 +251,34 @@ def test_device_resident_power_vectors():
     assert res.y.on_device
     host = lm.run_plan(plan, x=x.cpu().numpy())
     assert np.array_equal(res.y.data.cpu().numpy(), host.y.data)
+
+
+@pytest.mark.parametrize("variant", ["ready_queue", "x_staged", "x_staged_misaligned"])
+def test_opt_in_walks_bitwise(variant, monkeypatch):
+    """Opt-in paths of the group kernel: the dependency-driven ready-queue walk
+    (LMPK_FLAG_READY_QUEUE) and x-segment staging (LMPK_XFRAC; a slot stride
+    that is not 16-byte aligned takes the cooperative-copy fallback)."""
+    import torch
+
+    a = lm.gen_stencil_3d(24, 2)
+    _, perm = lm.bfs_levels(a, 0)
+    ap = lm.permute_symmetric(a, perm)
+    n, k = a.n_rows, 6
+    x = np.random.default_rng(21).standard_normal(n)
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, x, k)
+    flags = 0
+    if variant.startswith("x_staged"):
+        monkeypatch.setenv("LMPK_XFRAC", "30")
+    else:
+        flags = _lib.FLAG_READY_QUEUE
+    t = K.Tiling(ap.device(), k, tile_nnz=700, slots=2, mode_flags=_lib.FLAG_MODE_STREAM)
+    if variant.startswith("x_staged"):
+        assert t.info["x_staged_tiles"] > 0
+    ld = n + (1 if variant == "x_staged_misaligned" and n % 2 == 0 else 0)
+    buf = torch.zeros((k + 1) * ld + 1, dtype=torch.float64, device="cuda")
+    y = buf[1:1 + (k + 1) * ld].view(k + 1, ld)[:, :n] if variant == "x_staged_misaligned" \
+        else buf[:(k + 1) * ld].view(k + 1, ld)
+    y[0] = torch.from_numpy(x)
+    for _ in range(3):
+        K.mpk_run(t, y, K.mpk_power_cfg(k), flags=flags)
+        assert np.array_equal(y.cpu().numpy(), ref)

@@ -31,4 +31,4 @@ for q, slots, tile, slack in json.loads(os.environ.get("SPECS", '[[1,2,0,0],[2,2
         cons_wait_us_per_item_warp=round(v[0] / nw / 1e3, 3), polls=v[3], notready_frac=round(v[4] / max(v[3], 1), 3),
         prod_alive_ms_per_cta=round(v[5] / 148 / 1e6, 3), items_grabbed=v[6],
         us_tma_wait_per_item=round(v[7] / max(v[6], 1) / 1e3, 3), us_dep_wait_per_item=round(v[8] / max(v[6], 1) / 1e3, 3),
-        us_free_wait_per_item=round(v[9] / max(v[6], 1) / 1e3, 3), us_xstage_per_item=round(v[11] / max(v[6], 1) / 1e3, 3), dep_rounds=v[3], xstaged=t.info.get('x_staged_tiles'))), flush=True)
+        us_free_wait_per_item=round(v[9] / max(v[6], 1) / 1e3, 3), us_xstage_per_item=round(v[11] / max(v[6], 1) / 1e3, 3), dep_rounds=v[3], ready_spins=v[13], q_items=v[14], p1_items=v[15], us_fetch_per_item=round(v[0] / max(v[6], 1) / 1e3, 3), us_push_per_item=round(v[1] / max(v[6], 1) / 1e3, 3), us_entrywait_per_qitem=round(v[10] / max(v[14], 1) / 1e3, 3), cas_fail=v[12], xstaged=t.info.get('x_staged_tiles'))), flush=True)
