@@ -54,7 +54,10 @@ namespace lmpk {
 
 constexpr uint32_t kEpochStride = 128;  // > LMPK_MAX_POWERS
 constexpr unsigned long long kWatchdogNs = 8ull * 1000 * 1000 * 1000;
-constexpr int kMaxSlots = 4;
+#ifndef LMPK_MAXSLOTS
+#define LMPK_MAXSLOTS 4
+#endif
+constexpr int kMaxSlots = LMPK_MAXSLOTS;
 constexpr int kWorkRing = 8;
 #ifndef LMPK_NC
 #define LMPK_NC 24
