@@ -123,3 +123,53 @@ def test_cfg3_and_cfg5_reduced_size():
         ref[0] = x[pre.perm.perm]
         C.mpk_baseline(rp, c, v, ref, k)
         assert np.array_equal(res.y.data, ref)
+
+
+@pytest.mark.parametrize("case", ["stencil3d", "27pt", "rmat"])
+def test_fast_fma_mode_within_north_star_tolerance(case):
+    """Without LMPK_FLAG_EXACT the ordered row sums use DFMA; the contract
+    (BASELINE.json north_star) is relative L2 error <= 1e-12 per power."""
+    import torch
+
+    from paper_2205_01598_b200 import kernels as K
+
+    a = {"stencil3d": lambda: lm.gen_stencil_3d(40, 2),
+         "27pt": lambda: lm.gen_stencil_3d27pt(24, seed=3),
+         "rmat": lambda: lm.gen_rmat(14)}[case]()
+    _, perm = lm.bfs_levels(a, 0)
+    ap = lm.permute_symmetric(a, perm)
+    k = 8
+    x = np.random.default_rng(5).uniform(-1, 1, a.n_rows)
+    ref = np.zeros((k + 1, a.n_rows))
+    ref[0] = x
+    C.mpk_baseline(ap.row_ptr, ap.col, ap.val, ref, k)
+    t = K.Tiling(ap.device(), k)
+    y = torch.zeros((k + 1, a.n_rows), dtype=torch.float64, device="cuda")
+    y[0] = torch.from_numpy(x)
+    K.mpk_run(t, y, K.mpk_power_cfg(k), exact=False)
+    got = y.cpu().numpy()
+    for p in range(1, k + 1):
+        rel = np.linalg.norm(got[p] - ref[p]) / max(np.linalg.norm(ref[p]), 1e-300)
+        assert rel <= 1e-12, (p, rel)
+
+
+def test_rmat_scale18_mpk_bitwise():
+    """Config-4 shape at scale 18 (262K rows, ~4.2M nnz, a giant level next to
+    113K singleton levels): the level-blocked walk equals k baseline sweeps."""
+    import torch
+
+    from paper_2205_01598_b200 import kernels as K
+
+    a = lm.gen_rmat(18)
+    _, perm = lm.bfs_levels(a, 0)
+    ap = lm.permute_symmetric(a, perm)
+    k = 6
+    x = np.random.default_rng(1).uniform(0, 1, a.n_rows)
+    ref = np.zeros((k + 1, a.n_rows))
+    ref[0] = x
+    C.mpk_baseline(ap.row_ptr, ap.col, ap.val, ref, k)
+    t = K.Tiling(ap.device(), k)
+    y = torch.zeros((k + 1, a.n_rows), dtype=torch.float64, device="cuda")
+    y[0] = torch.from_numpy(x)
+    K.mpk_run(t, y, K.mpk_power_cfg(k))
+    assert np.array_equal(y.cpu().numpy(), ref)
