@@ -90,6 +90,9 @@ int64_t lmpk_ctx_launch_count(const lmpk_ctx* ctx);
 /* Phase counters of the pipelined MPK kernels, collected only when the
  * environment variable LMPK_PROFILE is set at ctx creation (16 words). */
 int lmpk_ctx_profile(lmpk_ctx* ctx, unsigned long long* out, int reset);
+/* Debug: event trace of CTAs 0-1 of the last MPK launch (LMPK_PROFILE and
+ * LMPK_TRACE set at ctx creation); 16-byte records, returns the count. */
+int lmpk_ctx_trace(lmpk_ctx* ctx, void* out, int64_t max_records);
 
 /* ---------------------------------------------------------------- SpMV
  * out[r] = sum_k val[k]*x[col[k]] for r in [r0, r1); other rows untouched.

@@ -85,6 +85,7 @@ SIGNATURES = {
     "lmpk_ctx_launch_count": (_i64, [_vp]),
     "lmpk_ctx_check": (_int, [_vp, _vp]),
     "lmpk_ctx_profile": (_int, [_vp, _vp, _int]),
+    "lmpk_ctx_trace": (_int, [_vp, _vp, _i64]),
     "lmpk_spmv_rows": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _int, _vp]),
     "lmpk_mpk_baseline": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _i32, _int, _vp]),
     "lmpk_tiling_create": (_int, [_vp, _i32, _vp, _vp, _vp, _i32, ctypes.POINTER(TilingParams),

@@ -3,6 +3,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 
 #include "lmpk_internal.cuh"
@@ -115,8 +116,11 @@ extern "C" int lmpk_ctx_create(lmpk_ctx** out, int device) {
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->queue_ctr, 64);
   if (e == cudaSuccess && getenv("LMPK_PROFILE") != nullptr) {
-    e = cudaMalloc(&c->prof, 16 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(c->prof, 0, 16 * sizeof(unsigned long long));
+    // 16 phase counters + (LMPK_TRACE) an event trace of CTAs 0 and 1
+    const size_t words = 16 + (getenv("LMPK_TRACE") ? size_t(kTraceCtas) * kTraceEvents * 2 : 0);
+    c->prof_words = words;
+    e = cudaMalloc(&c->prof, words * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->prof, 0, words * sizeof(unsigned long long));
   }
   if (e == cudaSuccess) e = cudaMemset(c->queue_ctr, 0, 64);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -143,6 +147,19 @@ extern "C" int lmpk_ctx_destroy(lmpk_ctx* c) {
 }
 
 extern "C" int64_t lmpk_ctx_launch_count(const lmpk_ctx* c) { return c ? c->launches : 0; }
+
+// Event trace of the last MPK launch (LMPK_PROFILE + LMPK_TRACE at ctx
+// creation): per traced CTA kTraceEvents records {time_ns, kind | slot << 8 |
+// warp << 16, item}; returns the number of 16-byte records copied.
+extern "C" int lmpk_ctx_trace(lmpk_ctx* c, void* out, int64_t max_records) {
+  LMPK_ARG_CHECK(c && out, "lmpk_ctx_trace: NULL argument");
+  if (!c->prof || c->prof_words <= 16) return 0;
+  const int64_t n = std::min<int64_t>(max_records, int64_t(kTraceCtas) * kTraceEvents);
+  LMPK_CHECK_CUDA(cudaDeviceSynchronize());
+  LMPK_CHECK_CUDA(cudaMemcpy(out, c->prof + 16, size_t(n) * 16, cudaMemcpyDeviceToHost));
+  LMPK_CHECK_CUDA(cudaMemset(c->prof + 16, 0, (c->prof_words - 16) * sizeof(unsigned long long)));
+  return static_cast<int>(n);
+}
 
 // Phase counters of the pipelined kernels (LMPK_PROFILE=1 at ctx creation):
 // [0] consumer ns waiting for work, [1] consumer ns computing, [2] items

@@ -14,6 +14,9 @@
 
 namespace lmpk {
 
+constexpr int kTraceCtas = 2;        // CTAs traced with LMPK_TRACE
+constexpr int kTraceEvents = 16384;  // records per traced CTA
+
 // ------------------------------------------------------------------ errors
 void set_error(const char* fmt, ...);
 
@@ -73,6 +76,7 @@ struct lmpk_ctx {
   uint64_t* queue_ctr = nullptr;  // monotone work-queue counter (device)
   uint64_t queue_base = 0;        // host mirror of the counter value
   unsigned long long* prof = nullptr;  // phase counters when LMPK_PROFILE is set
+  size_t prof_words = 0;
 };
 
 // Tile geometry + the matrix re-laid out as tile-SELL-32 blocks (see mpk.cu).

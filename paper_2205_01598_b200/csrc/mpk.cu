@@ -111,7 +111,24 @@ struct MpkParams {
   int32_t flags;     // LMPK_FLAG_* (NO_TMA, policy bits 8-9)
   int* err;          // host-mapped
   unsigned long long* prof;  // optional phase counters (LMPK_PROFILE), else null
+  uint4* trace;              // optional event trace (LMPK_TRACE), else null
 };
+
+// Trace events (kind): producer 1 fetched, 2 TMA issued, 3 staged, 4 deps
+// ready, 5 pushed, 6 slot freed; consumer 10 item start, 11 item end, 12 last
+// warp published.
+__device__ __forceinline__ void trace_ev(const MpkParams& P, uint32_t* ctr, uint32_t kind, uint32_t slot,
+                                         uint32_t item) {
+  if (P.trace && blockIdx.x < kTraceCtas) {
+    const uint32_t i = atomicAdd(ctr, 1u);
+    if (i < uint32_t(kTraceEvents)) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      P.trace[blockIdx.x * kTraceEvents + i] =
+          make_uint4(uint32_t(t), uint32_t(t >> 32), kind | (slot << 8) | ((threadIdx.x >> 5) << 16), item);
+    }
+  }
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -133,6 +150,10 @@ __host__ __device__ inline int64_t align16(int64_t b) { return (b + 15) & ~int64
 // fills with one bulk copy per run once the dependencies of a power are met
 // (gathers then come from shared memory); nseg == 0 keeps global columns.
 constexpr int kMaxSegs = 64;
+#ifndef LMPK_TMA_SPLIT
+#define LMPK_TMA_SPLIT 1
+#endif
+constexpr int kTmaSplit = LMPK_TMA_SPLIT;  // concurrent bulk copies per staged block
 __host__ __device__ inline int64_t blk_seg_off(int32_t ns) { return align16(int64_t(ns) * 72); }
 __host__ __device__ inline int64_t blk_col_off(int32_t ns, int32_t nseg) {
   return blk_seg_off(ns) + int64_t(nseg) * 16;
@@ -657,7 +678,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
   __shared__ uint64_t full_bar[kWorkRing], empty_bar[kWorkRing];
   __shared__ int32_t w_slot[kWorkRing], w_p[kWorkRing];
   __shared__ uint32_t w_done[kWorkRing];
-  __shared__ uint32_t ring_ctr, prod_done;
+  __shared__ uint32_t ring_ctr, prod_done, trace_ctr;
   __shared__ int32_t h_t[kMaxSlots], h_last[kMaxSlots], h_glb[kMaxSlots];
   __shared__ int32_t h_r0[kMaxSlots], h_rows[kMaxSlots], h_E[kMaxSlots], h_nseg[kMaxSlots];
   __shared__ int64_t h_ofs[kMaxSlots];
@@ -678,6 +699,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
     }
     ring_ctr = 0;
     prod_done = 0;
+    trace_ctr = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -877,6 +899,8 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
     while (nx.valid && !abort) {
       const Next cur = nx;
       const bool glb = no_tma || cur.bytes > P.blk_cap;
+      const uint32_t tcode = uint32_t(cur.t) << 8 | uint32_t(cur.first);
+      if (lane == 0) trace_ev(P, &trace_ctr, 1, r, tcode);
       if (lane == 0) {
         h_t[r] = cur.t;
         h_last[r] = cur.last;
@@ -889,10 +913,23 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         if (!glb) {
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&tile_bar[r], uint32_t(cur.bytes));
-          bulk_g2s(smem_raw + int64_t(r) * P.smem_cap, P.blocks + cur.ofs, uint32_t(cur.bytes), &tile_bar[r],
+        }
+      }
+      __syncwarp();
+      if (!glb) {
+        // the block as kTmaSplit bulk copies (16-byte aligned pieces) on the
+        // slot's one barrier; 4 or 8 concurrent pieces measured no faster
+        // than one on cfg2 (the per-SM transfer is bandwidth-, not
+        // request-bound), so LMPK_TMA_SPLIT defaults to 1
+        const int64_t piece = ((cur.bytes + kTmaSplit - 1) / kTmaSplit + 15) & ~int64_t(15);
+        const int64_t a = int64_t(lane) * piece, b = std::min<int64_t>(a + piece, cur.bytes);
+        if (lane < kTmaSplit && b > a) {
+          if (lane) fence_proxy_async_smem();
+          bulk_g2s(smem_raw + int64_t(r) * P.smem_cap + a, P.blocks + cur.ofs + a, uint32_t(b - a), &tile_bar[r],
                    cur.last == P.n_powers ? pol_drop : pol_keep);
         }
       }
+      if (lane == 0) trace_ev(P, &trace_ctr, 2, r, tcode);
       __syncwarp();
       tma_pending = !glb;
       ++p_items;
@@ -904,6 +941,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
             break;
           }
           if (P.prof) p_dep += globaltimer() - t0;
+          if (lane == 0) trace_ev(P, &trace_ctr, 4, r, tcode);
         }
         if (tma_pending) {
           const unsigned long long t0 = P.prof ? globaltimer() : 0;
@@ -915,6 +953,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
             break;
           }
           if (P.prof) p_tma += globaltimer() - t0;
+          if (lane == 0) trace_ev(P, &trace_ctr, 3, r, tcode);
         }
         if (P.xmode == 1 && !glb && cur.nseg > 0) {
           const unsigned long long t0 = P.prof ? globaltimer() : 0;
@@ -925,6 +964,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
           if (P.prof) p_x += globaltimer() - t0;
         }
         push(p);
+        if (lane == 0) trace_ev(P, &trace_ctr, 5, r, tcode);
         if (p == cur.first && prefetch) fetch_next();
       }
       if (abort) break;
@@ -934,6 +974,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         break;
       }
       ++frees;
+      if (lane == 0) trace_ev(P, &trace_ctr, 6, r, tcode);
       if (P.prof) p_free += globaltimer() - t0;
       if (!prefetch) fetch_next();
     }
@@ -966,6 +1007,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
       const int p = w_p[ws];
       const int32_t t = h_t[r];
       const int32_t r0 = h_r0[r], rows = h_rows[r];
+      if (lane == 0 && (warp == 0 || warp == NC - 1)) trace_ev(P, &trace_ctr, 10, r, uint32_t(t) << 8 | uint32_t(p));
       const uint32_t E = uint32_t(h_E[r]);
       const PowTab& pt = s_pow[p - 1];
       const bool use_acc = P.use_acc != 0;
@@ -1012,11 +1054,23 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
       }
       __syncwarp();
       ++n_it;
+      if (lane == 0 && (warp == 0 || warp == NC - 1)) trace_ev(P, &trace_ctr, 11, r, uint32_t(t) << 8 | uint32_t(p));
       uint32_t old = 0;
       if (lane == 0) old = atom_add_acqrel_cta_smem(&w_done[ws], 1u);
       const bool last = __shfl_sync(0xffffffffu, old, 0) == uint32_t(NC - 1);
       if (last) {
-        // this warp finished (t, p) last: every warp's rows are stored
+        // this warp finished (t, p) last: every warp's rows are stored and
+        // every warp is done reading the slot.  Free the slot and the ring
+        // entry FIRST (CTA-scope releases), then publish at gpu scope -- the
+        // release fence of the publish waits for this warp's global stores
+        // (~1.4 us) and must not delay the refill.
+        if (lane == 0) {
+          trace_ev(P, &trace_ctr, 12, r, uint32_t(t) << 8 | uint32_t(p));
+          const int last_p = h_last[r];
+          w_done[ws] = 0;
+          if (p == last_p) mbar_arrive(&free_bar[r]);  // release.cta: the slot may be refilled
+          mbar_arrive(&empty_bar[ws]);
+        }
         if (P.mode == 4) {
           if (p < P.n_powers) {
             // count (t, p) towards each dependent (u, p+1); the increment that
@@ -1038,12 +1092,9 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         } else if (P.mode != 3 && lane == 0) {
           st_release_u32(P.progress + t, P.epoch_base + uint32_t(p));
         }
-        if (lane == 0) {
-          w_done[ws] = 0;
-          if (p == h_last[r]) mbar_arrive(&free_bar[r]);  // release.cta: the slot may be refilled
-        }
+      } else if (lane == 0) {
+        mbar_arrive(&empty_bar[ws]);
       }
-      if (lane == 0) mbar_arrive(&empty_bar[ws]);
     }
     if (P.prof && lane == 0) atomicAdd(P.prof + 2, n_it);
   }
@@ -1779,6 +1830,7 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   Pm.flags = flags;
   Pm.err = ctx->err.dev;
   Pm.prof = ctx->prof;
+  Pm.trace = (ctx->prof && ctx->prof_words > 16) ? reinterpret_cast<uint4*>(ctx->prof + 16) : nullptr;
   const int grid = T->info.grid;
   if (sweep) {
     // n_powers back-to-back, dependency-free passes (one launch per power)
