@@ -154,6 +154,37 @@ def window_csr(row_ptr, col, val, lo: int, hi: int):
     return rp, (c[keep] - lo).astype(np.int32), np.ascontiguousarray(val[e0:e1][keep])
 
 
+def _real_view(v):
+    import torch
+
+    return torch.view_as_real(v) if v.is_complex() else v
+
+
+def halo_exchange(shards: "LevelShards", rank: int, group, vecs):
+    """One batched P2P group: for every window-local vector, send my first /
+    last owned rows to the left / right neighbour (their halos) and receive
+    my left / right halo from them (NCCL over NVLink on GPUs, gloo on CPU)."""
+    if shards.world == 1:
+        return
+    import torch.distributed as dist
+
+    s = shards[rank]
+    o0, o1 = s.own_offset, s.own_offset + s.n_own
+    ops = []
+    for v in vecs:
+        v = _real_view(v)
+        if rank > 0:
+            left = shards[rank - 1]
+            ops.append(dist.P2POp(dist.isend, v[o0:o0 + left.right_halo], rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, v[0:s.left_halo], rank - 1, group))
+        if rank < shards.world - 1:
+            right = shards[rank + 1]
+            ops.append(dist.P2POp(dist.isend, v[o1 - right.left_halo:o1], rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, v[o1:o1 + s.right_halo], rank + 1, group))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
 class CudaWindowMpk:
     """Local MPK on one rank's window: the single-GPU level-blocked kernel."""
 
@@ -195,26 +226,9 @@ class DistMpk:
         self.local = local if local is not None else CudaWindowMpk(rp, c, v, k, **tiling_kw)
         self.y = torch.zeros((k + 1, s.n_win), dtype=torch.float64, device=self.device)
 
-    def exchange(self, y0):
-        """Fill the halo rows of y0 (window-local) from the neighbour ranks."""
-        if self.world == 1:
-            return
-        import torch.distributed as dist
-
-        s, shards = self.shard, self.shards
-        ops = []
-        o0, o1 = s.own_offset, s.own_offset + s.n_own
-        if self.rank > 0:
-            left = shards[self.rank - 1]
-            # my first rows are rank-1's right halo; rank-1's last rows are my left halo
-            ops.append(dist.P2POp(dist.isend, y0[o0:o0 + left.right_halo], self.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, y0[0:s.left_halo], self.rank - 1, self.group))
-        if self.rank < self.world - 1:
-            right = shards[self.rank + 1]
-            ops.append(dist.P2POp(dist.isend, y0[o1 - right.left_halo:o1], self.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, y0[o1:o1 + s.right_halo], self.rank + 1, self.group))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    def exchange(self, *vecs):
+        """Fill the halo rows of window-local vectors from the neighbour ranks."""
+        halo_exchange(self.shards, self.rank, self.group, vecs)
 
     def run(self, x_own, check_errors=True):
         s = self.shard
@@ -227,3 +241,102 @@ class DistMpk:
     @property
     def redundant_flops(self) -> int:
         return self.shards.redundant_flops(self.rank)
+
+
+def cheb_batch_config(coeffs_c, k_base, pb, n_slots, first_batch):
+    """Per-power slots/kernels/coefficients of one Chebyshev batch over a ring
+    of n_slots state vectors (cheb.py:209-219, ChebPropagator._configure)."""
+    from .plan import KERNEL_CHEB, KERNEL_SPMV
+
+    p = np.arange(1, pb + 1)
+    out_slot = (k_base + p) % n_slots
+    in_slot = (k_base + p - 1) % n_slots
+    prev_slot = (k_base + p - 2) % n_slots
+    kernel = np.full(pb, KERNEL_CHEB)
+    if first_batch:
+        kernel[0] = KERNEL_SPMV
+    c = np.asarray(coeffs_c)[k_base + 1:k_base + pb + 1]
+    return out_slot, in_slot, prev_slot, kernel, np.real(c), (np.imag(c) if np.iscomplexobj(c) else None)
+
+
+class CudaWindowCheb:
+    """Chebyshev batches on one rank's window through the level-blocked kernel."""
+
+    def __init__(self, rp, col, val, p_b, complex_state, **tiling_kw):
+        from . import _lib
+        from . import kernels as K
+
+        self.K, self._lib = K, _lib
+        self.a = K.DeviceCsr.from_host(rp, col, val)
+        flags = int(tiling_kw.pop("mode_flags", 0)) | (_lib.FLAG_COMPLEX if complex_state else 0)
+        self.tiling = K.Tiling(self.a, p_b, mode_flags=flags, **tiling_kw)
+        self.complex = complex_state
+
+    def __call__(self, ring, acc, coeffs_c, k_base, pb, first_batch):
+        import torch
+
+        o, i, pv, kern, cre, cim = cheb_batch_config(coeffs_c, k_base, pb, ring.shape[0], first_batch)
+        cfg = self.K.power_cfg(pb, o, i, pv, kern, cre, cim)
+        yv = torch.view_as_real(ring).reshape(ring.shape[0], -1) if self.complex else ring
+        av = torch.view_as_real(acc).reshape(-1) if self.complex else acc
+        self.K.mpk_run(self.tiling, yv, cfg, acc=av, use_acc=True, complex_state=self.complex)
+
+
+class DistCheb:
+    """Level-range sharded Chebyshev propagation (BASELINE config 5 shape).
+
+    Every rank holds a ring of p_b + 2 Chebyshev states T_k over its window
+    (depth-p_b halo).  Before each batch of <= p_b powers the halos of the two
+    newest states (T_k and T_{k-1}) are exchanged in one P2P group; the
+    accumulator needs no exchange (only owned rows are returned).  Owned rows
+    are bitwise identical to the single-GPU propagator: the same rows, entries
+    and summation order.  ``local(ring, acc, coeffs_c, k_base, pb, first)``
+    runs one batch on the window (CUDA by default)."""
+
+    def __init__(self, row_ptr, col, val, level_ptr, level_nnz, coeffs_c, p_b, rank, world, group=None,
+                 device=None, local=None, complex_state=None, **tiling_kw):
+        import torch
+
+        self.torch = torch
+        self.c = np.asarray(coeffs_c)
+        self.complex = bool(np.iscomplexobj(self.c)) if complex_state is None else bool(complex_state)
+        self.m = self.c.shape[0] - 1
+        self.p_b = max(1, min(int(p_b), self.m)) if self.m >= 1 else 1
+        self.rank, self.world, self.group = rank, world, group
+        self.shards = LevelShards(level_ptr, level_nnz, world, self.p_b)
+        s = self.shard = self.shards[rank]
+        rp, c, v = window_csr(row_ptr, col, val, s.win_lo, s.win_hi)
+        self.device = torch.device("cpu") if device is None else torch.device(device)
+        self.local = local if local is not None else CudaWindowCheb(rp, c, v, self.p_b, self.complex, **tiling_kw)
+        dt = torch.complex128 if self.complex else torch.float64
+        self.ring = torch.zeros((self.p_b + 2, s.n_win), dtype=dt, device=self.device)
+
+    def step(self, x_own):
+        """One propagation step; x_own = T_0 on the owned rows (level-permuted
+        order).  Returns acc = sum_k c_k T_k on the owned rows."""
+        torch = self.torch
+        s, S = self.shard, self.ring.shape[0]
+        ring = self.ring
+        o0, o1 = s.own_offset, s.own_offset + s.n_own
+        ring[0, o0:o1].copy_(torch.as_tensor(x_own, device=self.device).to(ring.dtype))
+        halo_exchange(self.shards, self.rank, self.group, [ring[0]])
+        c0 = complex(self.c[0]) if self.complex else float(np.real(self.c[0]))
+        if self.complex:
+            # acc = c_0 * T_0 with the product spelled out (oracle order)
+            acc = torch.empty_like(ring[0])
+            acc.real.copy_(ring[0].real * c0.real - ring[0].imag * c0.imag)
+            acc.imag.copy_(ring[0].imag * c0.real + ring[0].real * c0.imag)
+        else:
+            acc = ring[0] * c0
+        k = 0
+        while k < self.m:
+            pb = min(self.p_b, self.m - k)
+            if k > 0:
+                halo_exchange(self.shards, self.rank, self.group, [ring[k % S], ring[(k - 1) % S]])
+            self.local(ring, acc, self.c, k, pb, k == 0)
+            k += pb
+        return acc[o0:o1]
+
+    @property
+    def redundant_flops_per_step(self) -> int:
+        return self.shards.redundant_flops(self.rank) // self.p_b * max(self.m, 1)

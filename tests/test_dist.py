@@ -179,3 +179,104 @@ def test_gpu_shard_windows_bitwise_equal_single_gpu(world):
         loc(yw)
         got = yw[:, s.own_offset:s.own_offset + s.n_own].cpu().numpy()
         assert np.array_equal(got, ref[:, s.own_lo:s.own_hi])
+
+
+def _cheb_window_batch(rp, c, v):
+    """Test-only CPU restatement of one Chebyshev batch on a window (the GPU
+    kernel's per-power semantics, oracle spmv), in place on the torch ring."""
+    import torch
+
+    def run(ring, acc, coeffs_c, k_base, pb, first):
+        S = ring.shape[0]
+        cplx = ring.is_complex()
+        R = ring.numpy()
+        A = acc.numpy()
+        for p in range(1, pb + 1):
+            k = k_base + p
+            tin, tprev = R[(k - 1) % S], R[(k - 2) % S]
+            if cplx:
+                tr = O.spmv(rp, c, v, np.ascontiguousarray(tin.real))
+                ti = O.spmv(rp, c, v, np.ascontiguousarray(tin.imag))
+                if not (first and p == 1):
+                    tr = 2.0 * tr - tprev.real
+                    ti = 2.0 * ti - tprev.imag
+                cr, ci = float(np.real(coeffs_c[k])), float(np.imag(coeffs_c[k]))
+                ar = A.real + (cr * tr - ci * ti)
+                ai = A.imag + (cr * ti + ci * tr)
+                R[k % S] = tr + 1j * ti
+                A[...] = ar + 1j * ai
+            else:
+                t = O.spmv(rp, c, v, np.ascontiguousarray(tin))
+                if not (first and p == 1):
+                    t = 2.0 * t - tprev
+                R[k % S] = t
+                A[...] = A + float(np.real(coeffs_c[k])) * t
+        return ring
+
+    return run
+
+
+def _gloo_cheb_worker(rank, world, port, p_b, cplx, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_01598_b200.dist import DistCheb, window_csr
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        prp, pcol, pval, lp, lnnz = _level_permuted(12)
+        n = prp.shape[0] - 1
+        rng = np.random.default_rng(17)
+        coeffs = rng.uniform(-1, 1, 11) + (1j * rng.uniform(-1, 1, 11) if cplx else 0)
+        x = rng.uniform(-1, 1, n) + (1j * rng.uniform(-1, 1, n) if cplx else 0)
+        sh = LevelShards(lp, lnnz, world, p_b)
+        s = sh[rank]
+        rp, c, v = window_csr(prp, pcol, pval, s.win_lo, s.win_hi)
+        dc = DistCheb(prp, pcol, pval, lp, lnnz, coeffs, p_b, rank, world, local=_cheb_window_batch(rp, c, v))
+        out = dc.step(torch.from_numpy(np.asarray(x[s.own_lo:s.own_hi])))
+        np.save(os.path.join(out_dir, f"cheb{rank}.npy"), out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,p_b,cplx", [(2, 4, True), (3, 3, False), (2, 3, True)])
+def test_gloo_sharded_chebyshev_bitwise(tmp_path, world, p_b, cplx):
+    """Config-5 shape on CPU ranks: sharded Chebyshev propagation (halo of the
+    two newest states exchanged per batch) equals the single-rank oracle."""
+    import torch.multiprocessing as mp
+
+    port = _free_port()
+    mp.start_processes(_gloo_cheb_worker, args=(world, port, p_b, cplx, str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    prp, pcol, pval, lp, lnnz = _level_permuted(12)
+    n = prp.shape[0] - 1
+    rng = np.random.default_rng(17)
+    coeffs = rng.uniform(-1, 1, 11) + (1j * rng.uniform(-1, 1, 11) if cplx else 0)
+    x = rng.uniform(-1, 1, n) + (1j * rng.uniform(-1, 1, n) if cplx else 0)
+    ref = O.cheb_batches(prp, pcol, pval, x, np.real(coeffs), np.imag(coeffs) if cplx else None)
+    sh = LevelShards(lp, lnnz, world, p_b)
+    for g, s in enumerate(sh.shards):
+        got = np.load(tmp_path / f"cheb{g}.npy")
+        assert np.array_equal(got, ref[s.own_lo:s.own_hi]), g
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cplx,p_b", [(True, 4), (False, 3)])
+def test_gpu_dist_cheb_window_runner_vs_oracle(cplx, p_b):
+    """DistCheb's CUDA batch runner (world 1: the window is the whole matrix)
+    against the oracle propagation, bitwise."""
+    import torch
+
+    from paper_2205_01598_b200.dist import DistCheb
+
+    prp, pcol, pval, lp, lnnz = _level_permuted(20)
+    n = prp.shape[0] - 1
+    rng = np.random.default_rng(23)
+    coeffs = rng.uniform(-1, 1, 13) + (1j * rng.uniform(-1, 1, 13) if cplx else 0)
+    x = rng.uniform(-1, 1, n) + (1j * rng.uniform(-1, 1, n) if cplx else 0)
+    dc = DistCheb(prp, pcol, pval, lp, lnnz, coeffs, p_b, 0, 1, device="cuda")
+    got = dc.step(torch.from_numpy(np.asarray(x)).cuda()).cpu().numpy()
+    ref = O.cheb_batches(prp, pcol, pval, x, np.real(coeffs), np.imag(coeffs) if cplx else None)
+    assert np.array_equal(got, ref)
