@@ -67,6 +67,9 @@ extern "C" {
                                     /* same tiles -- the blocking-free baseline */
 #define LMPK_FLAG_EXACT 0x400       /* bit-exact row sums (see Summation below) */
 #define LMPK_FLAG_READY_QUEUE 0x1000 /* q = 1: dependency-driven ready-queue walk */
+#define LMPK_FLAG_COMPRESS 0x2000   /* tiling: compressed tile blocks (int16     */
+                                    /* column offsets, per-tile dictionary of   */
+                                    /* <= 256 values), bitwise-identical sums   */
                                      /* instead of the skewed-key item order      */
 /* bits 8-9 (0x100, 0x200): L2 eviction policy of staged blocks that a later
  * power group re-reads: 0 evict_last, 1 evict_normal, 2/3 evict_first.      */
@@ -135,6 +138,9 @@ typedef struct lmpk_tiling_info {
   int32_t powers_per_item; /* q: powers computed per staged tile block          */
   int32_t slots;         /* R: staged items held per CTA                        */
   int32_t x_staged_tiles; /* tiles whose gathers come from a staged x buffer    */
+  int32_t compressed_tiles; /* tiles in the compressed block format (int16      */
+                            /* column offsets; LMPK_FLAG_COMPRESS)              */
+  int32_t dict_tiles;    /* compressed tiles with a value dictionary (<= 256)   */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */

@@ -91,6 +91,7 @@ struct lmpk_tiling {
   int32_t* d_dep_hi = nullptr;     // [n_tiles]
   int32_t* d_tile_nseg = nullptr;  // [n_tiles] x-segments (0: global columns)
   int32_t* d_tile_xent = nullptr;  // [n_tiles] x-buffer entries
+  int32_t* d_tile_mode = nullptr;  // [n_tiles] compressed block format (NULL: all plain)
   int32_t staged_tiles = 0, max_xent = 0;
   int64_t xoff = 0;                // byte offset of the x buffer in a slot (0: no staging)
   int32_t* d_rdep_ptr = nullptr;   // [n_tiles+1] reverse dependencies (ready-queue walk)
@@ -172,6 +173,24 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// try_wait with a suspend-time hint: the warp sleeps in the barrier unit until
+// the phase completes (or ~hint ns pass) instead of re-issuing the poll, so
+// idle warps leave the issue slots to the warps that compute.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait_sleep(bar, parity, 1000000u)) {
   }
 }
 
@@ -289,6 +308,11 @@ struct SmemBlk {
   __device__ __forceinline__ uint32_t u16(uint32_t o) const {
     uint16_t v;
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a + o));
+    return v;
+  }
+  __device__ __forceinline__ uint32_t u8(uint32_t o) const {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a + o));
     return v;
   }
 };

@@ -90,6 +90,7 @@ struct MpkParams {
   int32_t n_tiles;
   const int32_t* tile_nseg;  // x-segments per tile (0: global columns)
   const int32_t* tile_xent;  // x-buffer entries per tile
+  const int32_t* tile_mode;  // compressed block format per tile (kModeC16 | kModeDict | nd << 8), 0 = plain
   const int32_t* items;  // packed (t << 8) | g in queue order (NULL: item i = tile i, g = 0)
   double* y;
   int64_t ldy;
@@ -482,6 +483,311 @@ __device__ __forceinline__ double slice_real(const Blk& B, uint32_t cb, uint32_t
   }
 }
 
+// ---------------------------------------------------------------- compressed blocks
+// Compressed tile block (tile_mode bit 0): the same slices, chunks and entry
+// order as above, but
+//   * columns are int16 offsets from the entry's own row (col - row): a
+//     level-ordered matrix couples a row only to its own and the adjacent
+//     levels, so the offsets stay within +-32767 for level widths up to that
+//     (index compression in the style of CSR-DU, Kourtis et al. 2008);
+//   * values are either raw f64, or (tile_mode bit 1) uint8 codes into a
+//     per-tile dictionary of <= 256 distinct values (CSR-VI value indexing).
+//     The dictionary holds the exact bit patterns, so every product is the
+//     same double as from the CRS arrays and the row sums stay bitwise equal.
+// Layout: [rec int2 x ns] [lens u16 x 32 ns] | align16 | [dict f64 x nd]
+//   | align16 | [col16 x E] | align16 | [code u8 x E  or  val f64 x E]
+// rec[s] = {first entry of slice s (relative to the tile), w | wmin << 16}.
+// Matrix bytes per entry: 3 (dictionary) or 10 (raw) instead of 12.
+constexpr int kDictMax = 256;
+constexpr int32_t kModeC16 = 1, kModeDict = 2;
+__host__ __device__ inline int64_t cblk_dict_off(int32_t ns) { return align16(int64_t(ns) * 72); }
+__host__ __device__ inline int64_t cblk_col_off(int32_t ns, int32_t nd) {
+  return align16(cblk_dict_off(ns) + int64_t(nd) * 8);
+}
+__host__ __device__ inline int64_t cblk_val_off(int32_t ns, int32_t nd, int64_t E) {
+  return align16(cblk_col_off(ns, nd) + E * 2);
+}
+__host__ __device__ inline int64_t cblk_bytes(int32_t ns, int32_t nd, int64_t E, bool dict) {
+  return (cblk_val_off(ns, nd, E) + E * (dict ? 1 : 8) + 127) & ~int64_t(127);
+}
+__device__ __forceinline__ int32_t sx16(int32_t v) { return (v << 16) >> 16; }
+
+// Column indices of lane's W entries (row = the lane's row).
+template <int W>
+__device__ __forceinline__ void c16_cols(const SmemBlk& B, uint32_t cb, uint32_t lane, int32_t row,
+                                         int32_t (&c)[W]) {
+  constexpr int Q = W >> 2, PR = (W >> 1) & 1, SG = W & 1;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int2 v = B.i2(cb + q * 256 + lane * 8);
+    c[4 * q] = row + sx16(v.x);
+    c[4 * q + 1] = row + (v.x >> 16);
+    c[4 * q + 2] = row + sx16(v.y);
+    c[4 * q + 3] = row + (v.y >> 16);
+  }
+  if constexpr (PR) {
+    const int32_t v = B.i1(cb + Q * 256 + lane * 4);
+    c[4 * Q] = row + sx16(v);
+    c[4 * Q + 1] = row + (v >> 16);
+  }
+  if constexpr (SG) c[W - 1] = row + sx16(int32_t(B.u16(cb + Q * 256 + PR * 128 + lane * 2)));
+}
+
+// Values of lane's W entries: dictionary codes (VD) or raw f64.
+template <int W, bool VD>
+__device__ __forceinline__ void c16_vals(const SmemBlk& B, uint32_t vb, uint32_t lane, uint32_t dict,
+                                         double (&v)[W]) {
+  constexpr int Q = W >> 2, PR = (W >> 1) & 1, SG = W & 1;
+  if constexpr (VD) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const uint32_t k = uint32_t(B.i1(vb + q * 128 + lane * 4));
+      v[4 * q] = lds_f64(dict + (k & 255u) * 8u);
+      v[4 * q + 1] = lds_f64(dict + ((k >> 8) & 255u) * 8u);
+      v[4 * q + 2] = lds_f64(dict + ((k >> 16) & 255u) * 8u);
+      v[4 * q + 3] = lds_f64(dict + (k >> 24) * 8u);
+    }
+    if constexpr (PR) {
+      const uint32_t k = B.u16(vb + Q * 128 + lane * 2);
+      v[4 * Q] = lds_f64(dict + (k & 255u) * 8u);
+      v[4 * Q + 1] = lds_f64(dict + (k >> 8) * 8u);
+    }
+    if constexpr (SG) v[W - 1] = lds_f64(dict + B.u8(vb + Q * 128 + PR * 64 + lane) * 8u);
+  } else {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const double2 a = B.d2(vb + q * 1024 + lane * 32), b = B.d2(vb + q * 1024 + lane * 32 + 16);
+      v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = b.x, v[4 * q + 3] = b.y;
+    }
+    if constexpr (PR) {
+      const double2 a = B.d2(vb + Q * 1024 + lane * 16);
+      v[4 * Q] = a.x, v[4 * Q + 1] = a.y;
+    }
+    if constexpr (SG) v[W - 1] = B.d1(vb + Q * 1024 + PR * 512 + lane * 8);
+  }
+}
+
+// Byte offsets of a compressed slice's column / value arrays (entry e_s).
+struct CSlice {
+  uint32_t cb, vb;
+};
+template <bool VD>
+__device__ __forceinline__ CSlice cslice(uint32_t col_o, uint32_t val_o, uint32_t e_s) {
+  return CSlice{col_o + e_s * 2u, val_o + e_s * (VD ? 1u : 8u)};
+}
+
+template <bool EXACT, bool FULL, int W>
+__device__ __forceinline__ double chain(const double (&v)[W], const double (&x)[W], int len) {
+  double t = 0.0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    if constexpr (FULL)
+      t = madd<EXACT>(t, v[j], x[j]);
+    else
+      madd_if<EXACT>(t, v[j], x[j], j, len);
+  }
+  return t;
+}
+
+// One compressed slice of width W <= 8 (real vectors).
+template <int W, bool EXACT, bool FULL, bool VD, class G>
+__device__ __forceinline__ double cslice_real_w(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row,
+                                                uint32_t dict, const G& g, int len) {
+  int32_t c[W];
+  c16_cols<W>(B, a.cb, lane, row, c);
+  double x[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) x[j] = g.d(c[j]);
+  double v[W];
+  c16_vals<W, VD>(B, a.vb, lane, dict, v);
+  return chain<EXACT, FULL, W>(v, x, len);
+}
+
+// Two compressed slices of the same width W <= 8: all gathers in flight together.
+template <int W, bool EXACT, bool FULL, bool VD, class G>
+__device__ __forceinline__ double2 cslice_real_w2(const SmemBlk& B, CSlice a0, CSlice a1, uint32_t lane,
+                                                  int32_t row0, int32_t row1, uint32_t dict, const G& g,
+                                                  int len0, int len1) {
+  int32_t c0[W], c1[W];
+  c16_cols<W>(B, a0.cb, lane, row0, c0);
+  c16_cols<W>(B, a1.cb, lane, row1, c1);
+  double x0[W], x1[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) x0[j] = g.d(c0[j]);
+#pragma unroll
+  for (int j = 0; j < W; ++j) x1[j] = g.d(c1[j]);
+  double t0, t1;
+  {
+    double v[W];
+    c16_vals<W, VD>(B, a0.vb, lane, dict, v);
+    t0 = chain<EXACT, FULL, W>(v, x0, len0);
+  }
+  {
+    double v[W];
+    c16_vals<W, VD>(B, a1.vb, lane, dict, v);
+    t1 = chain<EXACT, FULL, W>(v, x1, len1);
+  }
+  return make_double2(t0, t1);
+}
+
+// Any width (real or complex vectors), one entry at a time in chunk order.
+template <bool CPLX, bool EXACT, bool VD, class G>
+__device__ __noinline__ double2 cslice_any(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
+                                           const G& g, int w, int len) {
+  double tr = 0.0, ti = 0.0;
+  const int Q = w >> 2, PR = (w >> 1) & 1;
+  for (int j = 0; j < w; ++j) {
+    uint32_t ec;  // entry offset inside the slice (chunk order of chunk_entry)
+    if (j < 4 * Q)
+      ec = uint32_t(j >> 2) * 128u + lane * 4u + uint32_t(j & 3);
+    else if (PR && j < 4 * Q + 2)
+      ec = uint32_t(Q) * 128u + lane * 2u + uint32_t(j - 4 * Q);
+    else
+      ec = uint32_t(Q) * 128u + (PR ? 64u : 0u) + lane;
+    const int32_t c = row + sx16(int32_t(B.u16(a.cb + ec * 2u)));
+    double v;
+    if constexpr (VD)
+      v = lds_f64(dict + B.u8(a.vb + ec) * 8u);
+    else
+      v = B.d1(a.vb + ec * 8u);
+    if constexpr (CPLX) {
+      const double2 x = g.d2(c);
+      madd_if<EXACT>(tr, v, x.x, j, len);
+      madd_if<EXACT>(ti, v, x.y, j, len);
+    } else {
+      madd_if<EXACT>(tr, v, g.d(c), j, len);
+    }
+  }
+  return make_double2(tr, ti);
+}
+
+template <bool EXACT, bool FULL, bool VD, class G>
+__device__ __forceinline__ double cslice_real(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row,
+                                              uint32_t dict, const G& g, int w, int len) {
+  switch (w) {
+    case 1: return cslice_real_w<1, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 2: return cslice_real_w<2, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 3: return cslice_real_w<3, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 4: return cslice_real_w<4, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 5: return cslice_real_w<5, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 6: return cslice_real_w<6, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 7: return cslice_real_w<7, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 8: return cslice_real_w<8, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
+    case 0: return 0.0;
+    default: return cslice_any<false, EXACT, VD>(B, a, lane, row, dict, g, w, FULL ? w : len).x;
+  }
+}
+
+template <bool EXACT, bool FULL, bool VD, class G>
+__device__ __forceinline__ double2 cslice_real_pair(const SmemBlk& B, CSlice a0, CSlice a1, uint32_t lane,
+                                                    int32_t row0, int32_t row1, uint32_t dict, const G& g, int w,
+                                                    int len0, int len1) {
+  switch (w) {
+    case 1: return cslice_real_w2<1, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    case 2: return cslice_real_w2<2, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    case 3: return cslice_real_w2<3, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    case 4: return cslice_real_w2<4, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    case 5: return cslice_real_w2<5, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    case 6: return cslice_real_w2<6, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    case 7: return cslice_real_w2<7, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+    default: return cslice_real_w2<8, EXACT, FULL, VD>(B, a0, a1, lane, row0, row1, dict, g, len0, len1);
+  }
+}
+
+// One power step of one COMPRESSED tile (see tile_power for the contract).
+template <bool CPLX, bool EXACT, bool GENERAL, bool VD, class G>
+__device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base, bool use_acc, const SmemBlk& B,
+                                             const G& g, int32_t r0, int32_t nrows, uint32_t E, int32_t nd,
+                                             int wid, int nwarps) {
+  const int32_t ns = (nrows + 31) >> 5;
+  const uint32_t lens_o = uint32_t(ns) * 8;
+  const uint32_t dict = B.a + uint32_t(cblk_dict_off(ns));
+  const uint32_t col_o = uint32_t(cblk_col_off(ns, nd));
+  const uint32_t val_o = uint32_t(cblk_val_off(ns, nd, E));
+  const uint32_t lane = threadIdx.x & 31;
+  constexpr int cw = CPLX ? 2 : 1;
+  double* yout = pt.yout + int64_t(r0) * cw;
+  const double* ypv = pt.ypv + int64_t(r0) * cw;
+  double* acc = acc_base + int64_t(r0) * cw;
+  auto len_of = [&](int32_t s, int2 rec) -> int {
+    const int w = rec.y & 0xffff;
+    return int(uint32_t(rec.y) >> 16) == w ? w : int(B.u16(lens_o + uint32_t(s) * 64 + lane * 2));
+  };
+  if constexpr (!CPLX) {
+    auto epilogue = [&](int32_t s, double t) {
+      const int32_t lr = s * 32 + int32_t(lane);
+      if (lr < nrows) {
+        if constexpr (GENERAL) {
+          if (pt.cheb) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(ypv + lr));
+          stg_f64(yout + lr, t);
+          if (use_acc) stg_f64(acc + lr, madd<EXACT>(ld_cg(acc + lr), pt.cre, t));
+        } else {
+          stg_f64(yout + lr, t);
+        }
+      }
+    };
+    auto single = [&](int32_t s, int2 rec) -> double {
+      const CSlice a = cslice<VD>(col_o, val_o, uint32_t(rec.x));
+      const int w = rec.y & 0xffff;
+      const int32_t row = r0 + s * 32 + int32_t(lane);
+      if (int(uint32_t(rec.y) >> 16) == w) return cslice_real<EXACT, true, VD>(B, a, lane, row, dict, g, w, w);
+      return cslice_real<EXACT, false, VD>(B, a, lane, row, dict, g, w, len_of(s, rec));
+    };
+    for (int32_t s = wid; s < ns; s += 2 * nwarps) {
+      const int32_t s2 = s + nwarps;
+      const int2 rec0 = B.i2(uint32_t(s) * 8);
+      if (s2 >= ns) {
+        epilogue(s, single(s, rec0));
+        break;
+      }
+      const int2 rec1 = B.i2(uint32_t(s2) * 8);
+      const int w0 = rec0.y & 0xffff, w1 = rec1.y & 0xffff;
+      if (w0 == w1 && w0 >= 1 && w0 <= 8) {
+        const bool full0 = int(uint32_t(rec0.y) >> 16) == w0, full1 = int(uint32_t(rec1.y) >> 16) == w1;
+        const CSlice a0 = cslice<VD>(col_o, val_o, uint32_t(rec0.x)), a1 = cslice<VD>(col_o, val_o, uint32_t(rec1.x));
+        const int32_t row0 = r0 + s * 32 + int32_t(lane), row1 = r0 + s2 * 32 + int32_t(lane);
+        double2 t;
+        if (full0 && full1)
+          t = cslice_real_pair<EXACT, true, VD>(B, a0, a1, lane, row0, row1, dict, g, w0, w0, w0);
+        else
+          t = cslice_real_pair<EXACT, false, VD>(B, a0, a1, lane, row0, row1, dict, g, w0, len_of(s, rec0),
+                                                 len_of(s2, rec1));
+        epilogue(s, t.x);
+        epilogue(s2, t.y);
+      } else {
+        epilogue(s, single(s, rec0));
+        epilogue(s2, single(s2, rec1));
+      }
+    }
+  } else {
+    for (int32_t s = wid; s < ns; s += nwarps) {
+      const int2 rec = B.i2(uint32_t(s) * 8);
+      const CSlice a = cslice<VD>(col_o, val_o, uint32_t(rec.x));
+      const int w = rec.y & 0xffff;
+      const int32_t lr = s * 32 + int32_t(lane);
+      double2 t = cslice_any<true, EXACT, VD>(B, a, lane, r0 + lr, dict, g, w, len_of(s, rec));
+      if (lr < nrows) {
+        const int64_t r2 = 2 * int64_t(lr);
+        if constexpr (GENERAL) {
+          if (pt.cheb) {
+            t.x = __dsub_rn(__dmul_rn(2.0, t.x), ld_cg(ypv + r2));
+            t.y = __dsub_rn(__dmul_rn(2.0, t.y), ld_cg(ypv + r2 + 1));
+          }
+        }
+        stg_f64x2(yout + r2, t);
+        if constexpr (GENERAL) {
+          if (use_acc) {
+            const double ar = ld_cg(acc + r2), ai = ld_cg(acc + r2 + 1);
+            const double pr = __dsub_rn(__dmul_rn(pt.cre, t.x), __dmul_rn(pt.cim, t.y));
+            const double pim = __dadd_rn(__dmul_rn(pt.cre, t.y), __dmul_rn(pt.cim, t.x));
+            stg_f64x2(acc + r2, make_double2(__dadd_rn(ar, pr), __dadd_rn(ai, pim)));
+          }
+        }
+      }
+    }
+  }
+}
+
 // One power step of one tile (rows r0 .. r0+nrows-1, E block entries): warps
 // stride over the 32-row slices, lane = row.  GENERAL adds the Chebyshev
 // three-term step and the accumulation; plain SpMV powers skip both.
@@ -680,7 +986,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
   __shared__ uint32_t w_done[kWorkRing];
   __shared__ uint32_t ring_ctr, prod_done, trace_ctr;
   __shared__ int32_t h_t[kMaxSlots], h_last[kMaxSlots], h_glb[kMaxSlots];
-  __shared__ int32_t h_r0[kMaxSlots], h_rows[kMaxSlots], h_E[kMaxSlots], h_nseg[kMaxSlots];
+  __shared__ int32_t h_r0[kMaxSlots], h_rows[kMaxSlots], h_E[kMaxSlots], h_nseg[kMaxSlots], h_mode[kMaxSlots];
   __shared__ int64_t h_ofs[kMaxSlots];
   __shared__ PowTab s_pow[LMPK_MAX_POWERS];
   const int R = P.n_slots;
@@ -719,7 +1025,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
     unsigned long long p_rounds = 0, p_items = 0, p_tma = 0, p_dep = 0, p_free = 0, p_x = 0;
     const unsigned long long p_t0 = P.prof ? globaltimer() : 0;
     struct Next {
-      int32_t t, first, last, r0, rows, E, lo, hi, nseg, xent;
+      int32_t t, first, last, r0, rows, E, lo, hi, nseg, xent, mode;
       int64_t ofs, bytes;
       bool valid;
     } nx;
@@ -824,6 +1130,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
           nx.lo = nx.hi = t;
           nx.nseg = P.xmode ? __ldg(P.tile_nseg + t) : 0;
           nx.xent = nx.nseg ? __ldg(P.tile_xent + t) : 0;
+          nx.mode = P.tile_mode ? __ldg(P.tile_mode + t) : 0;
           nx.valid = true;
           return;
         }
@@ -853,6 +1160,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         nx.hi = __ldg(P.dep_hi + t);
         nx.nseg = P.xmode ? __ldg(P.tile_nseg + t) : 0;
         nx.xent = nx.nseg ? __ldg(P.tile_xent + t) : 0;
+        nx.mode = P.tile_mode ? __ldg(P.tile_mode + t) : 0;
         nx.valid = true;
         return;
       }
@@ -910,6 +1218,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         h_rows[r] = cur.rows;
         h_E[r] = cur.E;
         h_nseg[r] = glb ? 0 : cur.nseg;
+        h_mode[r] = glb ? 0 : cur.mode;
         if (!glb) {
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&tile_bar[r], uint32_t(cur.bytes));
@@ -1001,7 +1310,7 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
     unsigned long long n_it = 0;
     for (int k = 0;; ++k) {
       const int ws = k % kWorkRing;
-      mbar_wait(&full_bar[ws], uint32_t(k / kWorkRing) & 1);
+      mbar_wait_sleep(&full_bar[ws], uint32_t(k / kWorkRing) & 1);
       const int r = w_slot[ws];
       if (r < 0) break;
       const int p = w_p[ws];
@@ -1012,13 +1321,28 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
       const PowTab& pt = s_pow[p - 1];
       const bool use_acc = P.use_acc != 0;
       const int32_t nseg = h_nseg[r];
+      const int32_t tmode = h_mode[r];
       // separate inlined copies so each sees a known address space (LDS vs
       // LDG); plain SpMV powers take the epilogue without Chebyshev/acc
       if (!h_glb[r]) {
         const uint32_t sb = smem_u32(smem_raw) + uint32_t(r) * uint32_t(P.smem_cap);
         const SmemBlk B{sb};
         const bool pairs = (P.flags & 0x800) == 0;  // internal A/B switch
-        if (nseg > 0) {
+        if (tmode != 0) {
+          const GatherGlobal G{pt.yin};
+          const int32_t nd = tmode >> 8;
+          if (tmode & kModeDict) {
+            if (pt.general)
+              tile_power_c<CPLX, EXACT, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, warp, NC);
+            else
+              tile_power_c<CPLX, EXACT, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, warp, NC);
+          } else {
+            if (pt.general)
+              tile_power_c<CPLX, EXACT, true, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, warp, NC);
+            else
+              tile_power_c<CPLX, EXACT, false, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, warp, NC);
+          }
+        } else if (nseg > 0) {
           const uint32_t xb = sb + uint32_t(P.xoff);
           if (P.xmode == 2) {
             // vectors not 16-byte aligned: all consumer warps copy the
@@ -1101,20 +1425,89 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
 }
 
 // ---------------------------------------------------------------- tiling kernels
-// per slice: longest row (width) and shortest row (padding-free prefix)
-__global__ void k_slice_width(const int32_t* row_ptr, int32_t n, int32_t n_slices, int32_t* width,
-                              int32_t* wmin) {
+// per slice: longest row (width), shortest row (padding-free prefix) and,
+// when fit16 != NULL, whether every entry's column offset col - row fits int16
+__global__ void k_slice_width(const int32_t* row_ptr, const int32_t* col, int32_t n, int32_t n_slices,
+                              int32_t* width, int32_t* wmin, uint8_t* fit16) {
   const int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
   const int32_t r = s * 32 + lane;
-  const int len = r < n ? __ldg(row_ptr + r + 1) - __ldg(row_ptr + r) : 0;
+  const int32_t a = r < n ? __ldg(row_ptr + r) : 0;
+  const int len = r < n ? __ldg(row_ptr + r + 1) - a : 0;
   const int w = __reduce_max_sync(0xffffffffu, len);
   const int m = __reduce_min_sync(0xffffffffu, len);
+  if (fit16) {
+    bool ok = true;
+    for (int j = 0; j < len; ++j) {
+      const int32_t d = __ldg(col + a + j) - r;
+      ok = ok && d >= -32768 && d <= 32767;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (lane == 0) fit16[s] = ok ? 1 : 0;
+  }
   if (lane == 0) {
     width[s] = w;
     wmin[s] = m;
   }
+}
+
+// Per-tile value dictionary (one CTA per listed tile): the distinct bit
+// patterns of the tile's CRS values, sorted ascending, or nd = -1 if there
+// are more than kDictMax.  Open-addressing hash set in shared memory.
+constexpr int kDictHash = 1024;
+__global__ void __launch_bounds__(256) k_tile_dict(const int32_t* row_ptr, const double* val, const int32_t* tile_row,
+                                                   const int32_t* list, int32_t n_list, uint64_t* dict_out,
+                                                   int32_t* nd_out) {
+  __shared__ unsigned long long keys[kDictHash];
+  __shared__ uint32_t state[kDictHash];
+  __shared__ unsigned long long packed[kDictMax];
+  __shared__ uint32_t count, overflow, npk;
+  const int32_t li = blockIdx.x;
+  if (li >= n_list) return;
+  const int32_t t = list[li];
+  for (int i = threadIdx.x; i < kDictHash; i += blockDim.x) state[i] = 0;
+  if (threadIdx.x == 0) count = overflow = npk = 0;
+  __syncthreads();
+  const int32_t e0 = row_ptr[tile_row[t]], e1 = row_ptr[tile_row[t + 1]];
+  volatile uint32_t* vs = state;
+  volatile unsigned long long* vk = keys;
+  for (int32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    if (*(volatile uint32_t*)&overflow) break;
+    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(__ldg(val + e)));
+    uint32_t h = uint32_t((bits * 0x9E3779B97F4A7C15ull) >> 54);
+    for (;;) {
+      const uint32_t st = vs[h];
+      if (st == 2) {
+        if (vk[h] == bits) break;
+        h = (h + 1) & (kDictHash - 1);
+      } else if (st == 0) {
+        if (atomicCAS(&state[h], 0u, 1u) == 0u) {
+          vk[h] = bits;
+          __threadfence_block();
+          atomicExch(&state[h], 2u);
+          if (atomicAdd(&count, 1u) >= uint32_t(kDictMax)) atomicExch(&overflow, 1u);
+          break;
+        }
+      }  // st == 1: another thread is writing this key, re-read
+    }
+  }
+  __syncthreads();
+  if (overflow) {
+    if (threadIdx.x == 0) nd_out[li] = -1;
+    return;
+  }
+  for (int i = threadIdx.x; i < kDictHash; i += blockDim.x)
+    if (state[i] == 2) packed[atomicAdd(&npk, 1u)] = keys[i];
+  __syncthreads();
+  const uint32_t nd = npk;
+  for (uint32_t j = threadIdx.x; j < nd; j += blockDim.x) {
+    const unsigned long long k = packed[j];
+    uint32_t rank = 0;
+    for (uint32_t i = 0; i < nd; ++i) rank += packed[i] < k;
+    dict_out[int64_t(li) * kDictMax + rank] = k;
+  }
+  if (threadIdx.x == 0) nd_out[li] = int32_t(nd);
 }
 
 // one warp per slice: slice record, row lengths and the chunked entries.
@@ -1124,7 +1517,8 @@ __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const 
                               int32_t n_slices, const int32_t* slice_tile, const int32_t* slice_off,
                               const int32_t* width, const int32_t* wmin, const int32_t* tile_row,
                               const int64_t* tile_ofs, const int32_t* tile_E, const int32_t* seg_ptr,
-                              const int4* segs, unsigned char* blocks) {
+                              const int4* segs, const int32_t* tile_mode, const int32_t* tile_dict,
+                              const uint64_t* dict_tab, unsigned char* blocks) {
   const int32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= n_slices) return;
@@ -1132,6 +1526,59 @@ __global__ void k_fill_blocks(const int32_t* row_ptr, const int32_t* col, const 
   const int32_t r0 = tile_row[t], r1 = tile_row[t + 1];
   const int32_t ns = (r1 - r0 + 31) >> 5;
   const int32_t ls = s - (r0 >> 5);
+  const int32_t mode = tile_mode ? tile_mode[t] : 0;
+  if (mode != 0) {
+    // compressed block (see cblk_*): int16 column offsets, dictionary codes or raw values
+    const int32_t nd = mode >> 8;
+    const bool vd = (mode & kModeDict) != 0;
+    unsigned char* blk = blocks + tile_ofs[t];
+    const int32_t E = tile_E[t];
+    const uint64_t* dict = vd ? dict_tab + int64_t(tile_dict[t]) * kDictMax : nullptr;
+    if (ls == 0 && vd)
+      for (int j = lane; j < nd; j += 32) reinterpret_cast<uint64_t*>(blk + cblk_dict_off(ns))[j] = dict[j];
+    int16_t* c16 = reinterpret_cast<int16_t*>(blk + cblk_col_off(ns, nd));
+    unsigned char* vbase = blk + cblk_val_off(ns, nd, E);
+    const int32_t base = slice_off[s];
+    const int32_t r = s * 32 + lane;
+    const bool valid = r < r1;
+    const int32_t a = valid ? row_ptr[r] : 0;
+    const int len = valid ? row_ptr[r + 1] - a : 0;
+    const int w = width[s];
+    if (lane == 0) reinterpret_cast<int2*>(blk)[ls] = make_int2(base, w | (wmin[s] << 16));
+    reinterpret_cast<uint16_t*>(blk + int64_t(ns) * 8)[ls * 32 + lane] = uint16_t(len);
+    // padding: the row's last column (own row if empty; r0 for lanes past the tile)
+    int32_t pad = valid ? 0 : r0 - r;
+    for (int j = 0; j < w; ++j) {
+      const int64_t e = chunk_entry(base, w, lane, j);
+      int32_t d = pad;
+      double v = 0.0;
+      if (j < len) {
+        d = col[a + j] - r;
+        v = val[a + j];
+        pad = d;
+      }
+      c16[e] = int16_t(d);
+      if (vd) {
+        uint8_t code = 0;
+        if (j < len) {
+          const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+          int lo = 0, hi = nd - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (dict[mid] < bits)
+              lo = mid + 1;
+            else
+              hi = mid;
+          }
+          code = uint8_t(lo);
+        }
+        vbase[e] = code;
+      } else {
+        reinterpret_cast<double*>(vbase)[e] = v;
+      }
+    }
+    return;
+  }
   const int32_t sg0 = seg_ptr ? seg_ptr[t] : 0;
   const int32_t nseg = seg_ptr ? seg_ptr[t + 1] - sg0 : 0;
   unsigned char* blk = blocks + tile_ofs[t];
@@ -1345,6 +1792,7 @@ extern "C" int lmpk_tiling_destroy(lmpk_tiling* t) {
   cudaFree(t->d_dep_hi);
   cudaFree(t->d_tile_nseg);
   cudaFree(t->d_tile_xent);
+  cudaFree(t->d_tile_mode);
   cudaFree(t->d_rdep_ptr);
   cudaFree(t->d_rdep);
   cudaFree(t->d_rcnt);
@@ -1419,15 +1867,124 @@ static void plan_segments(const std::vector<int32_t>& rp, const std::vector<int3
   seg_ptr[nt] = static_cast<int32_t>(segs.size());
 }
 
-// Tiles + chunked tile-SELL-32 blocks + dependency ranges for block cap `cap` bytes.
+// Greedy partition of slices [s0, s1) into tiles whose block cost(ns, E) fits
+// `cap` bytes and whose entries stay <= e_cap (a tile holds >= 1 slice).
+template <class Cost>
+static void partition_range(const std::vector<int32_t>& width, int32_t s0, int32_t s1, int64_t cap, int64_t e_cap,
+                            Cost cost, std::vector<int32_t>& first, std::vector<int64_t>& Es) {
+  int32_t s = s0;
+  while (s < s1) {
+    int32_t ns = 0;
+    int64_t E = 0;
+    while (s + ns < s1) {
+      const int64_t e2 = E + int64_t(width[s + ns]) * 32;
+      if (ns > 0 && (cost(ns + 1, e2) > cap || e2 > e_cap)) break;
+      E = e2;
+      ++ns;
+    }
+    first.push_back(s);
+    Es.push_back(E);
+    s += ns;
+  }
+}
+
+// Tiles + chunked tile-SELL-32 blocks + dependency ranges for block cap `cap`
+// bytes.  With fit16 (compressed tiling), runs of slices whose column offsets
+// fit int16 become compressed tiles: first partitioned for the dictionary
+// format (3 B/entry), then every tile with more than kDictMax distinct values
+// is re-partitioned for raw values (10 B/entry); the other slices stay plain.
 static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
                         const int32_t* col, const double* val, const std::vector<int32_t>& width,
                         const int32_t* d_wmin, int64_t cap, const std::vector<int32_t>* h_rp,
-                        const std::vector<int32_t>* h_col, int64_t xcap, cudaStream_t st) {
+                        const std::vector<int32_t>* h_col, int64_t xcap, const std::vector<uint8_t>* fit16,
+                        int64_t e_cap, cudaStream_t st) {
   const int32_t S = static_cast<int32_t>(width.size());
   std::vector<int32_t> first;
   std::vector<int64_t> Es;
-  partition_slices(width, cap, first, Es);
+  std::vector<int32_t> tmode;   // per tile: 0 plain, else kModeC16 [| kModeDict | nd << 8]
+  std::vector<int32_t> tdict;   // per tile: index into the dictionary table (dict tiles)
+  uint64_t* d_dict_tab = nullptr;
+  int32_t* d_tile_dict = nullptr;
+  auto plain_cost = [](int32_t ns, int64_t E) { return blk_bytes(ns, E, 0); };
+  if (fit16 && S > 0) {
+    auto dict_cost = [](int32_t ns, int64_t E) { return cblk_bytes(ns, kDictMax, E, true); };
+    auto raw_cost = [](int32_t ns, int64_t E) { return cblk_bytes(ns, 0, E, false); };
+    // pass 1: runs of equal fit16, compressed runs cut for the dictionary format
+    std::vector<int32_t> f1;
+    std::vector<int64_t> E1;
+    std::vector<uint8_t> c1;
+    for (int32_t s = 0; s < S;) {
+      int32_t e = s;
+      while (e < S && (*fit16)[e] == (*fit16)[s]) ++e;
+      const size_t before = f1.size();
+      if ((*fit16)[s])
+        partition_range(width, s, e, cap, e_cap, dict_cost, f1, E1);
+      else
+        partition_range(width, s, e, cap, INT64_MAX, plain_cost, f1, E1);
+      c1.resize(f1.size(), (*fit16)[s]);
+      (void)before;
+      s = e;
+    }
+    const int32_t n1 = static_cast<int32_t>(f1.size());
+    // dictionaries of the compressed pass-1 tiles (on the device)
+    std::vector<int32_t> row1(n1 + 1), list;
+    for (int32_t t = 0; t < n1; ++t) {
+      row1[t] = std::min(f1[t] * 32, n);
+      if (c1[t]) list.push_back(t);
+    }
+    row1[n1] = n;
+    const int32_t nl = static_cast<int32_t>(list.size());
+    std::vector<int32_t> nd(nl, -1);
+    if (nl > 0) {
+      int32_t *d_row1 = nullptr, *d_list = nullptr, *d_nd = nullptr;
+      LMPK_TRY(dmalloc(&d_row1, n1 + 1));
+      LMPK_TRY(dmalloc(&d_list, nl));
+      LMPK_TRY(dmalloc(&d_nd, nl));
+      LMPK_TRY(dmalloc(&d_dict_tab, size_t(nl) * kDictMax));
+      LMPK_CHECK_CUDA(cudaMemcpyAsync(d_row1, row1.data(), size_t(n1 + 1) * 4, cudaMemcpyHostToDevice, st));
+      LMPK_CHECK_CUDA(cudaMemcpyAsync(d_list, list.data(), size_t(nl) * 4, cudaMemcpyHostToDevice, st));
+      k_tile_dict<<<nl, 256, 0, st>>>(row_ptr, val, d_row1, d_list, nl, d_dict_tab, d_nd);
+      launch_count_add(ctx, 1);
+      LMPK_CHECK_CUDA(cudaGetLastError());
+      LMPK_CHECK_CUDA(cudaMemcpyAsync(nd.data(), d_nd, size_t(nl) * 4, cudaMemcpyDeviceToHost, st));
+      LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+      cudaFree(d_row1);
+      cudaFree(d_list);
+      cudaFree(d_nd);
+    }
+    // pass 2: final tiles
+    for (int32_t t = 0, li = 0; t < n1; ++t) {
+      const int32_t s0 = f1[t], s1 = t + 1 < n1 ? f1[t + 1] : S;
+      if (!c1[t]) {
+        first.push_back(s0);
+        Es.push_back(E1[t]);
+        tmode.push_back(0);
+        tdict.push_back(-1);
+        continue;
+      }
+      const int32_t k = nd[li];
+      if (k >= 0 && dict_cost(s1 - s0, E1[t]) <= cap) {
+        first.push_back(s0);
+        Es.push_back(E1[t]);
+        tmode.push_back(kModeC16 | kModeDict | (k << 8));
+        tdict.push_back(li);
+      } else {
+        const size_t b = first.size();
+        partition_range(width, s0, s1, cap, e_cap, raw_cost, first, Es);
+        for (size_t i = b; i < first.size(); ++i) {
+          const int32_t a0 = first[i], a1 = i + 1 < first.size() ? first[i + 1] : s1;
+          // a single slice too large for a slot stays plain (read from global)
+          tmode.push_back(raw_cost(a1 - a0, Es[i]) <= cap ? kModeC16 : 0);
+          tdict.push_back(-1);
+        }
+      }
+      ++li;
+    }
+  } else {
+    partition_slices(width, cap, first, Es);
+    tmode.assign(first.size(), 0);
+    tdict.assign(first.size(), -1);
+  }
   const int32_t nt = static_cast<int32_t>(first.size());
   std::vector<int32_t> tile_row(nt + 1), tile_E(nt), slice_tile(std::max(S, 1)), slice_off(std::max(S, 1));
   std::vector<int64_t> tile_ofs(nt + 1);
@@ -1441,18 +1998,22 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     std::vector<uint8_t> allow(nt);
     for (int32_t t = 0; t < nt; ++t) {
       const int32_t s1 = (t + 1 < nt) ? first[t + 1] : S;
-      allow[t] = blk_bytes(s1 - first[t], Es[t], 0) <= cap;
+      allow[t] = tmode[t] == 0 && blk_bytes(s1 - first[t], Es[t], 0) <= cap;
     }
     plan_segments(*h_rp, *h_col, tile_row, allow, n, xcap, seg_ptr, segs, xent);
   }
   int64_t ofs = 0;
   int64_t maxb = 0;
+  int32_t n_comp = 0, n_dict = 0;
   for (int32_t t = 0; t < nt; ++t) {
     const int32_t s0 = first[t], s1 = (t + 1 < nt) ? first[t + 1] : S;
     tile_E[t] = static_cast<int32_t>(Es[t]);
     tile_ofs[t] = ofs;
     const int32_t nseg = seg_ptr.empty() ? 0 : seg_ptr[t + 1] - seg_ptr[t];
-    const int64_t b = blk_bytes(s1 - s0, Es[t], nseg);
+    const int64_t b = tmode[t] ? cblk_bytes(s1 - s0, tmode[t] >> 8, Es[t], (tmode[t] & kModeDict) != 0)
+                               : blk_bytes(s1 - s0, Es[t], nseg);
+    n_comp += tmode[t] != 0;
+    n_dict += (tmode[t] & kModeDict) != 0;
     maxb = std::max(maxb, b);
     ofs += b;
     int32_t e = 0;
@@ -1463,6 +2024,14 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     }
   }
   tile_ofs[nt] = ofs;
+  T->info.compressed_tiles = n_comp;
+  T->info.dict_tiles = n_dict;
+  if (n_comp > 0) {
+    LMPK_TRY(dmalloc(&T->d_tile_mode, nt));
+    LMPK_TRY(dmalloc(&d_tile_dict, nt));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_mode, tmode.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(d_tile_dict, tdict.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
+  }
   T->h_tile_row = tile_row;
   T->block_bytes = ofs;
   T->max_block = static_cast<int32_t>(std::min<int64_t>(maxb, INT32_MAX));
@@ -1513,7 +2082,8 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   if (S > 0) {
     k_fill_blocks<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_slice_tile, d_slice_off,
                                                                  d_width, d_wmin, T->d_tile_row, T->d_tile_ofs,
-                                                                 T->d_tile_E, d_seg_ptr, d_segs, T->d_blocks);
+                                                                 T->d_tile_E, d_seg_ptr, d_segs, T->d_tile_mode,
+                                                                 d_tile_dict, d_dict_tab, T->d_blocks);
     launch_count_add(ctx, 1);
   }
   k_tile_deps<<<div_up(int64_t(nt) * 32, 256), 256, 0, st>>>(row_ptr, col, T->d_tile_row, nt, T->d_dep_lo,
@@ -1530,6 +2100,8 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   cudaFree(d_width);
   cudaFree(d_seg_ptr);
   cudaFree(d_segs);
+  cudaFree(d_tile_dict);
+  cudaFree(d_dict_tab);
   T->info.n_tiles = nt;
   T->info.block_bytes = ofs;
   return LMPK_OK;
@@ -1554,19 +2126,34 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   std::vector<int32_t> width(S);
   int32_t* d_w = nullptr;
   int32_t* d_wmin = nullptr;
+  uint8_t* d_fit = nullptr;
   LMPK_TRY(dmalloc(&d_w, std::max(S, 1)));
   LMPK_TRY(dmalloc(&d_wmin, std::max(S, 1)));
+  LMPK_TRY(dmalloc(&d_fit, std::max(S, 1)));
   struct Guard {
     int32_t *a, *b;
+    uint8_t* c;
     ~Guard() {
       cudaFree(a);
       cudaFree(b);
+      cudaFree(c);
     }
-  } guard{d_w, d_wmin};
+  } guard{d_w, d_wmin, d_fit};
+  // compressed blocks (int16 column offsets + value dictionary): opt-in via
+  // LMPK_FLAG_COMPRESS or LMPK_COMPRESS=1; not with unstaged blocks or x staging
+  bool compress = (prm.mode_flags & LMPK_FLAG_COMPRESS) != 0;
+  if (const char* e = getenv("LMPK_COMPRESS")) compress = atoi(e) != 0;
+  if (prm.mode_flags & LMPK_FLAG_NO_TMA) compress = false;
+  std::vector<uint8_t> fit16;
   if (S > 0) {
-    k_slice_width<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, n, S, d_w, d_wmin);
+    k_slice_width<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, n, S, d_w, d_wmin,
+                                                               compress ? d_fit : nullptr);
     launch_count_add(ctx, 1);
     LMPK_CHECK_CUDA(cudaMemcpyAsync(width.data(), d_w, size_t(S) * 4, cudaMemcpyDeviceToHost, st));
+    if (compress) {
+      fit16.resize(S);
+      LMPK_CHECK_CUDA(cudaMemcpyAsync(fit16.data(), d_fit, size_t(S), cudaMemcpyDeviceToHost, st));
+    }
   }
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   int32_t max_row = 0;
@@ -1613,7 +2200,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   // off: measured slower on cfg2 -- 1.36 vs 0.99 ms at 25%)
   int xfrac = 0;
   if (const char* e = getenv("LMPK_XFRAC")) xfrac = std::max(0, std::min(60, atoi(e)));
-  const bool xstage = !unstaged && !(prm.mode_flags & LMPK_FLAG_COMPLEX) && xfrac > 0 && n > 0;
+  const bool xstage = !compress && !unstaged && !(prm.mode_flags & LMPK_FLAG_COMPLEX) && xfrac > 0 && n > 0;
   std::vector<int32_t> h_rp, h_col;
   if (xstage) {
     h_rp.resize(size_t(n) + 1);
@@ -1623,11 +2210,16 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
       LMPK_CHECK_CUDA(cudaMemcpyAsync(h_col.data(), col, size_t(h_nnz) * 4, cudaMemcpyDeviceToHost, st));
     LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   }
+  // LMPK_SLOT_KB caps a slot (experiments: smaller slots leave the rest of
+  // the SM's unified L1/shared memory to the gathers)
+  int64_t slot_cap = INT64_MAX;
+  if (const char* e = getenv("LMPK_SLOT_KB")) slot_cap = std::max(4, atoi(e)) * int64_t(1024);
   for (const Cand& cd : cands) {
-    const int64_t slot = (unstaged ? per_cta / 2 : per_cta / cd.slots) & ~int64_t(127);
+    const int64_t slot = std::min<int64_t>(unstaged ? per_cta / 2 : per_cta / cd.slots, slot_cap) & ~int64_t(127);
     int64_t xbytes = xstage ? (slot * xfrac / 100) & ~int64_t(127) : 0;
     int64_t cap = slot - xbytes - (xstage ? kMaxSegs * 16 : 0);
-    if (prm.tile_nnz_hint > 0) cap = std::min<int64_t>(cap, int64_t(prm.tile_nnz_hint) * 12 + 2048);
+    if (prm.tile_nnz_hint > 0 && !compress) cap = std::min<int64_t>(cap, int64_t(prm.tile_nnz_hint) * 12 + 2048);
+    const int64_t e_cap = (compress && prm.tile_nnz_hint > 0) ? int64_t(prm.tile_nnz_hint) : INT64_MAX;
     cap &= ~int64_t(127);
     if (cap < 2048) continue;
     const int64_t xoff = xstage ? cap + kMaxSegs * 16 : 0;
@@ -1639,7 +2231,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     cand->ctx = ctx;
     cand->n = n;
     const int rc = build_tiling(ctx, cand, n, row_ptr, col, val, width, d_wmin, cap, xstage ? &h_rp : nullptr,
-                                xstage ? &h_col : nullptr, xbytes / 8, st);
+                                xstage ? &h_col : nullptr, xbytes / 8, compress ? &fit16 : nullptr, e_cap, st);
     if (rc != LMPK_OK) {
       lmpk_tiling_destroy(cand);
       return rc;
@@ -1753,6 +2345,25 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
   void* args[] = {&Pm, &C};
   const void* fn = group_fn(cplx, exact);
   const int block = 32 * (kConsumers + Pm.n_slots);
+  // shared-memory carveout: just what the slots need, so the rest of the
+  // unified L1 serves the gathers (the driver rounds up to a supported split)
+  {
+    static int last[4] = {-1, -1, -1, -1};
+    const int idx = (cplx ? 2 : 0) + (exact ? 1 : 0);
+    int stat = 0;
+    LMPK_TRY(group_static_smem(&stat));
+    const int per_sm = std::max(1, ctx->max_smem_sm);
+    const int pct = std::min(100, int((int64_t(smem + stat + 1024) * 100 + per_sm - 1) / per_sm));
+    if (last[idx] != pct) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        set_error("carveout: %s", cudaGetErrorString(e));
+        return LMPK_ERR_CUDA;
+      }
+      last[idx] = pct;
+    }
+  }
   cudaError_t e = coop ? cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, st)
                        : cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, st);
   if (e != cudaSuccess) {
@@ -1819,6 +2430,9 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   Pm.blk_cap = T->xoff > 0 ? Pm.xoff : Pm.smem_cap;
   Pm.tile_nseg = T->d_tile_nseg;
   Pm.tile_xent = T->d_tile_xent;
+  Pm.tile_mode = T->d_tile_mode;
+  LMPK_ARG_CHECK(!T->d_tile_mode || !(flags & LMPK_FLAG_NO_TMA),
+                 "LMPK_FLAG_NO_TMA cannot read a compressed tiling (build it without LMPK_FLAG_COMPRESS)");
   if (T->staged_tiles > 0) {
     LMPK_ARG_CHECK(!cplx, "this tiling stages real x-segments; build it with LMPK_FLAG_COMPLEX in "
                           "mode_flags for complex vectors");

@@ -1,0 +1,149 @@
+"""GPU parity of the compressed tile blocks (LMPK_FLAG_COMPRESS: int16 column
+offsets, per-tile value dictionary): the MPK, the sweep and the complex
+Chebyshev path must give the same bits as the oracle's sequential CRS sums
+(executor.py:121-135) on matrices that exercise every block format -- all
+dictionary tiles, raw-value tiles, plain tiles for slices whose column offsets
+do not fit int16, and tilings that mix the three."""
+
+import numpy as np
+import pytest
+
+import paper_2205_01598_b200 as lm
+from oracle import levelmpk_oracle as O
+from paper_2205_01598_b200 import _lib
+from paper_2205_01598_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    lm.warmup()
+
+
+def _level_ordered(a):
+    _, perm = lm.bfs_levels(a, 0)
+    return lm.permute_symmetric(a, perm)
+
+
+def _band_mixed(n=50_000, seed=5):
+    """Band matrix (offsets +-1, +-37) with a few long-range couplings
+    (|col - row| > 32767 in some slices) and small-set values in the first
+    half, distinct random values in the second half."""
+    rng = np.random.default_rng(seed)
+    i = np.arange(n)
+    rows, cols = [i], [i]
+    for d in (1, 37):
+        rows += [i[:-d], i[d:]]
+        cols += [i[d:], i[:-d]]
+    far = np.arange(0, n - 40_000, 997)
+    rows += [far, far + 40_000]
+    cols += [far + 40_000, far]
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    v = np.where(r < n // 2, rng.choice([-1.0, 0.5, 2.25, 6.0], r.size), rng.standard_normal(r.size))
+    return lm.CsrMatrix.from_triplets(n, r, c, v)
+
+
+def _with_empty_rows(n=3001):
+    """2D stencil rows interleaved with empty rows; n not a multiple of 32."""
+    a = lm.gen_stencil_2d7pt(40, 40)
+    r, c, v = a.to_triplets()
+    return lm.CsrMatrix.from_triplets(n, r, c, v)
+
+
+MATRICES = {
+    "3d-24-o2": lambda: _level_ordered(lm.gen_stencil_3d(24, 2)),
+    "3d-16-o4": lambda: _level_ordered(lm.gen_stencil_3d(16, 4)),
+    "27pt-perturbed-20": lambda: _level_ordered(lm.gen_stencil_3d27pt(20)),
+    "anderson-12": lambda: _level_ordered(lm.gen_anderson_3d(12)),
+    "rmat-s12": lambda: _level_ordered(lm.gen_rmat(12)),
+    "band-mixed": _band_mixed,
+    "empty-rows": _with_empty_rows,
+}
+
+
+def _run(ap, k, mode, slots, tile, x, sweep=False):
+    import torch
+
+    fl = (_lib.FLAG_MODE_RESIDENT if mode == "res" else _lib.FLAG_MODE_STREAM) | _lib.FLAG_COMPRESS
+    t = K.Tiling(ap.device(), k, tile_nnz=tile, slots=slots, mode_flags=fl)
+    y = torch.zeros((k + 1, ap.n_rows), dtype=torch.float64, device="cuda")
+    y[0] = torch.from_numpy(x)
+    K.mpk_run(t, y, K.mpk_power_cfg(k), flags=_lib.FLAG_SWEEP if sweep else 0, exact=True)
+    return t, y.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", list(MATRICES))
+@pytest.mark.parametrize("mode,slots,tile", [("stream", 2, 0), ("stream", 4, 600), ("res", 3, 900)])
+def test_compressed_mpk_bitwise(name, mode, slots, tile):
+    ap = MATRICES[name]()
+    k = 6
+    x = np.random.default_rng(17).uniform(-1, 1, ap.n_rows)
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, x, k)
+    try:
+        t, y = _run(ap, k, mode, slots, tile, x)
+    except RuntimeError as e:  # the resident walk needs its window of tiles co-resident
+        assert mode == "res" and "no feasible tiling" in str(e)
+        pytest.skip("resident walk infeasible for this tiling")
+    assert t.info["compressed_tiles"] > 0 or name == "rmat-s12"
+    assert np.array_equal(y, ref)
+
+
+@pytest.mark.parametrize("name", ["3d-24-o2", "band-mixed"])
+def test_compressed_sweep_bitwise(name):
+    ap = MATRICES[name]()
+    k = 4
+    x = np.random.default_rng(3).uniform(-1, 1, ap.n_rows)
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, x, k)
+    _, y = _run(ap, k, "stream", 2, 500, x, sweep=True)
+    assert np.array_equal(y, ref)
+
+
+def test_block_formats_present():
+    """band-mixed must produce all three formats: dictionary tiles (first
+    half), raw-value tiles (second half) and plain tiles (far couplings)."""
+    ap = _band_mixed()
+    t = K.Tiling(ap.device(), 4, tile_nnz=2000, slots=2, mode_flags=_lib.FLAG_MODE_STREAM | _lib.FLAG_COMPRESS)
+    info = t.info
+    assert 0 < info["dict_tiles"] < info["compressed_tiles"] < info["n_tiles"]
+    plain = K.Tiling(ap.device(), 4, tile_nnz=2000, slots=2, mode_flags=_lib.FLAG_MODE_STREAM)
+    assert plain.info["compressed_tiles"] == 0
+    assert info["block_bytes"] < plain.info["block_bytes"]
+
+
+def test_stencil_dictionary_bytes():
+    """A level-ordered 7-point stencil compresses to ~3 bytes per entry."""
+    ap = MATRICES["3d-24-o2"]()
+    t = K.Tiling(ap.device(), 8, slots=2, mode_flags=_lib.FLAG_MODE_STREAM | _lib.FLAG_COMPRESS)
+    assert t.info["dict_tiles"] == t.info["n_tiles"]
+    assert t.info["block_bytes"] < 4.0 * ap.n_nz
+
+
+def test_compressed_complex_cheb_bitwise():
+    """Complex state through the compressed blocks, Chebyshev kernel + acc."""
+    import torch
+
+    ap = MATRICES["anderson-12"]()
+    n, k = ap.n_rows, 5
+    rng = np.random.default_rng(9)
+    x = (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+    cre = rng.standard_normal(k)
+    cim = rng.standard_normal(k)
+    outs = []
+    for fl in (_lib.FLAG_COMPRESS, 0):
+        t = K.Tiling(ap.device(), k, tile_nnz=700, slots=2,
+                     mode_flags=_lib.FLAG_MODE_STREAM | _lib.FLAG_COMPLEX | fl)
+        y = torch.zeros((k + 2, 2 * n), dtype=torch.float64, device="cuda")
+        y[0] = torch.from_numpy(x.view(np.float64).copy())
+        y[1] = torch.from_numpy((0.5 * x).view(np.float64).copy())
+        acc = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        p = np.arange(1, k + 1)
+        cfg = K.power_cfg(k, p + 1, p, p - 1, np.full(k, _lib.KERNEL_CHEB), cre, cim)
+        K.mpk_run(t, y, cfg, acc=acc, use_acc=True, complex_state=True, exact=True)
+        outs.append((y.cpu().numpy(), acc.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
