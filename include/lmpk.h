@@ -67,6 +67,10 @@ extern "C" {
                                     /* same tiles -- the blocking-free baseline */
 #define LMPK_FLAG_EXACT 0x400       /* bit-exact row sums (see Summation below) */
 #define LMPK_FLAG_READY_QUEUE 0x1000 /* q = 1: dependency-driven ready-queue walk */
+#define LMPK_FLAG_RING 0x4000       /* tiling: ring walk (small tiles streamed   */
+                                    /* through a ring of smem pieces; items are */
+                                    /* runs of tiles, tile_nnz_hint = run nnz,  */
+                                    /* slots = ring depth <= 16)                */
 #define LMPK_FLAG_COMPRESS 0x2000   /* tiling: compressed tile blocks (int16     */
                                     /* column offsets, per-tile dictionary of   */
                                     /* <= 256 values), bitwise-identical sums   */
@@ -141,6 +145,8 @@ typedef struct lmpk_tiling_info {
   int32_t compressed_tiles; /* tiles in the compressed block format (int16      */
                             /* column offsets; LMPK_FLAG_COMPRESS)              */
   int32_t dict_tiles;    /* compressed tiles with a value dictionary (<= 256)   */
+  int32_t super_tiles;   /* ring walk (mode 3): work items per power = runs of  */
+                         /* consecutive tiles streamed through the smem ring   */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */

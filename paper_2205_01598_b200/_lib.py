@@ -34,6 +34,7 @@ FLAG_SWEEP = 0x80
 FLAG_EXACT = 0x400
 FLAG_READY_QUEUE = 0x1000
 FLAG_COMPRESS = 0x2000
+FLAG_RING = 0x4000
 
 MAX_POWERS = 64
 
@@ -52,7 +53,7 @@ class TilingInfo(ctypes.Structure):
         ("max_fwd_reach", _i32), ("chain_reach", _i32), ("max_row_nnz", _i32),
         ("queue_slack", _i32), ("nnz", _i64), ("block_bytes", _i64),
         ("powers_per_item", _i32), ("slots", _i32), ("x_staged_tiles", _i32),
-        ("compressed_tiles", _i32), ("dict_tiles", _i32),
+        ("compressed_tiles", _i32), ("dict_tiles", _i32), ("super_tiles", _i32),
     ]
 
     def as_dict(self):

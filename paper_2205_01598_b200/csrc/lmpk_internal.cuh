@@ -92,6 +92,11 @@ struct lmpk_tiling {
   int32_t* d_tile_nseg = nullptr;  // [n_tiles] x-segments (0: global columns)
   int32_t* d_tile_xent = nullptr;  // [n_tiles] x-buffer entries
   int32_t* d_tile_mode = nullptr;  // [n_tiles] compressed block format (NULL: all plain)
+  bool ring = false;               // ring walk (mpk_ring_kernel): items are super-tiles
+  int32_t piece = 0;               // ring: bytes of one smem piece (= tile cap)
+  int32_t* d_st_first = nullptr;   // ring: [n_super+1] first tile of each super-tile
+  int32_t* d_st_lo = nullptr;      // ring: [n_super] dependency range (tiles)
+  int32_t* d_st_hi = nullptr;
   int32_t staged_tiles = 0, max_xent = 0;
   int64_t xoff = 0;                // byte offset of the x buffer in a slot (0: no staging)
   int32_t* d_rdep_ptr = nullptr;   // [n_tiles+1] reverse dependencies (ready-queue walk)
@@ -202,6 +207,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
+}
+// L2 prefetch of a global range (bytes a multiple of 16, 16-byte aligned).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
 }
 // Same with a 32-bit shared-memory destination address.
 __device__ __forceinline__ void bulk_g2s_a(uint32_t dst_smem, const void* src_gmem, uint32_t bytes,

@@ -1,0 +1,7 @@
+// mpk_k_ce.cu -- one instantiation of the group walk kernel (complex=true, exact=true).
+#include "mpk_kernel.cuh"
+
+namespace lmpk {
+const void* mpk_ring_fn_ce() { return reinterpret_cast<const void*>(mpk_ring_kernel<true, true, kConsumers>); }
+const void* mpk_group_fn_ce() { return reinterpret_cast<const void*>(mpk_group_kernel<true, true, kConsumers>); }
+}  // namespace lmpk

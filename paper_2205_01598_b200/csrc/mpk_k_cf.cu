@@ -1,0 +1,7 @@
+// mpk_k_cf.cu -- one instantiation of the group walk kernel (complex=true, exact=false).
+#include "mpk_kernel.cuh"
+
+namespace lmpk {
+const void* mpk_ring_fn_cf() { return reinterpret_cast<const void*>(mpk_ring_kernel<true, false, kConsumers>); }
+const void* mpk_group_fn_cf() { return reinterpret_cast<const void*>(mpk_group_kernel<true, false, kConsumers>); }
+}  // namespace lmpk

@@ -1,0 +1,7 @@
+// mpk_k_re.cu -- one instantiation of the group walk kernel (complex=false, exact=true).
+#include "mpk_kernel.cuh"
+
+namespace lmpk {
+const void* mpk_ring_fn_re() { return reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kConsumers>); }
+const void* mpk_group_fn_re() { return reinterpret_cast<const void*>(mpk_group_kernel<false, true, kConsumers>); }
+}  // namespace lmpk

@@ -1,0 +1,7 @@
+// mpk_k_rf.cu -- one instantiation of the group walk kernel (complex=false, exact=false).
+#include "mpk_kernel.cuh"
+
+namespace lmpk {
+const void* mpk_ring_fn_rf() { return reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kConsumers>); }
+const void* mpk_group_fn_rf() { return reinterpret_cast<const void*>(mpk_group_kernel<false, false, kConsumers>); }
+}  // namespace lmpk

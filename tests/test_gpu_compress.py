@@ -147,3 +147,75 @@ def test_compressed_complex_cheb_bitwise():
         outs.append((y.cpu().numpy(), acc.cpu().numpy()))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("name", ["3d-24-o2", "27pt-perturbed-20", "band-mixed"])
+@pytest.mark.parametrize("misaligned", [False, True])
+def test_compressed_x_staged_bitwise(name, misaligned, monkeypatch):
+    """Compressed blocks whose gathers come from the staged x-segments (local
+    int16 columns, LMPK_XFRAC); a slot stride that is not 16-byte aligned
+    takes the cooperative-copy path."""
+    import torch
+
+    monkeypatch.setenv("LMPK_XFRAC", "50")
+    ap = MATRICES[name]()
+    n, k = ap.n_rows, 6
+    x = np.random.default_rng(23).uniform(-1, 1, n)
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, x, k)
+    t = K.Tiling(ap.device(), k, tile_nnz=1500, slots=2, mode_flags=_lib.FLAG_MODE_STREAM | _lib.FLAG_COMPRESS)
+    assert t.info["x_staged_tiles"] > 0 and t.info["compressed_tiles"] > 0
+    ld = n + (1 if misaligned and n % 2 == 0 else 0)
+    buf = torch.zeros((k + 1) * ld + 1, dtype=torch.float64, device="cuda")
+    y = buf[1:1 + (k + 1) * ld].view(k + 1, ld)[:, :n] if misaligned else buf[:(k + 1) * ld].view(k + 1, ld)
+    y[0] = torch.from_numpy(x)
+    for _ in range(2):
+        K.mpk_run(t, y, K.mpk_power_cfg(k), exact=True)
+        assert np.array_equal(y.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("name", ["3d-24-o2", "27pt-perturbed-20", "band-mixed", "rmat-s12", "empty-rows"])
+@pytest.mark.parametrize("comp,pieces,run", [(1, 6, 0), (1, 4, 3000), (0, 8, 5000), (1, 16, 1)])
+def test_ring_walk_bitwise(name, comp, pieces, run):
+    """Ring walk (LMPK_FLAG_RING): tiles streamed through a ring of smem
+    pieces, items = runs of tiles; plain and compressed tiles, tiny runs
+    (run = 1 nnz: one tile per item) and deep rings."""
+    import torch
+
+    ap = MATRICES[name]()
+    n, k = ap.n_rows, 7
+    x = np.random.default_rng(31).uniform(-1, 1, n)
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, x, k)
+    fl = _lib.FLAG_MODE_STREAM | _lib.FLAG_RING | (_lib.FLAG_COMPRESS if comp else 0)
+    t = K.Tiling(ap.device(), k, tile_nnz=run, slots=pieces, mode_flags=fl)
+    assert t.info["mode"] == 3 and t.info["super_tiles"] >= 1
+    y = torch.zeros((k + 1, n), dtype=torch.float64, device="cuda")
+    y[0] = torch.from_numpy(x)
+    for rep in range(3):
+        K.mpk_run(t, y, K.mpk_power_cfg(k), exact=True)
+        assert np.array_equal(y.cpu().numpy(), ref), rep
+    y[1:] = 0
+    K.mpk_run(t, y, K.mpk_power_cfg(k), flags=_lib.FLAG_SWEEP, exact=True)
+    assert np.array_equal(y.cpu().numpy(), ref)
+
+
+def test_ring_cheb_complex_bitwise():
+    """Complex Chebyshev + accumulation through the ring walk equals the group walk."""
+    import torch
+
+    ap = MATRICES["anderson-12"]()
+    n, k = ap.n_rows, 6
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    cre, cim = rng.standard_normal(k), rng.standard_normal(k)
+    outs = []
+    for fl in (_lib.FLAG_RING | _lib.FLAG_COMPRESS, 0):
+        t = K.Tiling(ap.device(), k, tile_nnz=2000, slots=4, mode_flags=_lib.FLAG_MODE_STREAM | _lib.FLAG_COMPLEX | fl)
+        y = torch.zeros((k + 2, 2 * n), dtype=torch.float64, device="cuda")
+        y[0] = torch.from_numpy(x.view(np.float64).copy())
+        y[1] = torch.from_numpy((0.25 * x).view(np.float64).copy())
+        acc = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+        p = np.arange(1, k + 1)
+        cfg = K.power_cfg(k, p + 1, p, p - 1, np.full(k, _lib.KERNEL_CHEB), cre, cim)
+        K.mpk_run(t, y, cfg, acc=acc, use_acc=True, complex_state=True, exact=True)
+        outs.append((y.cpu().numpy(), acc.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])

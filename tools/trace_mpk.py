@@ -14,7 +14,9 @@ a = K.DeviceCsr.from_host(rp, c, v)
 perm, inv, lp = K.bfs_levels(a, 0)
 b = K.permute_symmetric(a, perm, inv)
 ctx = _lib.context()
-t = K.Tiling(b, k, slots=int(os.environ.get("SLOTS", "2")), tile_nnz=int(os.environ.get("TILE", "0")))
+t = K.Tiling(b, k, slots=int(os.environ.get("SLOTS", "2")), tile_nnz=int(os.environ.get("TILE", "0")),
+             mode_flags=int(os.environ.get("MODE_FLAGS", "0")), queue_slack=int(os.environ.get("SLACK", "0")))
+print("tiling", t.info)
 y = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); y[0] = 1.0
 cfg = K.mpk_power_cfg(k)
 flags = int(os.environ.get("FLAGS", "0"))
@@ -35,7 +37,7 @@ print("events", len(ev), "span us", tm[-1] / 1e3)
 # steady-state window
 mid = tm[-1] // 2
 sel = (tm > mid) & (tm < mid + 40000)
-for i in np.nonzero(sel)[0][:120]:
+for i in np.nonzero(sel)[0][:int(os.environ.get('NEV', '60'))]:
     print(f"{tm[i]/1e3:9.3f} us  slot {slot[i]} warp {warp[i]:2d} {names.get(int(kind[i]), kind[i]):10s} tile {item[i] >> 8:5d} p {item[i] & 255}")
 # per-item phase durations (producer view), by (slot, item)
 import collections
