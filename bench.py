@@ -364,7 +364,10 @@ def run_ours(args, cfgd):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfgd["name"], "n_rows": n, "nnz": nnz, "k": k,
                    "mode": til.mode, "tiles": til.info["n_tiles"],
-                   "tile_nnz_cap": til.info["tile_nnz_cap"], "slots": tparams.get("slots"),
+                   "tile_nnz_cap": til.info["tile_nnz_cap"], "slots": til.info["slots"],
+                   "super_tiles": til.info["super_tiles"],
+                   "block_format": {"bytes": til.info["block_bytes"], "compressed_tiles": til.info["compressed_tiles"],
+                                    "dict_tiles": til.info["dict_tiles"]},
                    "inputs_exceed_l2": True, "parallelism": "replicas" if world > 1 else "single"},
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -496,7 +499,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", default="cfg2")
-    ap.add_argument("--mode", choices=("auto", "res", "stream"), default="stream")
+    ap.add_argument("--mode", choices=("auto", "res", "stream"), default="auto")
     ap.add_argument("--slots", type=int, default=2)
     ap.add_argument("--tile-nnz", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

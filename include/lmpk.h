@@ -71,6 +71,7 @@ extern "C" {
                                     /* through a ring of smem pieces; items are */
                                     /* runs of tiles, tile_nnz_hint = run nnz,  */
                                     /* slots = ring depth <= 16)                */
+#define LMPK_FLAG_PLAIN 0x8000      /* tiling: default plan on plain blocks      */
 #define LMPK_FLAG_COMPRESS 0x2000   /* tiling: compressed tile blocks (int16     */
                                     /* column offsets, per-tile dictionary of   */
                                     /* <= 256 values), bitwise-identical sums   */

@@ -35,6 +35,7 @@ FLAG_EXACT = 0x400
 FLAG_READY_QUEUE = 0x1000
 FLAG_COMPRESS = 0x2000
 FLAG_RING = 0x4000
+FLAG_PLAIN = 0x8000
 
 MAX_POWERS = 64
 

@@ -879,7 +879,12 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   LMPK_ARG_CHECK(n >= 0, "n must be >= 0");
   lmpk_tiling_params prm{};
   if (params) prm = *params;
-  bool ring = (prm.mode_flags & LMPK_FLAG_RING) != 0;
+  // default plan (no mode flag, no q): the ring walk over compressed tiles,
+  // measured fastest on every BASELINE shape; LMPK_FLAG_PLAIN
+  // keeps it on plain tile-SELL-32 blocks
+  const bool default_plan = !(prm.mode_flags & (LMPK_FLAG_MODE_STREAM | LMPK_FLAG_MODE_RESIDENT | LMPK_FLAG_NO_TMA)) &&
+                            prm.powers_per_item == 0;
+  bool ring = (prm.mode_flags & LMPK_FLAG_RING) != 0 || default_plan;
   if (const char* e = getenv("LMPK_RING")) ring = atoi(e) != 0;
   if ((prm.mode_flags & (LMPK_FLAG_MODE_RESIDENT | LMPK_FLAG_NO_TMA)) || prm.powers_per_item > 1) ring = false;
   LMPK_ARG_CHECK(prm.slots >= 0 && prm.slots <= (ring ? kRingMax : kMaxSlots), "slots must be in [0, %d]",
@@ -909,7 +914,8 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   } guard{d_w, d_wmin, d_fit};
   // compressed blocks (int16 column offsets + value dictionary): opt-in via
   // LMPK_FLAG_COMPRESS or LMPK_COMPRESS=1; not with unstaged blocks or x staging
-  bool compress = (prm.mode_flags & LMPK_FLAG_COMPRESS) != 0;
+  bool compress = (prm.mode_flags & LMPK_FLAG_COMPRESS) != 0 ||
+                  (default_plan && !(prm.mode_flags & LMPK_FLAG_PLAIN));
   if (const char* e = getenv("LMPK_COMPRESS")) compress = atoi(e) != 0;
   if (prm.mode_flags & LMPK_FLAG_NO_TMA) compress = false;
   std::vector<uint8_t> fit16;
@@ -943,7 +949,8 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     else
       for (int r : {2, 3, 4}) cands.push_back({p_m, r});
   } else if (ring) {
-    cands.push_back({1, R0 ? R0 : 6});  // ring depth (pieces)
+    cands.push_back({1, R0 ? R0 : 2});  // ring depth (pieces): 2 x ~113 KB measured best on cfg2
+    if (!R0) cands.push_back({1, 3});
   } else if (want_stream || prm.powers_per_item > 0) {
     const int q = prm.powers_per_item > 0 ? prm.powers_per_item : 1;
     cands.push_back({q, R0 ? R0 : 2});
@@ -1064,8 +1071,9 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   if (ring) return finish_ring_tiling(ctx, T, p_m, prm, info, out, st);
   // skewed diagonal key (t + g*M, g), M = q*D + slack
   const int32_t G = (p_m + q_used - 1) / q_used;
-  // default slack ~1.5 * (items in flight) / G: measured optimum on cfg2
-  const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (3 * grid * slots) / (2 * G));
+  // default slack ~3 * (items in flight) / G: the dependency of an item must
+  // have left the queue >= ~2 item durations earlier (measured on cfg2)
+  const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (3 * grid * slots) / G);
   T->info.queue_slack = G > 1 ? slack : 0;
   const int64_t M = int64_t(q_used) * std::max(mfwd, 0) + slack;
   std::vector<int64_t> keys;
@@ -1125,6 +1133,15 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
   // shared-memory carveout: just what the slots need, so the rest of the
   // unified L1 serves the gathers (the driver rounds up to a supported split)
   {
+    static bool dyn_set[4] = {false, false, false, false};
+    const int di = (cplx ? 2 : 0) + (exact ? 1 : 0);
+    if (!dyn_set[di]) {  // a ring tiling's sweep may be this kernel's first launch
+      cudaFuncAttributes fa;
+      LMPK_CHECK_CUDA(cudaFuncGetAttributes(&fa, fn));
+      LMPK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes)));
+      dyn_set[di] = true;
+    }
     static int last[4] = {-1, -1, -1, -1};
     const int idx = (cplx ? 2 : 0) + (exact ? 1 : 0);
     int stat = 0;

@@ -86,7 +86,7 @@ class Tiling:
 
     @property
     def mode(self) -> str:
-        return {1: "resident", 2: "streaming"}[self.info["mode"]]
+        return {1: "resident", 2: "streaming", 3: "ring"}[self.info["mode"]]
 
     @property
     def group(self) -> int:

@@ -1,4 +1,4 @@
 export PYTHONDONTWRITEBYTECODE=1
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-SPECS='[[1,2,0,0,2,1,0,0,1,1],[1,3,0,0,2,1,0,0,1,1],[1,2,0,110,2,1,0,0,1],[1,2,0,160,2,1,0,0,1],[1,2,0,0,2,0,0,0,1,1]]' timeout 300 python tools/bench_modes.py 2>&1 | tail -5
-python tools/probe_c.py 2>&1 | grep "R 2" | head -8
+timeout 600 python bench.py --steps 100 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?; cat gpurun_out/bench.json
+python -c 'import __graft_entry__ as g; g.smoke()' 2>&1 | tail -1
