@@ -977,7 +977,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   // off: measured slower on cfg2 -- 1.36 vs 0.99 ms at 25%)
   int xfrac = 0;
   if (const char* e = getenv("LMPK_XFRAC")) xfrac = std::max(0, std::min(60, atoi(e)));
-  const bool xstage = !ring && !unstaged && !(prm.mode_flags & LMPK_FLAG_COMPLEX) && xfrac > 0 && n > 0;
+  const bool xstage = !unstaged && !(prm.mode_flags & LMPK_FLAG_COMPLEX) && xfrac > 0 && n > 0;
   std::vector<int32_t> h_rp, h_col;
   if (xstage) {
     h_rp.resize(size_t(n) + 1);

@@ -730,6 +730,127 @@ __device__ __noinline__ double2 cslice_any(const SmemBlk& B, CSlice a, uint32_t 
   return make_double2(tr, ti);
 }
 
+// One chunk of n (4, 2 or 1) entries of a compressed slice: the lane's
+// column offsets, values and gathers (padding entries j >= len gather
+// nothing; their stored value is 0.0, so they add +0 exactly).
+template <int NQ, bool VD>
+__device__ __forceinline__ void c16_quads(const SmemBlk& B, uint32_t cb, uint32_t vb, uint32_t lane, uint32_t dict,
+                                          int q0, int32_t (&c)[4 * NQ], double (&v)[4 * NQ]) {
+#pragma unroll
+  for (int u = 0; u < NQ; ++u) {
+    const int2 cc = B.i2(cb + uint32_t(q0 + u) * 256u + lane * 8u);
+    c[4 * u] = sx16(cc.x), c[4 * u + 1] = cc.x >> 16, c[4 * u + 2] = sx16(cc.y), c[4 * u + 3] = cc.y >> 16;
+    if constexpr (VD) {
+      const uint32_t k = uint32_t(B.i1(vb + uint32_t(q0 + u) * 128u + lane * 4u));
+      v[4 * u] = lds_f64(dict + (k & 255u));
+      v[4 * u + 1] = lds_f64(dict + ((k >> 8) & 255u));
+      v[4 * u + 2] = lds_f64(dict + ((k >> 16) & 255u));
+      v[4 * u + 3] = lds_f64(dict + (k >> 24));
+    } else {
+      const double2 a0 = B.d2(vb + uint32_t(q0 + u) * 1024u + lane * 32u);
+      const double2 a1 = B.d2(vb + uint32_t(q0 + u) * 1024u + lane * 32u + 16u);
+      v[4 * u] = a0.x, v[4 * u + 1] = a0.y, v[4 * u + 2] = a1.x, v[4 * u + 3] = a1.y;
+    }
+  }
+}
+
+// Long rows (w > 8, real vectors): quads two at a time (8 gathers in flight),
+// then the pair / single tail; storage order throughout.
+template <bool EXACT, bool VD, class G>
+__device__ __noinline__ double cslice_real_long(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
+                                                const G& g, int w, int len) {
+  const int Q = w >> 2, PR = (w >> 1) & 1;
+  const typename G::Row rp = g.row(row);
+  double t = 0.0;
+  int q = 0;
+  for (; q + 2 <= Q; q += 2) {
+    int32_t c[8];
+    double v[8], x[8];
+    c16_quads<2, VD>(B, a.cb, a.vb, lane, dict, q, c, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = (4 * q + j < len) ? g.at(rp, c[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t = madd<EXACT>(t, v[j], x[j]);
+  }
+  if (q < Q) {
+    int32_t c[4];
+    double v[4], x[4];
+    c16_quads<1, VD>(B, a.cb, a.vb, lane, dict, q, c, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = (4 * q + j < len) ? g.at(rp, c[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t = madd<EXACT>(t, v[j], x[j]);
+  }
+  const int j0 = 4 * Q;
+  if (PR) {
+    const int32_t cc = B.i1(a.cb + uint32_t(Q) * 256u + lane * 4u);
+    double v0, v1;
+    if constexpr (VD) {
+      const uint32_t k = B.u16(a.vb + uint32_t(Q) * 128u + lane * 2u);
+      v0 = lds_f64(dict + (k & 255u));
+      v1 = lds_f64(dict + (k >> 8));
+    } else {
+      const double2 vv = B.d2(a.vb + uint32_t(Q) * 1024u + lane * 16u);
+      v0 = vv.x, v1 = vv.y;
+    }
+    const double x0 = j0 < len ? g.at(rp, sx16(cc)) : 0.0;
+    const double x1 = j0 + 1 < len ? g.at(rp, cc >> 16) : 0.0;
+    t = madd<EXACT>(t, v0, x0);
+    t = madd<EXACT>(t, v1, x1);
+  }
+  if (w & 1) {
+    const int32_t cc = sx16(int32_t(B.u16(a.cb + uint32_t(Q) * 256u + uint32_t(PR) * 128u + lane * 2u)));
+    double v0;
+    if constexpr (VD)
+      v0 = lds_f64(dict + B.u8(a.vb + uint32_t(Q) * 128u + uint32_t(PR) * 64u + lane));
+    else
+      v0 = B.d1(a.vb + uint32_t(Q) * 1024u + uint32_t(PR) * 512u + lane * 8u);
+    const double x0 = w - 1 < len ? g.at(rp, cc) : 0.0;
+    t = madd<EXACT>(t, v0, x0);
+  }
+  return t;
+}
+
+// Complex vectors (real matrix), any width: a quad at a time (4 complex
+// gathers in flight); storage order, re and im chains as the plain path.
+template <bool EXACT, bool VD, class G>
+__device__ __noinline__ double2 cslice_cplx(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
+                                            const G& g, int w, int len) {
+  const int Q = w >> 2, PR = (w >> 1) & 1;
+  double tr = 0.0, ti = 0.0;
+  for (int q = 0; q < Q; ++q) {
+    int32_t c[4];
+    double v[4];
+    c16_quads<1, VD>(B, a.cb, a.vb, lane, dict, q, c, v);
+    double2 x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = (4 * q + j < len) ? g.d2(row + c[j]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      tr = madd<EXACT>(tr, v[j], x[j].x);
+      ti = madd<EXACT>(ti, v[j], x[j].y);
+    }
+  }
+  const int j0 = 4 * Q;
+  for (int j = j0; j < w; ++j) {
+    uint32_t ec;
+    if (PR && j < j0 + 2)
+      ec = uint32_t(Q) * 128u + lane * 2u + uint32_t(j - j0);
+    else
+      ec = uint32_t(Q) * 128u + (PR ? 64u : 0u) + lane;
+    const int32_t c = row + sx16(int32_t(B.u16(a.cb + ec * 2u)));
+    double v;
+    if constexpr (VD)
+      v = lds_f64(dict + B.u8(a.vb + ec));
+    else
+      v = B.d1(a.vb + ec * 8u);
+    const double2 x = j < len ? g.d2(c) : make_double2(0.0, 0.0);
+    tr = madd<EXACT>(tr, v, x.x);
+    ti = madd<EXACT>(ti, v, x.y);
+  }
+  return make_double2(tr, ti);
+}
+
 template <bool EXACT, bool FULL, bool VD, class G>
 __device__ __forceinline__ double cslice_real(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row,
                                               uint32_t dict, const G& g, int w, int len) {
@@ -743,7 +864,7 @@ __device__ __forceinline__ double cslice_real(const SmemBlk& B, CSlice a, uint32
     case 7: return cslice_real_w<7, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
     case 8: return cslice_real_w<8, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
     case 0: return 0.0;
-    default: return cslice_any<false, EXACT, VD>(B, a, lane, row, dict, g, w, FULL ? w : len).x;
+    default: return cslice_real_long<EXACT, VD>(B, a, lane, row, dict, g, w, FULL ? w : len);
   }
 }
 
@@ -785,15 +906,19 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
     return int(uint32_t(rec.y) >> 16) == w ? w : int(B.u16(lens_o + uint32_t(s) * 64 + lane * 2));
   };
   if constexpr (!CPLX) {
+    // lane-offset pointers: slice s of this lane is element s * 32
+    double* yl = yout + lane;
+    const double* pl = ypv + lane;
+    double* al = acc + lane;
     auto epilogue = [&](int32_t s, double t) {
-      const int32_t lr = s * 32 + int32_t(lane);
-      if (lr < nrows) {
+      if (s * 32 + int32_t(lane) < nrows) {
+        const int32_t o = s * 32;
         if constexpr (GENERAL) {
-          if (pt.cheb) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(ypv + lr));
-          stg_y(yout + lr, t, pt.ypol);
-          if (use_acc) stg_f64(acc + lr, madd<EXACT>(ld_cg(acc + lr), pt.cre, t));
+          if (pt.cheb) t = __dsub_rn(__dmul_rn(2.0, t), ld_cg(pl + o));
+          stg_f64(yl + o, t);
+          if (use_acc) stg_f64(al + o, madd<EXACT>(ld_cg(al + o), pt.cre, t));
         } else {
-          stg_y(yout + lr, t, pt.ypol);
+          stg_f64(yl + o, t);
         }
       }
     };
@@ -804,8 +929,12 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
       if (int(uint32_t(rec.y) >> 16) == w) return cslice_real<EXACT, true, VD>(B, a, lane, row, dict, g, w, w);
       return cslice_real<EXACT, false, VD>(B, a, lane, row, dict, g, w, len_of(s, rec));
     };
-    for (int32_t s = sched_first(sched, wid, 2); s < ns; s = sched_next(sched, s, 2 * nwarps, 2)) {
-      const int32_t s2 = sched != kSchedStatic ? s + 1 : s + nwarps;
+    // slices s and s2 (dynamic grabs: s + 1; static: s + nwarps): a
+    // same-width pair keeps both slices' gathers in flight.  One loop so the
+    // body is inlined once (two call sites made ptxas outline it to a stack frame).
+    const bool dyn = sched != kSchedStatic;
+    for (int32_t s = dyn ? sched_grab(sched, 2) : wid; s < ns; s = dyn ? sched_grab(sched, 2) : s + 2 * nwarps) {
+      const int32_t s2 = dyn ? s + 1 : s + nwarps;
       const int2 rec0 = B.i2(uint32_t(s) * 8);
       if (s2 >= ns) {
         epilogue(s, single(s, rec0));
@@ -813,12 +942,12 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
       }
       const int2 rec1 = B.i2(uint32_t(s2) * 8);
       const int w0 = rec0.y & 0xffff, w1 = rec1.y & 0xffff;
-      if (w0 == w1 && w0 >= 1 && w0 <= 8) {
-        const bool full0 = int(uint32_t(rec0.y) >> 16) == w0, full1 = int(uint32_t(rec1.y) >> 16) == w1;
+      if (w0 == w1 && uint32_t(w0 - 1) < 8u) {
+        const bool full = (uint32_t(rec0.y) >> 16) == uint32_t(w0) && (uint32_t(rec1.y) >> 16) == uint32_t(w1);
         const CSlice a0 = cslice<VD>(col_o, val_o, uint32_t(rec0.x)), a1 = cslice<VD>(col_o, val_o, uint32_t(rec1.x));
         const int32_t row0 = LOCAL ? rb : rb + s * 32, row1 = LOCAL ? rb : rb + s2 * 32;
         double2 t;
-        if (full0 && full1)
+        if (full)
           t = cslice_real_pair<EXACT, true, VD>(B, a0, a1, lane, row0, row1, dict, g, w0, w0, w0);
         else
           t = cslice_real_pair<EXACT, false, VD>(B, a0, a1, lane, row0, row1, dict, g, w0, len_of(s, rec0),
@@ -836,7 +965,7 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
       const CSlice a = cslice<VD>(col_o, val_o, uint32_t(rec.x));
       const int w = rec.y & 0xffff;
       const int32_t lr = s * 32 + int32_t(lane);
-      double2 t = cslice_any<true, EXACT, VD>(B, a, lane, LOCAL ? rb : r0 + lr, dict, g, w, len_of(s, rec));
+      double2 t = cslice_cplx<EXACT, VD>(B, a, lane, LOCAL ? rb : r0 + lr, dict, g, w, len_of(s, rec));
       if (lr < nrows) {
         const int64_t r2 = 2 * int64_t(lr);
         if constexpr (GENERAL) {
@@ -1558,7 +1687,7 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kRingMax], empty_bar[kRingMax], done_bar[kRingMax];
   __shared__ int32_t d_t[kRingMax], d_p[kRingMax], d_r0[kRingMax], d_rows[kRingMax], d_E[kRingMax];
-  __shared__ int32_t d_mode[kRingMax], d_glb[kRingMax];
+  __shared__ int32_t d_mode[kRingMax], d_glb[kRingMax], d_nseg[kRingMax], d_xoff[kRingMax];
   __shared__ int64_t d_ofs[kRingMax];
   __shared__ uint32_t d_done[kRingMax], d_ctr[kRingMax];
   __shared__ uint32_t trace_ctr;
@@ -1595,9 +1724,11 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
     }
   } else if (warp == NC) {
     // ------------------------------------------------ producer
-    const uint64_t pol = ((P.flags >> 8) & 3) == 0 ? policy_evict_last()
-                                                   : (((P.flags >> 8) & 3) == 1 ? policy_evict_normal()
-                                                                                : policy_evict_first());
+    // block L2 policy (run flag bits 8-9): 0 (default) / 2 evict_first -- the
+    // blocks' 8-power reuse window exceeds L2, so keeping them only evicts the
+    // gathered vectors (measured: 0.51 vs 0.53 ms on cfg2) -- 1 normal, 3 last
+    const int pm = (P.flags >> 8) & 3;
+    const uint64_t pol = pm == 1 ? policy_evict_normal() : (pm == 3 ? policy_evict_last() : policy_evict_first());
     unsigned long long rounds = 0;
     uint32_t k = 0;
     bool abort = false;
@@ -1632,14 +1763,37 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
           d_mode[slot] = glb ? 0 : (P.tile_mode ? __ldg(P.tile_mode + m) : 0);
           d_glb[slot] = glb ? 1 : 0;
           d_ofs[slot] = ofs;
+          const int32_t nseg = (glb || !P.xmode) ? 0 : __ldg(P.tile_nseg + m);
+          d_nseg[slot] = nseg;
+          d_xoff[slot] = int32_t(bytes);  // the x buffer follows the block
           trace_ev(P, &trace_ctr, 2, uint32_t(slot), uint32_t(m) << 8 | uint32_t(p));
           if (!glb) {
+            const uint32_t xbytes = (nseg > 0 && P.xmode == 1) ? uint32_t(__ldg(P.tile_xent + m)) * 8u : 0u;
             fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&full_bar[slot], uint32_t(bytes));
+            mbar_arrive_expect_tx(&full_bar[slot], uint32_t(bytes) + xbytes);
             bulk_g2s(smem_raw + int64_t(slot) * P.smem_cap, P.blocks + ofs, uint32_t(bytes), &full_bar[slot],
                      p == P.n_powers ? policy_evict_first() : pol);
           } else {
             mbar_arrive(&full_bar[slot]);
+          }
+        }
+        __syncwarp();
+        // x staging: the runs of y_{p-1} this piece gathers, bulk-copied after
+        // the item's dependencies were acquired (segment table read from the
+        // block in global memory: the staged copy may not have landed yet)
+        const int32_t nseg = __shfl_sync(0xffffffffu, lane == 0 ? d_nseg[slot] : 0, 0);
+        if (nseg > 0 && P.xmode == 1) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const int64_t ofs = __ldg(P.tile_ofs + m);
+          const int32_t rows = __ldg(P.tile_row + m + 1) - __ldg(P.tile_row + m);
+          const int4* seg = reinterpret_cast<const int4*>(P.blocks + ofs + blk_seg_off((rows + 31) >> 5));
+          const uint32_t xb = ring_base + uint32_t(slot) * uint32_t(P.smem_cap) +
+                              uint32_t(__ldg(P.tile_ofs + m + 1) - ofs);
+          const char* yin = s_pow[p - 1].yin;
+          for (int j = lane; j < nseg; j += 32) {
+            const int4 sg = __ldg(seg + j);
+            bulk_g2s_a(xb + uint32_t(sg.z) * 8u, yin + int64_t(sg.x) * 8, uint32_t((sg.y + 1) & ~1) * 8u,
+                       &full_bar[slot], policy_evict_normal());
           }
         }
         __syncwarp();
@@ -1683,7 +1837,34 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
       const PowTab& pt = s_pow[p - 1];
       const uint32_t sch = (P.flags & 0x8000) ? kSchedStatic : smem_u32(&d_ctr[slot]);
       if (lane == 0 && (warp == 0 || warp == NC - 1)) trace_ev(P, &trace_ctr, 10, uint32_t(slot), uint32_t(t) << 8 | uint32_t(p));
-      if (!d_glb[slot]) {
+      const int32_t nseg = d_nseg[slot];
+      if (!CPLX && nseg > 0) {
+        // gathers from the staged x runs (local columns)
+        const SmemBlk B{ring_base + uint32_t(slot) * uint32_t(P.smem_cap)};
+        const uint32_t xb = B.a + uint32_t(d_xoff[slot]);
+        if (P.xmode == 2) copy_x_segments<CPLX, NC>(B, pt, rows, nseg, xb, warp, lane);
+        const GatherSmem G{xb};
+        if constexpr (!CPLX) {
+          const int32_t nd = tmode >> 8;
+          if (tmode == 0) {
+            if (pt.general)
+              tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
+            else
+              tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
+          } else if (tmode & kModeDict) {
+            if (pt.general)
+              tile_power_c<CPLX, EXACT, true, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
+            else
+              tile_power_c<CPLX, EXACT, false, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
+          } else {
+            if (pt.general)
+              tile_power_c<CPLX, EXACT, true, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
+            else
+              tile_power_c<CPLX, EXACT, false, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC,
+                                                            sch);
+          }
+        }
+      } else if (!d_glb[slot]) {
         const SmemBlk B{ring_base + uint32_t(slot) * uint32_t(P.smem_cap)};
         const GatherGlobal G{pt.yin};
         if (tmode != 0) {

@@ -151,7 +151,8 @@ def test_compressed_complex_cheb_bitwise():
 
 @pytest.mark.parametrize("name", ["3d-24-o2", "27pt-perturbed-20", "band-mixed"])
 @pytest.mark.parametrize("misaligned", [False, True])
-def test_compressed_x_staged_bitwise(name, misaligned, monkeypatch):
+@pytest.mark.parametrize("ring", [False, True])
+def test_compressed_x_staged_bitwise(name, misaligned, ring, monkeypatch):
     """Compressed blocks whose gathers come from the staged x-segments (local
     int16 columns, LMPK_XFRAC); a slot stride that is not 16-byte aligned
     takes the cooperative-copy path."""
@@ -162,8 +163,10 @@ def test_compressed_x_staged_bitwise(name, misaligned, monkeypatch):
     n, k = ap.n_rows, 6
     x = np.random.default_rng(23).uniform(-1, 1, n)
     ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, x, k)
-    t = K.Tiling(ap.device(), k, tile_nnz=1500, slots=2, mode_flags=_lib.FLAG_MODE_STREAM | _lib.FLAG_COMPRESS)
+    fl = (_lib.FLAG_RING if ring else _lib.FLAG_MODE_STREAM) | _lib.FLAG_COMPRESS
+    t = K.Tiling(ap.device(), k, tile_nnz=1500 if not ring else 4000, slots=2 if not ring else 6, mode_flags=fl)
     assert t.info["x_staged_tiles"] > 0 and t.info["compressed_tiles"] > 0
+    assert (t.info["mode"] == 3) == ring
     ld = n + (1 if misaligned and n % 2 == 0 else 0)
     buf = torch.zeros((k + 1) * ld + 1, dtype=torch.float64, device="cuda")
     y = buf[1:1 + (k + 1) * ld].view(k + 1, ld)[:, :n] if misaligned else buf[:(k + 1) * ld].view(k + 1, ld)
