@@ -25,6 +25,8 @@ from __future__ import annotations
 
 import time
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -114,6 +116,41 @@ def _to_device_f64(arr):
     return torch.from_numpy(np.ascontiguousarray(arr)).cuda()
 
 
+def _schedule(plan: ExecPlan, til, yv, cfg, av, use_acc, cplx, flags):
+    """Wavefront walk or per-power sweeps for this plan (same bits).  The walk
+    pays when the level window fits the L2 (cfg2, cfg5 shapes); for very wide
+    levels (cfg3 27-point 160^3: 20 MB per level) the blocks are re-read from
+    HBM at every power anyway and the dependency-free sweep is faster.  Chosen
+    once per plan by timing one call of each on scratch copies; LMPK_SCHEDULE=
+    walk|sweep forces it."""
+    forced = os.environ.get("LMPK_SCHEDULE", "auto")
+    if forced in ("walk", "sweep"):
+        return forced
+    got = plan.schedule_choice(cplx)
+    if got is not None:
+        return got
+    if plan.a.n_nz < 4_000_000:  # small problems: latency-bound either way, keep the walk
+        plan.set_schedule_choice(cplx, "walk")
+        return "walk"
+    torch = _torch()
+    ys = yv.clone()
+    as_ = av.clone() if av is not None else None
+    times = {}
+    for name, f in (("walk", 0), ("sweep", _lib.FLAG_SWEEP)):
+        K.mpk_run(til, ys, cfg, acc=as_, use_acc=use_acc, complex_state=cplx, flags=flags | f, check_errors=False)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        K.mpk_run(til, ys, cfg, acc=as_, use_acc=use_acc, complex_state=cplx, flags=flags | f, check_errors=False)
+        e1.record()
+        e1.synchronize()
+        times[name] = e0.elapsed_time(e1)
+    del ys, as_
+    choice = min(times, key=times.get)
+    plan.set_schedule_choice(cplx, choice)
+    return choice
+
+
 def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
     """Run one plan on device buffers; returns device seconds."""
     torch = _torch()
@@ -135,7 +172,16 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
             K.mpk_baseline(plan.a.device(), yv, plan.p_m)
     else:
         cfg = plan.power_config()
-        K.mpk_run(plan.tiling(complex_state=cplx), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=flags)
+        til = plan.tiling(complex_state=cplx)
+        if til is None:
+            # rows too long for the tile format: CRS sweeps (plain MPK only)
+            if cplx or use_acc or np.any(plan.kernel != 0):
+                raise NotImplementedError("rows longer than 65535 entries: only plain real MPK runs (CRS sweeps)")
+            K.mpk_baseline(plan.a.device(), yv, plan.p_m)
+        else:
+            sched = _schedule(plan, til, yv, cfg, av, use_acc, cplx, flags)
+            f = flags | (_lib.FLAG_SWEEP if sched == "sweep" else 0)
+            K.mpk_run(til, yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=f)
     e1.record()
     e1.synchronize()
     ctx = _lib.context()

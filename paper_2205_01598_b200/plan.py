@@ -79,6 +79,7 @@ class ExecPlan:
     acc_coef: np.ndarray = None
     tiling_params: dict = None
     _tiling: object = None
+    _sched: dict = None
 
     @property
     def n_items(self) -> int:
@@ -101,8 +102,26 @@ class ExecPlan:
             prm = dict(self.tiling_params or {})
             if key:
                 prm["mode_flags"] = int(prm.get("mode_flags", 0)) | _lib.FLAG_COMPLEX
-            self._tiling[key] = K.Tiling(self.a.device(), self.p_m, **prm)
+            try:
+                self._tiling[key] = K.Tiling(self.a.device(), self.p_m, **prm)
+            except ValueError as e:
+                # rows beyond the tile format (power-law hubs, > 65535 entries):
+                # the plan runs as CRS sweeps (executor._launch); None marks it
+                if "rows longer than" not in str(e):
+                    raise
+                self._tiling[key] = None
         return self._tiling[key]
+
+    def schedule_choice(self, complex_state=False):
+        """'walk' (level-blocked wavefront) or 'sweep' (dependency-free power
+        sweeps on the same tiles) -- identical bits, chosen per plan by timing
+        both once (executor._launch); None until measured."""
+        return (self._sched or {}).get(bool(complex_state))
+
+    def set_schedule_choice(self, complex_state, choice):
+        if self._sched is None:
+            self._sched = {}
+        self._sched[bool(complex_state)] = choice
 
     def power_config(self, acc_coef_im=None):
         """Per-power kernel configuration for liblmpk.  The reference stores it

@@ -222,3 +222,31 @@ def test_ring_cheb_complex_bitwise():
         K.mpk_run(t, y, cfg, acc=acc, use_acc=True, complex_state=True, exact=True)
         outs.append((y.cpu().numpy(), acc.cpu().numpy()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_hub_rows_fall_back_to_crs_sweeps():
+    """A star graph (row 0 couples to all 70,000 rows) exceeds the tile
+    format's 65535-entry rows: run_mpk runs the plan as CRS sweeps, same bits."""
+    n = 70_000
+    i = np.arange(1, n)
+    rows = np.concatenate([np.zeros(n - 1, dtype=np.int64), i, np.arange(n)])
+    cols = np.concatenate([i, np.zeros(n - 1, dtype=np.int64), np.arange(n)])
+    vals = np.concatenate([np.full(n - 1, -1e-3), np.full(n - 1, -1e-3), np.full(n, 2.0)])
+    a = lm.CsrMatrix.from_triplets(n, rows, cols, vals)
+    x = np.random.default_rng(2).uniform(-1, 1, n)
+    res, pre = lm.run_mpk(a, x, "lb_lg_p2p", 4, 126e6)
+    ap = pre.a
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, pre.perm.apply_to_vector(x), 4)
+    assert np.array_equal(np.asarray(res.y.data), ref)
+
+
+@pytest.mark.parametrize("sched", ["walk", "sweep", "auto"])
+def test_schedule_choice_bitwise(sched, monkeypatch):
+    """The executor's walk / sweep choice (LMPK_SCHEDULE) never changes the bits."""
+    monkeypatch.setenv("LMPK_SCHEDULE", sched)
+    a = lm.gen_stencil_3d27pt(72, seed=3)  # > 4M nnz: 'auto' times both
+    x = np.random.default_rng(8).uniform(-1, 1, a.n_rows)
+    res, pre = lm.run_mpk(a, x, "lb_lg_p2p", 4, 126e6)
+    ap = pre.a
+    ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, pre.perm.apply_to_vector(x), 4)
+    assert np.array_equal(np.asarray(res.y.data), ref)

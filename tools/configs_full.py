@@ -29,11 +29,13 @@ for name, gen, ks in cases:
         yb = torch.zeros(k + 1, a.n_rows, dtype=torch.float64, device="cuda"); yb[0] = x
         tc = ev(lambda: K.mpk_baseline(d, yb, k))
         out = {"case": name, "nnz": a.n_nz, "k": k, "crs_us": round(tc * 1e3, 1), "gen_s": round(tg)}
-        for plan, fl in (("ring", 0), ("group_plain", _lib.FLAG_MODE_STREAM)):
-            t = K.Tiling(d, k, mode_flags=fl)
+        for plan, fl, rf in (("ring", 0, 0), ("ring_tiles_sweep", 0, _lib.FLAG_SWEEP),
+                             ("group_plain", _lib.FLAG_MODE_STREAM, 0)):
+            t = K.Tiling(d, k, mode_flags=fl, **({"queue_slack": int(os.environ["SLACK"])} if os.environ.get("SLACK") else {}),
+                         **({"tile_nnz": int(os.environ["RUN"])} if os.environ.get("RUN") and fl == 0 else {}))
             y = torch.zeros_like(yb); y[0] = x
-            tm = ev(lambda: K.mpk_run(t, y, cfg, check_errors=False))
-            K.mpk_run(t, y, cfg)
+            tm = ev(lambda: K.mpk_run(t, y, cfg, flags=rf, check_errors=False))
+            K.mpk_run(t, y, cfg, flags=rf)
             out[plan] = {"us": round(tm * 1e3, 1), "gflops": round(2 * a.n_nz * k / tm / 1e6),
                          "speedup_vs_crs": round(tc / tm, 2), "bitwise": bool(torch.equal(y, yb)),
                          "tiles": t.info["n_tiles"], "dict_tiles": t.info["dict_tiles"],
