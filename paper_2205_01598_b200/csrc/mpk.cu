@@ -281,20 +281,20 @@ const void* mpk_group_fn_re();
 const void* mpk_group_fn_rf();
 const void* mpk_group_fn_ce();
 const void* mpk_group_fn_cf();
-const void* mpk_ring_fn_re();
-const void* mpk_ring_fn_rf();
-const void* mpk_ring_fn_ce();
-const void* mpk_ring_fn_cf();
-static const void* ring_fn(bool cplx, bool exact) {
-  if (cplx) return exact ? mpk_ring_fn_ce() : mpk_ring_fn_cf();
-  return exact ? mpk_ring_fn_re() : mpk_ring_fn_rf();
+const void* mpk_ring_fn_re(bool has_long);
+const void* mpk_ring_fn_rf(bool has_long);
+const void* mpk_ring_fn_ce(bool has_long);
+const void* mpk_ring_fn_cf(bool has_long);
+static const void* ring_fn(bool cplx, bool exact, bool has_long = true) {
+  if (cplx) return exact ? mpk_ring_fn_ce(has_long) : mpk_ring_fn_cf(has_long);
+  return exact ? mpk_ring_fn_re(has_long) : mpk_ring_fn_rf(has_long);
 }
 // Occupancy of the ring kernel (all instantiations) at `smem` dynamic bytes.
 static int ring_occupancy(lmpk_ctx* ctx, int smem, int* occ) {
   *occ = 1 << 20;
-  for (int c = 0; c < 2; ++c)
+  for (int c = 0; c < 4; ++c)
     for (int x = 0; x < 2; ++x) {
-      const void* fn = ring_fn(c != 0, x != 0);
+      const void* fn = ring_fn((c & 1) != 0, x != 0, c >= 2);
       cudaFuncAttributes fa;
       cudaError_t e = cudaFuncGetAttributes(&fa, fn);
       if (e == cudaSuccess && smem > ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes)) {
@@ -353,7 +353,12 @@ static int group_static_smem(int* out) {
   for (int c = 0; c < 4; ++c)
     for (int x = 0; x < 2; ++x) {
       cudaFuncAttributes fa;
-      cudaError_t e = cudaFuncGetAttributes(&fa, c < 2 ? group_fn(c != 0, x != 0) : ring_fn(c == 3, x != 0));
+      cudaError_t e = cudaFuncGetAttributes(&fa, c < 2 ? group_fn(c != 0, x != 0) : ring_fn(c == 3, x != 0, true));
+      if (e == cudaSuccess && c >= 2) {
+        cudaFuncAttributes fb;
+        e = cudaFuncGetAttributes(&fb, ring_fn(c == 3, x != 0, false));
+        fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+      }
       if (e != cudaSuccess) {
         cudaGetLastError();
         set_error("cudaFuncGetAttributes failed: %s", cudaGetErrorString(e));
@@ -679,6 +684,16 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     tdict.assign(first.size(), -1);
   }
   const int32_t nt = static_cast<int32_t>(first.size());
+  // compressed tiles with slices wider than 8 take the long-row kernel body
+  for (int32_t t = 0; t < nt; ++t) {
+    if (!tmode[t]) continue;
+    const int32_t s1 = t + 1 < nt ? first[t + 1] : S;
+    for (int32_t sl = first[t]; sl < s1; ++sl)
+      if (width[sl] > 8) {
+        tmode[t] |= kModeLong;
+        break;
+      }
+  }
   std::vector<int32_t> tile_row(nt + 1), tile_E(nt), slice_tile(std::max(S, 1)), slice_off(std::max(S, 1));
   std::vector<int64_t> tile_ofs(nt + 1);
   for (int32_t t = 0; t < nt; ++t) tile_row[t] = std::min(first[t] * 32, n);
@@ -1172,13 +1187,13 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
   return LMPK_OK;
 }
 
-static int launch_ring(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, int grid, int smem,
-                       cudaStream_t st) {
+static int launch_ring(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool has_long, int grid,
+                       int smem, cudaStream_t st) {
   void* args[] = {&Pm, &C};
-  const void* fn = ring_fn(cplx, exact);
+  const void* fn = ring_fn(cplx, exact, has_long);
   {
-    static int last[4] = {-1, -1, -1, -1};
-    const int idx = (cplx ? 2 : 0) + (exact ? 1 : 0);
+    static int last[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+    const int idx = (has_long ? 4 : 0) + (cplx ? 2 : 0) + (exact ? 1 : 0);
     cudaFuncAttributes fa;
     LMPK_CHECK_CUDA(cudaFuncGetAttributes(&fa, fn));
     const int per_sm = std::max(1, ctx->max_smem_sm);
@@ -1333,7 +1348,7 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   if (T->ring) {
     LMPK_ARG_CHECK(!(flags & (LMPK_FLAG_NO_TMA | LMPK_FLAG_READY_QUEUE)),
                    "the ring walk has no unstaged / ready-queue variant");
-    return launch_ring(ctx, Pm, C, cplx, exact, grid, T->info.smem_bytes, st);
+    return launch_ring(ctx, Pm, C, cplx, exact, T->info.max_row_nnz > 8, grid, T->info.smem_bytes, st);
   }
   // co-residency of all CTAs is part of the deadlock-freedom argument.
   // LMPK_FLAG_NO_TMA: blocks are streamed from global memory by the

@@ -2,6 +2,9 @@
 #include "mpk_kernel.cuh"
 
 namespace lmpk {
-const void* mpk_ring_fn_re() { return reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kConsumers>); }
+const void* mpk_ring_fn_re(bool has_long) {
+  return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kConsumers, true>)
+                  : reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kConsumers, false>);
+}
 const void* mpk_group_fn_re() { return reinterpret_cast<const void*>(mpk_group_kernel<false, true, kConsumers>); }
 }  // namespace lmpk

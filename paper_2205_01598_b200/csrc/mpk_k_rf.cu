@@ -2,6 +2,9 @@
 #include "mpk_kernel.cuh"
 
 namespace lmpk {
-const void* mpk_ring_fn_rf() { return reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kConsumers>); }
+const void* mpk_ring_fn_rf(bool has_long) {
+  return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kConsumers, true>)
+                  : reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kConsumers, false>);
+}
 const void* mpk_group_fn_rf() { return reinterpret_cast<const void*>(mpk_group_kernel<false, false, kConsumers>); }
 }  // namespace lmpk

@@ -498,7 +498,7 @@ __device__ __forceinline__ double2 slice_real_pair(const Blk& B, uint32_t cb0, u
   }
 }
 
-template <bool EXACT, bool FULL, class Blk, class G>
+template <bool EXACT, bool FULL, class Blk, class G, bool LONG = true>
 __device__ __forceinline__ double slice_real(const Blk& B, uint32_t cb, uint32_t vb, uint32_t l4,
                                              const G& g, int w, int len) {
   switch (w) {
@@ -511,7 +511,11 @@ __device__ __forceinline__ double slice_real(const Blk& B, uint32_t cb, uint32_t
     case 7: return slice_real_w<7, EXACT, FULL>(B, cb, vb, l4, g, len);
     case 8: return slice_real_w<8, EXACT, FULL>(B, cb, vb, l4, g, len);
     case 0: return 0.0;
-    default: return slice_real_any<EXACT>(B, cb, vb, l4, g, w, FULL ? w : len);
+    default:
+      if constexpr (LONG)
+        return slice_real_any<EXACT>(B, cb, vb, l4, g, w, FULL ? w : len);
+      else
+        return 0.0;  // the tiling has no slice wider than 8
   }
 }
 
@@ -552,7 +556,7 @@ __device__ __forceinline__ int32_t sched_next(uint32_t sched, int32_t s, int ste
 // rec[s] = {first entry of slice s (relative to the tile), w | wmin << 16}.
 // Matrix bytes per entry: 3 (dictionary) or 10 (raw) instead of 12.
 constexpr int kDictMax = 32;  // codes are stored premultiplied by 8 (dictionary byte offsets)
-constexpr int32_t kModeC16 = 1, kModeDict = 2;
+constexpr int32_t kModeC16 = 1, kModeDict = 2, kModeLong = 4;  // kModeLong: some slice has w > 8
 // With x-segments (nseg > 0) the segment table (int4 x nseg, as in the plain
 // layout) follows the lens, and the columns are LOCAL indices into the slot's
 // x buffer, stored biased by -32768 (decoded as 32768 + int16).
@@ -757,7 +761,7 @@ __device__ __forceinline__ void c16_quads(const SmemBlk& B, uint32_t cb, uint32_
 // Long rows (w > 8, real vectors): quads two at a time (8 gathers in flight),
 // then the pair / single tail; storage order throughout.
 template <bool EXACT, bool VD, class G>
-__device__ __noinline__ double cslice_real_long(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
+__device__ __forceinline__ double cslice_real_long(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
                                                 const G& g, int w, int len) {
   const int Q = w >> 2, PR = (w >> 1) & 1;
   const typename G::Row rp = g.row(row);
@@ -814,7 +818,7 @@ __device__ __noinline__ double cslice_real_long(const SmemBlk& B, CSlice a, uint
 // Complex vectors (real matrix), any width: a quad at a time (4 complex
 // gathers in flight); storage order, re and im chains as the plain path.
 template <bool EXACT, bool VD, class G>
-__device__ __noinline__ double2 cslice_cplx(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
+__device__ __forceinline__ double2 cslice_cplx(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
                                             const G& g, int w, int len) {
   const int Q = w >> 2, PR = (w >> 1) & 1;
   double tr = 0.0, ti = 0.0;
@@ -851,7 +855,7 @@ __device__ __noinline__ double2 cslice_cplx(const SmemBlk& B, CSlice a, uint32_t
   return make_double2(tr, ti);
 }
 
-template <bool EXACT, bool FULL, bool VD, class G>
+template <bool EXACT, bool FULL, bool VD, bool LONG, class G>
 __device__ __forceinline__ double cslice_real(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row,
                                               uint32_t dict, const G& g, int w, int len) {
   switch (w) {
@@ -864,7 +868,13 @@ __device__ __forceinline__ double cslice_real(const SmemBlk& B, CSlice a, uint32
     case 7: return cslice_real_w<7, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
     case 8: return cslice_real_w<8, EXACT, FULL, VD>(B, a, lane, row, dict, g, len);
     case 0: return 0.0;
-    default: return cslice_real_long<EXACT, VD>(B, a, lane, row, dict, g, w, FULL ? w : len);
+    default:
+      // tiles without slices wider than 8 (tile_mode kModeLong clear) never get
+      // here, and their kernel body carries no long-row code
+      if constexpr (LONG)
+        return cslice_real_long<EXACT, VD>(B, a, lane, row, dict, g, w, FULL ? w : len);
+      else
+        return 0.0;
   }
 }
 
@@ -886,7 +896,8 @@ __device__ __forceinline__ double2 cslice_real_pair(const SmemBlk& B, CSlice a0,
 
 // One power step of one COMPRESSED tile (see tile_power for the contract).
 // LOCAL: the columns index the slot's staged x buffer (G = GatherSmem).
-template <bool CPLX, bool EXACT, bool GENERAL, bool VD, bool LOCAL = false, class G>
+// LONG: the tile has slices wider than 8 (long-row path compiled in).
+template <bool CPLX, bool EXACT, bool GENERAL, bool VD, bool LOCAL = false, bool LONG = false, class G>
 __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base, bool use_acc, const SmemBlk& B,
                                              const G& g, int32_t r0, int32_t nrows, uint32_t E, int32_t nd,
                                              int32_t nseg, int wid, int nwarps, uint32_t sched = kSchedStatic) {
@@ -926,8 +937,8 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
       const CSlice a = cslice<VD>(col_o, val_o, uint32_t(rec.x));
       const int w = rec.y & 0xffff;
       const int32_t row = LOCAL ? rb : rb + s * 32;
-      if (int(uint32_t(rec.y) >> 16) == w) return cslice_real<EXACT, true, VD>(B, a, lane, row, dict, g, w, w);
-      return cslice_real<EXACT, false, VD>(B, a, lane, row, dict, g, w, len_of(s, rec));
+      if (int(uint32_t(rec.y) >> 16) == w) return cslice_real<EXACT, true, VD, LONG>(B, a, lane, row, dict, g, w, w);
+      return cslice_real<EXACT, false, VD, LONG>(B, a, lane, row, dict, g, w, len_of(s, rec));
     };
     // slices s and s2 (dynamic grabs: s + 1; static: s + nwarps): a
     // same-width pair keeps both slices' gathers in flight.  One loop so the
@@ -960,7 +971,7 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
       }
     }
   } else {
-    for (int32_t s = sched_first(sched, wid, 1); s < ns; s = sched_next(sched, s, nwarps, 1)) {
+    for (int32_t s = sched_grab(sched, 1); s < ns; s = sched_grab(sched, 1)) {
       const int2 rec = B.i2(uint32_t(s) * 8);
       const CSlice a = cslice<VD>(col_o, val_o, uint32_t(rec.x));
       const int w = rec.y & 0xffff;
@@ -988,10 +999,49 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
   }
 }
 
+// Dispatch one compressed tile on its format bits (tile_mode): GENERAL
+// (Chebyshev / accumulation), dictionary or raw values, long rows.  Tiles
+// with slices wider than 8 run in a separate non-inlined body (tile_c_long):
+// inlining the long-row code into the walk kernels cost the W <= 8 path its
+// register allocation (cfg2 0.50 -> 0.58 ms).
+#define LMPK_TPC(GEN, VDV, LG) \
+  tile_power_c<CPLX, EXACT, GEN, VDV, LOCAL, LG>(pt, acc, use_acc, B, g, r0, rows, E, nd, nseg, warp, nw, sch)
+template <bool CPLX, bool EXACT, bool LOCAL, class G>
+__device__ __noinline__ void tile_c_long(int32_t tmode, const PowTab& pt, double* acc, bool use_acc, const SmemBlk B,
+                                         const G g, int32_t r0, int32_t rows, uint32_t E, int32_t nseg, int warp,
+                                         int nw, uint32_t sch) {
+  const int32_t nd = tmode >> 8;
+  const bool vd = (tmode & kModeDict) != 0;
+  if (pt.general) {
+    if (vd) LMPK_TPC(true, true, true); else LMPK_TPC(true, false, true);
+  } else {
+    if (vd) LMPK_TPC(false, true, true); else LMPK_TPC(false, false, true);
+  }
+}
+template <bool CPLX, bool EXACT, bool LOCAL, class G, bool HASLONG = true>
+__device__ __forceinline__ void tile_c_dispatch(int32_t tmode, const PowTab& pt, double* acc, bool use_acc,
+                                                const SmemBlk& B, const G& g, int32_t r0, int32_t rows, uint32_t E,
+                                                int32_t nseg, int warp, int nw, uint32_t sch) {
+  if constexpr (!CPLX && HASLONG) {
+    if (tmode & kModeLong) {
+      tile_c_long<CPLX, EXACT, LOCAL>(tmode, pt, acc, use_acc, B, g, r0, rows, E, nseg, warp, nw, sch);
+      return;
+    }
+  }
+  const int32_t nd = tmode >> 8;
+  const bool vd = (tmode & kModeDict) != 0;
+  if (pt.general) {
+    if (vd) LMPK_TPC(true, true, false); else LMPK_TPC(true, false, false);
+  } else {
+    if (vd) LMPK_TPC(false, true, false); else LMPK_TPC(false, false, false);
+  }
+}
+#undef LMPK_TPC
+
 // One power step of one tile (rows r0 .. r0+nrows-1, E block entries): warps
 // stride over the 32-row slices, lane = row.  GENERAL adds the Chebyshev
 // three-term step and the accumulation; plain SpMV powers skip both.
-template <bool CPLX, bool EXACT, bool GENERAL, class Blk, class G>
+template <bool CPLX, bool EXACT, bool GENERAL, class Blk, class G, bool LONG = true>
 __device__ __forceinline__ void tile_power(const PowTab& pt, double* acc_base, bool use_acc, const Blk& B,
                                            const G& g, int32_t r0, int32_t nrows, uint32_t E, int32_t nseg,
                                            int wid, int nwarps, bool pairs = true, uint32_t sched = kSchedStatic) {
@@ -1021,9 +1071,9 @@ __device__ __forceinline__ void tile_power(const PowTab& pt, double* acc_base, b
     auto single = [&](int32_t s, int2 rec) -> double {
       const uint32_t cb = uint32_t(rec.x), vb = 2 * cb + vdelta;
       const int w = rec.y & 0xffff;
-      if (int(uint32_t(rec.y) >> 16) == w) return slice_real<EXACT, true>(B, cb, vb, l4, g, w, w);
+      if (int(uint32_t(rec.y) >> 16) == w) return slice_real<EXACT, true, Blk, G, LONG>(B, cb, vb, l4, g, w, w);
       const int len = int(B.u16(lens_o + uint32_t(s) * 64 + (l4 >> 1)));
-      return slice_real<EXACT, false>(B, cb, vb, l4, g, w, len);
+      return slice_real<EXACT, false, Blk, G, LONG>(B, cb, vb, l4, g, w, len);
     };
     // warp `wid` owns slices wid, wid + nwarps, ...; it takes them two at a time
     for (int32_t s = sched_first(sched, wid, 2); s < ns; s = sched_next(sched, s, 2 * nwarps, 2)) {
@@ -1566,32 +1616,11 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
             if (P.xmode == 2) copy_x_segments<CPLX, NC>(B, pt, rows, nseg, xb, warp, lane);
             const GatherSmem G{xb};
             if constexpr (!CPLX) {
-            if (vd) {
-              if (pt.general)
-                tile_power_c<CPLX, EXACT, true, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
-              else
-                tile_power_c<CPLX, EXACT, false, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
-            } else {
-              if (pt.general)
-                tile_power_c<CPLX, EXACT, true, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
-              else
-                tile_power_c<CPLX, EXACT, false, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp,
-                                                              NC, sch);
-            }
+            tile_c_dispatch<CPLX, EXACT, true>(tmode, pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, sch);
             }
           } else {
-            const GatherGlobal G{pt.yin};
-            if (vd) {
-              if (pt.general)
-                tile_power_c<CPLX, EXACT, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-              else
-                tile_power_c<CPLX, EXACT, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-            } else {
-              if (pt.general)
-                tile_power_c<CPLX, EXACT, true, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-              else
-                tile_power_c<CPLX, EXACT, false, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-            }
+            tile_c_dispatch<CPLX, EXACT, false>(tmode, pt, P.acc, use_acc, B, GatherGlobal{pt.yin}, r0, rows, E, 0,
+                                                warp, NC, sch);
           }
         } else if (nseg > 0) {
           const uint32_t xb = sb + uint32_t(h_xoff[r]);
@@ -1682,7 +1711,9 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
 // started item never wait on anything but ring space, which the CTA's own
 // consumers free unconditionally.
 constexpr int kRingMax = 16;
-template <bool CPLX, bool EXACT, int NC>
+// HASLONG = false: the tiling has no slice wider than 8, and the kernel body
+// carries no long-row code at all (it cost the W <= 8 path its registers).
+template <bool CPLX, bool EXACT, int NC, bool HASLONG>
 __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P, PowerCfgDev C) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[kRingMax], empty_bar[kRingMax], done_bar[kRingMax];
@@ -1848,45 +1879,23 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
           const int32_t nd = tmode >> 8;
           if (tmode == 0) {
             if (pt.general)
-              tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
+              tile_power<CPLX, EXACT, true, SmemBlk, decltype(G), HASLONG>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
             else
-              tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
-          } else if (tmode & kModeDict) {
-            if (pt.general)
-              tile_power_c<CPLX, EXACT, true, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
-            else
-              tile_power_c<CPLX, EXACT, false, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
-          } else {
-            if (pt.general)
-              tile_power_c<CPLX, EXACT, true, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC, sch);
-            else
-              tile_power_c<CPLX, EXACT, false, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, nseg, warp, NC,
-                                                            sch);
-          }
+              tile_power<CPLX, EXACT, false, SmemBlk, decltype(G), HASLONG>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
+          } else tile_c_dispatch<CPLX, EXACT, true, GatherSmem, HASLONG>(tmode, pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, sch);
         }
       } else if (!d_glb[slot]) {
         const SmemBlk B{ring_base + uint32_t(slot) * uint32_t(P.smem_cap)};
         const GatherGlobal G{pt.yin};
         if (tmode != 0) {
-          const int32_t nd = tmode >> 8;
-          if (tmode & kModeDict) {
-            if (pt.general)
-              tile_power_c<CPLX, EXACT, true, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-            else
-              tile_power_c<CPLX, EXACT, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-          } else {
-            if (pt.general)
-              tile_power_c<CPLX, EXACT, true, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-            else
-              tile_power_c<CPLX, EXACT, false, false>(pt, P.acc, use_acc, B, G, r0, rows, E, nd, 0, warp, NC, sch);
-          }
+          tile_c_dispatch<CPLX, EXACT, false, GatherGlobal, HASLONG>(tmode, pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, sch);
         } else {
           if (pt.general)
-            tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, true, sch);
+            tile_power<CPLX, EXACT, true, SmemBlk, decltype(G), HASLONG>(pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, true, sch);
           else
-            tile_power<CPLX, EXACT, false>(pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, true, sch);
+            tile_power<CPLX, EXACT, false, SmemBlk, decltype(G), HASLONG>(pt, P.acc, use_acc, B, G, r0, rows, E, 0, warp, NC, true, sch);
         }
-      } else {
+      } else if constexpr (HASLONG) {  // oversize tiles exist only with slices far wider than 8
         tile_power<CPLX, EXACT, true>(pt, P.acc, use_acc, GlbBlk{P.blocks + d_ofs[slot]}, GatherGlobal{pt.yin}, r0,
                                       rows, E, 0, warp, NC, true, sch);
       }

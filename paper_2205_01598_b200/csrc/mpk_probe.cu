@@ -34,8 +34,12 @@ __global__ void k_probe_compute(MpkParams P, PowerCfgDev C, int iters, int n_til
   const uint32_t E = uint32_t(P.tile_E[t]);
   const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   const int32_t tmode = P.tile_mode ? P.tile_mode[t] : 0;
+  __shared__ uint32_t probe_ctr;
   for (int it = 0; it < iters; ++it) {
     if (tmode != 0) {
+      __syncthreads();
+      if (threadIdx.x == 0) probe_ctr = 0;
+      __syncthreads();
       // compressed tile: MODE 0 = the production row kernel, 1..3 = W=7 full
       // slices with the probe gather variants
       if (!staged) return;
@@ -45,9 +49,9 @@ __global__ void k_probe_compute(MpkParams P, PowerCfgDev C, int iters, int n_til
       const bool vd = (tmode & kModeDict) != 0;
       if constexpr (MODE == 0) {
         if (vd)
-          tile_power_c<false, EXACT, false, true>(s_pow[0], P.acc, false, B, G, r0, rows, E, nd, 0, wid, nw);
+          tile_power_c<false, EXACT, false, true>(s_pow[0], P.acc, false, B, G, r0, rows, E, nd, 0, wid, nw, smem_u32(&probe_ctr));
         else
-          tile_power_c<false, EXACT, false, false>(s_pow[0], P.acc, false, B, G, r0, rows, E, nd, 0, wid, nw);
+          tile_power_c<false, EXACT, false, false>(s_pow[0], P.acc, false, B, G, r0, rows, E, nd, 0, wid, nw, smem_u32(&probe_ctr));
       } else {
         const int32_t ns = (rows + 31) >> 5;
         const uint32_t dict = B.a + uint32_t(cblk_dict_off(ns, 0));

@@ -1,4 +1,4 @@
 export PYTHONDONTWRITEBYTECODE=1
-for c in cfg3 cfg5; do
-CASE=$c ncu --set full --clock-control none --import-source on -k regex:mpk_ring -s 2 -c 1 -f -o gpurun_out/prof_$c python tools/prof_cfg.py > gpurun_out/ncu_$c.log 2>&1; tail -1 gpurun_out/ncu_$c.log
-done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "passed|failed|Error" | tail -3
+SPECS='[[1,2,0,0,0,1,0,0,1,1],[1,2,0,100,0,1,0,0,1,1]]' timeout 300 python tools/bench_modes.py 2>&1 | tail -2
+timeout 900 python tools/configs_full.py 2>&1 | grep case | head -4
