@@ -250,3 +250,31 @@ def test_schedule_choice_bitwise(sched, monkeypatch):
     ap = pre.a
     ref = O.mpk_powers(ap.row_ptr, ap.col, ap.val, pre.perm.apply_to_vector(x), 4)
     assert np.array_equal(np.asarray(res.y.data), ref)
+
+
+def test_ring_oversize_slices_read_from_global():
+    """Rows of 40,000 entries make slices far larger than a ring piece: those
+    tiles stay plain and are read from global memory by the consumers
+    (the ring kernel's long-row variant); the rest are compressed."""
+    import torch
+
+    n, k = 50_000, 3
+    rng = np.random.default_rng(12)
+    i = np.arange(n)
+    rows, cols = [i, i[:-1], i[1:]], [i, i[1:], i[:-1]]
+    hubs = np.array([10, 20_000, 49_990])
+    for h in hubs:
+        nb = rng.choice(n, 40_000, replace=False)
+        rows += [np.full(nb.size, h), nb]
+        cols += [nb, np.full(nb.size, h)]
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    a = lm.CsrMatrix.from_triplets(n, r, c, rng.uniform(-1, 1, r.size) * 1e-3)
+    x = rng.uniform(-1, 1, n)
+    ref = O.mpk_powers(a.row_ptr, a.col, a.val, x, k)
+    t = K.Tiling(a.device(), k)
+    assert t.info["mode"] == 3 and 0 < t.info["compressed_tiles"] < t.info["n_tiles"]
+    y = torch.zeros((k + 1, n), dtype=torch.float64, device="cuda")
+    y[0] = torch.from_numpy(x)
+    K.mpk_run(t, y, K.mpk_power_cfg(k), exact=True)
+    assert np.array_equal(y.cpu().numpy(), ref)

@@ -1,4 +1,2 @@
 export PYTHONDONTWRITEBYTECODE=1
-timeout 900 python -m pytest tests/test_gpu_compress.py -x -q 2>&1 | grep -E "passed|failed" | tail -2
-SPECS='[[1,2,0,0,0,1,0,0,1,1]]' timeout 300 python tools/bench_modes.py 2>&1 | tail -1
-timeout 900 python tools/configs_full.py 2>&1 | grep case | head -5 | tail -3
+timeout 900 python -m pytest tests/test_gpu_compress.py -x -q -k "oversize or hub or schedule" 2>&1 | grep -E "passed|failed|Error|assert" | tail -5
