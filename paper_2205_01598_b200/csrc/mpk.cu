@@ -305,7 +305,7 @@ static int ring_occupancy(lmpk_ctx* ctx, int smem, int* occ) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes));
       int o = 0;
-      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * (kConsumers + 2), smem);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 32 * (kRingConsumers + 2), smem);
       if (e != cudaSuccess) {
         cudaGetLastError();
         set_error("occupancy query failed: %s", cudaGetErrorString(e));
@@ -1068,7 +1068,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   }
   T->info.p_m = p_m;
   T->info.mode = ring ? 3 : (q_used == p_m ? 1 : 2);
-  T->info.block = 32 * (kConsumers + (ring ? 2 : slots));
+  T->info.block = ring ? 32 * (kRingConsumers + 2) : 32 * (kConsumers + slots);
   T->ring = ring;
   T->piece = static_cast<int32_t>(cap_used);
   T->slots = slots;
@@ -1203,7 +1203,7 @@ static int launch_ring(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, 
       last[idx] = pct;
     }
   }
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (kConsumers + 2)), args, smem, st);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (kRingConsumers + 2)), args, smem, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("mpk ring launch failed: %s (grid %d, smem %d)", cudaGetErrorString(e), grid, smem);

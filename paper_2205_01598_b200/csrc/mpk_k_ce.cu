@@ -3,8 +3,8 @@
 
 namespace lmpk {
 const void* mpk_ring_fn_ce(bool has_long) {
-  return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<true, true, kConsumers, true>)
-                  : reinterpret_cast<const void*>(mpk_ring_kernel<true, true, kConsumers, false>);
+  return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<true, true, kRingConsumers, true>)
+                  : reinterpret_cast<const void*>(mpk_ring_kernel<true, true, kRingConsumers, false>);
 }
 const void* mpk_group_fn_ce() { return reinterpret_cast<const void*>(mpk_group_kernel<true, true, kConsumers>); }
 }  // namespace lmpk

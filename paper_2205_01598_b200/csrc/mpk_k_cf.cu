@@ -3,8 +3,8 @@
 
 namespace lmpk {
 const void* mpk_ring_fn_cf(bool has_long) {
-  return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<true, false, kConsumers, true>)
-                  : reinterpret_cast<const void*>(mpk_ring_kernel<true, false, kConsumers, false>);
+  return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<true, false, kRingConsumers, true>)
+                  : reinterpret_cast<const void*>(mpk_ring_kernel<true, false, kRingConsumers, false>);
 }
 const void* mpk_group_fn_cf() { return reinterpret_cast<const void*>(mpk_group_kernel<true, false, kConsumers>); }
 }  // namespace lmpk
