@@ -821,6 +821,26 @@ __device__ __forceinline__ double cslice_real_long(const SmemBlk& B, CSlice a, u
   return t;
 }
 
+// Complex vectors, width W <= 8: all W complex gathers in flight at once.
+template <int W, bool EXACT, bool VD, class G>
+__device__ __forceinline__ double2 cslice_cplx_w(const SmemBlk& B, CSlice a, uint32_t lane, int32_t row, uint32_t dict,
+                                                 const G& g, int len) {
+  int32_t c[W];
+  c16_offs<W>(B, a.cb, lane, c);
+  double2 x[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) x[j] = j < len ? g.d2(row + c[j]) : make_double2(0.0, 0.0);
+  double v[W];
+  c16_vals<W, VD>(B, a.vb, lane, dict, v);
+  double tr = 0.0, ti = 0.0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    tr = madd<EXACT>(tr, v[j], x[j].x);
+    ti = madd<EXACT>(ti, v[j], x[j].y);
+  }
+  return make_double2(tr, ti);
+}
+
 // Complex vectors (real matrix), any width: a quad at a time (4 complex
 // gathers in flight); storage order, re and im chains as the plain path.
 template <bool EXACT, bool VD, class G>
@@ -982,7 +1002,20 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
       const CSlice a = cslice<VD>(col_o, val_o, uint32_t(rec.x));
       const int w = rec.y & 0xffff;
       const int32_t lr = s * 32 + int32_t(lane);
-      double2 t = cslice_cplx<EXACT, VD>(B, a, lane, LOCAL ? rb : r0 + lr, dict, g, w, len_of(s, rec));
+      const int32_t crow = LOCAL ? rb : r0 + lr;
+      const int clen = len_of(s, rec);
+      double2 t;
+      switch (w) {  // W <= 8: every complex gather of the row in flight at once
+        case 1: t = cslice_cplx_w<1, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 2: t = cslice_cplx_w<2, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 3: t = cslice_cplx_w<3, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 4: t = cslice_cplx_w<4, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 5: t = cslice_cplx_w<5, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 6: t = cslice_cplx_w<6, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 7: t = cslice_cplx_w<7, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        case 8: t = cslice_cplx_w<8, EXACT, VD>(B, a, lane, crow, dict, g, clen); break;
+        default: t = cslice_cplx<EXACT, VD>(B, a, lane, crow, dict, g, w, clen);
+      }
       if (lr < nrows) {
         const int64_t r2 = 2 * int64_t(lr);
         if constexpr (GENERAL) {
