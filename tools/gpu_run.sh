@@ -1,3 +1,6 @@
 export PYTHONDONTWRITEBYTECODE=1
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "passed|failed" | tail -2
-python tools/prep_breakdown.py 2>&1 | head -2
+python -c 'import __graft_entry__ as g; g.smoke()' 2>&1 | tail -1
+timeout 600 python bench.py --steps 200 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
+bash tools/profile_round.sh > /dev/null 2>&1; echo prof done
