@@ -117,14 +117,16 @@ def _to_device_f64(arr):
 
 
 def _schedule(plan: ExecPlan, til, yv, cfg, av, use_acc, cplx, flags):
-    """Wavefront walk or per-power sweeps for this plan (same bits).  The walk
+    """Wavefront walk, per-power sweeps on the tiles, or (plain real MPK) the
+    CRS sweeps of run_baseline for this plan -- same bits.  The walk
     pays when the level window fits the L2 (cfg2, cfg5 shapes); for very wide
     levels (cfg3 27-point 160^3: 20 MB per level) the blocks are re-read from
     HBM at every power anyway and the dependency-free sweep is faster.  Chosen
     once per plan by timing one call of each on scratch copies; LMPK_SCHEDULE=
-    walk|sweep forces it."""
+    walk|sweep|crs forces it."""
     forced = os.environ.get("LMPK_SCHEDULE", "auto")
-    if forced in ("walk", "sweep"):
+    plain = not cplx and not use_acc and not np.any(plan.kernel != 0) and K.EXACT_DEFAULT
+    if forced in ("walk", "sweep") or (forced == "crs" and plain):
         return forced
     got = plan.schedule_choice(cplx)
     if got is not None:
@@ -136,12 +138,21 @@ def _schedule(plan: ExecPlan, til, yv, cfg, av, use_acc, cplx, flags):
     ys = yv.clone()
     as_ = av.clone() if av is not None else None
     times = {}
-    for name, f in (("walk", 0), ("sweep", _lib.FLAG_SWEEP)):
-        K.mpk_run(til, ys, cfg, acc=as_, use_acc=use_acc, complex_state=cplx, flags=flags | f, check_errors=False)
+    cands = [("walk", 0), ("sweep", _lib.FLAG_SWEEP)]
+    if plain:  # plain real MPK: the CRS sweeps of run_baseline are a candidate too (same bits, EXACT)
+        cands.append(("crs", None))
+    for name, f in cands:
+        def once():
+            if f is None:
+                K.mpk_baseline(plan.a.device(), ys, plan.p_m)
+            else:
+                K.mpk_run(til, ys, cfg, acc=as_, use_acc=use_acc, complex_state=cplx, flags=flags | f,
+                          check_errors=False)
+        once()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        K.mpk_run(til, ys, cfg, acc=as_, use_acc=use_acc, complex_state=cplx, flags=flags | f, check_errors=False)
+        once()
         e1.record()
         e1.synchronize()
         times[name] = e0.elapsed_time(e1)
@@ -180,8 +191,11 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
             K.mpk_baseline(plan.a.device(), yv, plan.p_m)
         else:
             sched = _schedule(plan, til, yv, cfg, av, use_acc, cplx, flags)
-            f = flags | (_lib.FLAG_SWEEP if sched == "sweep" else 0)
-            K.mpk_run(til, yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=f)
+            if sched == "crs":
+                K.mpk_baseline(plan.a.device(), yv, plan.p_m)
+            else:
+                f = flags | (_lib.FLAG_SWEEP if sched == "sweep" else 0)
+                K.mpk_run(til, yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=f)
     e1.record()
     e1.synchronize()
     ctx = _lib.context()

@@ -240,7 +240,7 @@ def test_hub_rows_fall_back_to_crs_sweeps():
     assert np.array_equal(np.asarray(res.y.data), ref)
 
 
-@pytest.mark.parametrize("sched", ["walk", "sweep", "auto"])
+@pytest.mark.parametrize("sched", ["walk", "sweep", "crs", "auto"])
 def test_schedule_choice_bitwise(sched, monkeypatch):
     """The executor's walk / sweep choice (LMPK_SCHEDULE) never changes the bits."""
     monkeypatch.setenv("LMPK_SCHEDULE", sched)
