@@ -73,6 +73,7 @@ struct lmpk_ctx {
   uint32_t epoch = 0;
   // scratch pools
   lmpk::Scratch s_small, s_a, s_b, s_c, s_d, s_e, s_f, s_g;
+  lmpk::Scratch s_heavy;  // CRS kernel: list of heavy rows (count + indices)
   uint64_t* queue_ctr = nullptr;  // monotone work-queue counter (device)
   uint64_t queue_base = 0;        // host mirror of the counter value
   unsigned long long* prof = nullptr;  // phase counters when LMPK_PROFILE is set

@@ -10,10 +10,13 @@
 
 namespace lmpk {
 
-// One thread per row, grid-stride over [r0, r1).  No shared memory: the
-// whole unified L1 caches the row's col/val lines (a warp's 32 consecutive
-// rows share them across the 7-ish entry loads) and the gathered x lines.
-// The matrix and x are immutable during a launch, so the .nc path is safe.
+// One thread per light row (<= kHeavy entries), grid-stride over [r0, r1),
+// summed in storage order with unfused multiply/add (bitwise the numba
+// kernel).  No shared memory: the unified L1 caches the rows' col/val lines
+// and the gathered x lines.  The matrix and x are immutable during a launch,
+// so the .nc path is safe.  Heavy rows are skipped here and summed by
+// spmv_heavy_kernel.
+constexpr int kHeavy = 128;
 __global__ void __launch_bounds__(256) spmv_rows_kernel(const int32_t* __restrict__ row_ptr,
                                                         const int32_t* __restrict__ col,
                                                         const double* __restrict__ val,
@@ -22,20 +25,73 @@ __global__ void __launch_bounds__(256) spmv_rows_kernel(const int32_t* __restric
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t r = r0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < r1; r += stride) {
     const int32_t k0 = __ldg(row_ptr + r), k1 = __ldg(row_ptr + r + 1);
-    out[r] = row_sum_exact(col + k0, val + k0, k1 - k0, [x](int c) { return __ldg(x + c); });
+    if (k1 - k0 <= kHeavy)
+      out[r] = row_sum_exact(col + k0, val + k0, k1 - k0, [x](int c) { return __ldg(x + c); });
+  }
+}
+
+// Rows longer than kHeavy (power-law hubs: cfg4's largest has 97,280
+// entries) in [r0, r1), compacted once per call: list[0] = count.
+__global__ void k_heavy_rows(const int32_t* __restrict__ row_ptr, int32_t r0, int32_t r1, int32_t* list) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t r = r0 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < r1; r += stride)
+    if (__ldg(row_ptr + r + 1) - __ldg(row_ptr + r) > kHeavy) list[1 + atomicAdd(list, 1)] = int32_t(r);
+}
+
+// One warp per heavy row: the warp loads 32 entries at a time (coalesced)
+// and forms the 32 products in parallel -- each the same rounded double as
+// the sequential kernel's -- then every lane adds them in storage order from
+// shuffles: bitwise the sequential sum, with the row's loads no longer one
+// entry at a time and the hubs spread over all warps of the grid.
+__global__ void __launch_bounds__(256) spmv_heavy_kernel(const int32_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x, double* __restrict__ out,
+                                                         const int32_t* __restrict__ list) {
+  const int lane = threadIdx.x & 31;
+  const int32_t nh = __ldg(list);
+  const int32_t nw = int32_t((int64_t(gridDim.x) * blockDim.x) >> 5);
+  for (int32_t i = int32_t((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5); i < nh; i += nw) {
+    const int32_t r = __ldg(list + 1 + i);
+    const int32_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
+    double t = 0.0;
+    for (int32_t e = a; e < b; e += 32) {
+      const int n = min(32, b - e);
+      double m = 0.0;
+      if (lane < n) m = __dmul_rn(__ldg(val + e + lane), __ldg(x + __ldg(col + e + lane)));
+      for (int j = 0; j < n; ++j) t = __dadd_rn(t, __shfl_sync(0xffffffffu, m, j));
+    }
+    if (lane == 0) out[r] = t;
   }
 }
 
 static int spmv_launch(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col, const double* val,
-                       const double* x, double* out, int32_t r0, int32_t r1, cudaStream_t st) {
+                       const double* x, double* out, int32_t r0, int32_t r1, const int32_t* heavy,
+                       cudaStream_t st) {
   if (r1 <= r0) return LMPK_OK;
   const int threads = 256;
   const int64_t blocks = (int64_t(r1) - r0 + threads - 1) / threads;
   // enough CTAs for full occupancy (8 x 256 threads per SM), grid-stride beyond
   const int grid = static_cast<int>(std::min<int64_t>(blocks, int64_t(ctx->sm_count) * 8));
   spmv_rows_kernel<<<grid, threads, 0, st>>>(row_ptr, col, val, x, out, r0, r1);
+  spmv_heavy_kernel<<<ctx->sm_count * 8, threads, 0, st>>>(row_ptr, col, val, x, out, heavy);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 2);
+  return LMPK_OK;
+}
+
+// heavy-row list of [r0, r1) in the ctx scratch (count, then row indices)
+static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t r1, int32_t** out,
+                      cudaStream_t st) {
+  LMPK_TRY(ctx->s_heavy.ensure((size_t(r1 - r0) + 1) * 4));
+  int32_t* list = reinterpret_cast<int32_t*>(ctx->s_heavy.ptr);
+  LMPK_CHECK_CUDA(cudaMemsetAsync(list, 0, 4, st));
+  const int64_t blocks = (int64_t(r1) - r0 + 255) / 256;
+  k_heavy_rows<<<static_cast<int>(std::min<int64_t>(blocks, int64_t(ctx->sm_count) * 8)), 256, 0, st>>>(row_ptr, r0,
+                                                                                                          r1, list);
   LMPK_CHECK_CUDA(cudaGetLastError());
   launch_count_add(ctx, 1);
+  *out = list;
   return LMPK_OK;
 }
 
@@ -52,7 +108,10 @@ extern "C" int lmpk_spmv_rows(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, 
   LMPK_ARG_CHECK(x != out, "in_vec and out_vec must not alias");
   (void)flags;
   if (r1 == r0) return LMPK_OK;
-  return spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  int32_t* heavy = nullptr;
+  LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, st));
+  return spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, st);
 }
 
 extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr,
@@ -64,7 +123,9 @@ extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_pt
   if (n == 0) return LMPK_OK;
   (void)flags;
   cudaStream_t st = as_stream(stream);
+  int32_t* heavy = nullptr;
+  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, st));
   for (int32_t p = 1; p <= p_m; ++p)
-    LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, st));
+    LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy, st));
   return LMPK_OK;
 }

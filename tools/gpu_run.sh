@@ -1,3 +1,5 @@
 export PYTHONDONTWRITEBYTECODE=1
-timeout 900 python -m pytest tests/test_gpu_compress.py -q -x 2>&1 | grep -E "passed|failed" | tail -2
-SPECS='[[1,2,0,0,0,1,0,0,1,1],[1,2,0,0,0,1,0,0,1,1],[1,3,0,0,0,1,0,0,1,1]]' timeout 300 python tools/bench_modes.py 2>&1 | tail -3
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "passed|failed" | tail -2
+python tools/prof_cfg4.py 2>&1 | tail -2
+SCALE=22 timeout 1500 python tools/cfg4_run.py 2>&1 | tail -1
+timeout 600 python tools/configs_full.py 2>&1 | grep case | head -2
