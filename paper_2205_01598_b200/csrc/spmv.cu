@@ -59,7 +59,15 @@ __global__ void __launch_bounds__(256) spmv_heavy_kernel(const int32_t* __restri
       const int n = min(32, b - e);
       double m = 0.0;
       if (lane < n) m = __dmul_rn(__ldg(val + e + lane), __ldg(x + __ldg(col + e + lane)));
-      for (int j = 0; j < n; ++j) t = __dadd_rn(t, __shfl_sync(0xffffffffu, m, j));
+      if (n == 32) {
+        double ms[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ms[j] = __shfl_sync(0xffffffffu, m, j);  // shuffles off the add chain
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t = __dadd_rn(t, ms[j]);
+      } else {
+        for (int j = 0; j < n; ++j) t = __dadd_rn(t, __shfl_sync(0xffffffffu, m, j));
+      }
     }
     if (lane == 0) out[r] = t;
   }
