@@ -75,22 +75,27 @@ __global__ void __launch_bounds__(256) spmv_heavy_kernel(const int32_t* __restri
 
 static int spmv_launch(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col, const double* val,
                        const double* x, double* out, int32_t r0, int32_t r1, const int32_t* heavy,
-                       cudaStream_t st) {
+                       int32_t n_heavy, cudaStream_t st) {
   if (r1 <= r0) return LMPK_OK;
   const int threads = 256;
   const int64_t blocks = (int64_t(r1) - r0 + threads - 1) / threads;
   // enough CTAs for full occupancy (8 x 256 threads per SM), grid-stride beyond
   const int grid = static_cast<int>(std::min<int64_t>(blocks, int64_t(ctx->sm_count) * 8));
   spmv_rows_kernel<<<grid, threads, 0, st>>>(row_ptr, col, val, x, out, r0, r1);
-  spmv_heavy_kernel<<<ctx->sm_count * 8, threads, 0, st>>>(row_ptr, col, val, x, out, heavy);
+  launch_count_add(ctx, 1);
+  if (n_heavy > 0) {  // no second launch for matrices without hub rows
+    const int hgrid = static_cast<int>(std::min<int64_t>((int64_t(n_heavy) * 32 + threads - 1) / threads,
+                                                         int64_t(ctx->sm_count) * 8));
+    spmv_heavy_kernel<<<hgrid, threads, 0, st>>>(row_ptr, col, val, x, out, heavy);
+    launch_count_add(ctx, 1);
+  }
   LMPK_CHECK_CUDA(cudaGetLastError());
-  launch_count_add(ctx, 2);
   return LMPK_OK;
 }
 
 // heavy-row list of [r0, r1) in the ctx scratch (count, then row indices)
 static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t r1, int32_t** out,
-                      cudaStream_t st) {
+                      int32_t* n_heavy, cudaStream_t st) {
   LMPK_TRY(ctx->s_heavy.ensure((size_t(r1 - r0) + 1) * 4));
   int32_t* list = reinterpret_cast<int32_t*>(ctx->s_heavy.ptr);
   LMPK_CHECK_CUDA(cudaMemsetAsync(list, 0, 4, st));
@@ -99,6 +104,8 @@ static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t
                                                                                                           r1, list);
   LMPK_CHECK_CUDA(cudaGetLastError());
   launch_count_add(ctx, 1);
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(n_heavy, list, 4, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));  // once per call: decides the heavy-row launches
   *out = list;
   return LMPK_OK;
 }
@@ -118,8 +125,9 @@ extern "C" int lmpk_spmv_rows(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, 
   if (r1 == r0) return LMPK_OK;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
-  LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, st));
-  return spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, st);
+  int32_t n_heavy = 0;
+  LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, &n_heavy, st));
+  return spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, n_heavy, st);
 }
 
 extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr,
@@ -132,8 +140,10 @@ extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_pt
   (void)flags;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
-  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, st));
+  int32_t n_heavy = 0;
+  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_heavy, st));
   for (int32_t p = 1; p <= p_m; ++p)
-    LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy, st));
+    LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy,
+                         n_heavy, st));
   return LMPK_OK;
 }
