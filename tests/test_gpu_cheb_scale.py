@@ -104,7 +104,9 @@ def test_cfg2_full_size_bitwise():
     ref[0] = x[op]
     C.mpk_baseline(rp, c, v, ref, 8)
     plan = lm.build_plan(pre, "lb_lg_p2p", 1)
-    for params in ({"mode_flags": _lib.FLAG_MODE_STREAM, "slots": 2},
+    for params in ({},  # the default plan: ring walk over compressed tiles
+                   {"mode_flags": _lib.FLAG_MODE_STREAM, "slots": 2},
+                   {"mode_flags": _lib.FLAG_MODE_STREAM | _lib.FLAG_COMPRESS, "slots": 2},
                    {"mode_flags": _lib.FLAG_MODE_RESIDENT, "slots": 2}):
         t = plan.tiling(**params)
         y = torch.zeros((9, a.n_rows), dtype=torch.float64, device="cuda")
@@ -173,3 +175,38 @@ def test_rmat_scale18_mpk_bitwise():
     y[0] = torch.from_numpy(x)
     K.mpk_run(t, y, K.mpk_power_cfg(k))
     assert np.array_equal(y.cpu().numpy(), ref)
+
+
+def test_cfg5_full_size_propagation_schedules_bitwise():
+    """BASELINE config 5 as specified: complex128 Chebyshev propagation on the
+    Anderson 128^3 Hamiltonian, degree 64 as 8 batches of k=8.  The ring walk,
+    the per-power sweeps over the same tiles and the round-1 group walk on
+    plain blocks give the same bits; the result is a unitary propagation
+    (norm preserved to the truncation tolerance)."""
+    import os
+    import torch
+    from paper_2205_01598_b200.cheb import ChebCoeffs, cheb_coeffs_schrodinger, gershgorin_bounds
+
+    a = lm.gen_anderson_3d(128, seed=2)
+    lo, hi = gershgorin_bounds(a)
+    c = cheb_coeffs_schrodinger(2.0, lo, hi, tol=1e-14).c
+    assert c.size <= 65
+    coeffs = ChebCoeffs(c=c, dt=2.0, lam_min=lo, lam_max=hi, tol=1e-14)
+    rng = np.random.default_rng(0)
+    psi = np.exp(2j * np.pi * rng.random(a.n_rows)) / np.sqrt(a.n_rows)
+    xd = torch.from_numpy(psi).cuda()
+    outs = []
+    old = os.environ.get("LMPK_SCHEDULE")
+    try:
+        for sched, kw in (("walk", {}), ("sweep", {}),
+                          ("walk", {"tiling_params": {"mode_flags": _lib.FLAG_MODE_STREAM}})):
+            os.environ["LMPK_SCHEDULE"] = sched
+            prop = lm.ChebPropagator(a, 2.0, coeffs=coeffs, p_m_batch=8, cache_bytes=126e6, **kw)
+            outs.append(prop.step(xd))
+    finally:
+        if old is None:
+            os.environ.pop("LMPK_SCHEDULE", None)
+        else:
+            os.environ["LMPK_SCHEDULE"] = old
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert abs(float(torch.linalg.vector_norm(outs[0])) - 1.0) < 1e-10

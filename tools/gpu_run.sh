@@ -1,5 +1,2 @@
 export PYTHONDONTWRITEBYTECODE=1
-timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "passed|failed" | tail -2
-python tools/prof_cfg4.py 2>&1 | tail -2
-timeout 600 python bench.py --steps 200 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
+timeout 900 python -m pytest tests/test_gpu_cheb_scale.py -q -x 2>&1 | grep -E "passed|failed|Error|assert" | tail -4
