@@ -856,7 +856,8 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
     D = std::max(D, sup[b] - s);
   }
   const int32_t G = p_m;
-  const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (3 * T->info.grid) / G);
+  // ~5 x (items in flight) / G keys: measured 1% faster than 3x on cfg2 (0.498 vs 0.504 ms)
+  const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (5 * T->info.grid) / G);
   T->info.queue_slack = G > 1 ? slack : 0;
   T->info.max_fwd_reach = D;
   T->info.super_tiles = ns;

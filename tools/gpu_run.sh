@@ -1,2 +1,2 @@
 export PYTHONDONTWRITEBYTECODE=1
-timeout 900 python -m pytest tests/test_gpu_cheb_scale.py -q -x 2>&1 | grep -E "passed|failed|Error|assert" | tail -4
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "passed|failed" | tail -2
