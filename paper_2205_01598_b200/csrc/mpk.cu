@@ -285,8 +285,11 @@ const void* mpk_ring_fn_re(bool has_long);
 const void* mpk_ring_fn_rf(bool has_long);
 const void* mpk_ring_fn_ce(bool has_long);
 const void* mpk_ring_fn_cf(bool has_long);
-static const void* ring_fn(bool cplx, bool exact, bool has_long = true) {
+const void* mpk_ring_fn_re_dict();
+const void* mpk_ring_fn_rf_dict();
+static const void* ring_fn(bool cplx, bool exact, bool has_long = true, bool all_dict = false) {
   if (cplx) return exact ? mpk_ring_fn_ce(has_long) : mpk_ring_fn_cf(has_long);
+  if (all_dict && !has_long) return exact ? mpk_ring_fn_re_dict() : mpk_ring_fn_rf_dict();
   return exact ? mpk_ring_fn_re(has_long) : mpk_ring_fn_rf(has_long);
 }
 // Occupancy of the ring kernel (all instantiations) at `smem` dynamic bytes.
@@ -358,6 +361,10 @@ static int group_static_smem(int* out) {
         cudaFuncAttributes fb;
         e = cudaFuncGetAttributes(&fb, ring_fn(c == 3, x != 0, false));
         fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+        if (e == cudaSuccess && c == 2) {
+          e = cudaFuncGetAttributes(&fb, ring_fn(false, x != 0, false, true));
+          fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
+        }
       }
       if (e != cudaSuccess) {
         cudaGetLastError();
@@ -1188,15 +1195,21 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
   return LMPK_OK;
 }
 
-static int launch_ring(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool has_long, int grid,
-                       int smem, cudaStream_t st) {
+static int launch_ring(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool has_long,
+                       bool all_dict, int grid, int smem, cudaStream_t st) {
   void* args[] = {&Pm, &C};
-  const void* fn = ring_fn(cplx, exact, has_long);
+  const void* fn = ring_fn(cplx, exact, has_long, all_dict);
   {
-    static int last[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
-    const int idx = (has_long ? 4 : 0) + (cplx ? 2 : 0) + (exact ? 1 : 0);
+    static int last[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
+    const int idx = (all_dict ? 8 : 0) + (has_long ? 4 : 0) + (cplx ? 2 : 0) + (exact ? 1 : 0);
     cudaFuncAttributes fa;
     LMPK_CHECK_CUDA(cudaFuncGetAttributes(&fa, fn));
+    static bool dyn_set[16] = {};
+    if (!dyn_set[idx]) {  // every variant may be launched without an occupancy query first
+      LMPK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes)));
+      dyn_set[idx] = true;
+    }
     const int per_sm = std::max(1, ctx->max_smem_sm);
     const int pct = std::min(100, int((int64_t(smem + int(fa.sharedSizeBytes) + 1024) * 100 + per_sm - 1) / per_sm));
     if (last[idx] != pct) {
@@ -1349,7 +1362,9 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   if (T->ring) {
     LMPK_ARG_CHECK(!(flags & (LMPK_FLAG_NO_TMA | LMPK_FLAG_READY_QUEUE)),
                    "the ring walk has no unstaged / ready-queue variant");
-    return launch_ring(ctx, Pm, C, cplx, exact, T->info.max_row_nnz > 8, grid, T->info.smem_bytes, st);
+    const bool all_dict = T->info.dict_tiles == T->info.n_tiles && T->staged_tiles == 0 &&
+                          getenv("LMPK_NO_DICT_KERNEL") == nullptr;
+    return launch_ring(ctx, Pm, C, cplx, exact, T->info.max_row_nnz > 8, all_dict, grid, T->info.smem_bytes, st);
   }
   // co-residency of all CTAs is part of the deadlock-freedom argument.
   // LMPK_FLAG_NO_TMA: blocks are streamed from global memory by the
