@@ -285,11 +285,17 @@ const void* mpk_ring_fn_re(bool has_long);
 const void* mpk_ring_fn_rf(bool has_long);
 const void* mpk_ring_fn_ce(bool has_long);
 const void* mpk_ring_fn_cf(bool has_long);
-const void* mpk_ring_fn_re_dict();
-const void* mpk_ring_fn_rf_dict();
-static const void* ring_fn(bool cplx, bool exact, bool has_long = true, bool all_dict = false) {
+const void* mpk_ring_fn_re_uniform(int u);
+const void* mpk_ring_fn_rf_uniform(int u);
+const void* mpk_ring_fn_ce_uniform(int u);
+const void* mpk_ring_fn_cf_uniform(int u);
+// uniform: 0 general kernel, 1 all tiles dictionary (w <= 8), 2 all tiles raw compressed (w <= 8)
+static const void* ring_fn(bool cplx, bool exact, bool has_long = true, int uniform = 0) {
+  if (uniform && !has_long) {
+    if (cplx) return exact ? mpk_ring_fn_ce_uniform(uniform) : mpk_ring_fn_cf_uniform(uniform);
+    return exact ? mpk_ring_fn_re_uniform(uniform) : mpk_ring_fn_rf_uniform(uniform);
+  }
   if (cplx) return exact ? mpk_ring_fn_ce(has_long) : mpk_ring_fn_cf(has_long);
-  if (all_dict && !has_long) return exact ? mpk_ring_fn_re_dict() : mpk_ring_fn_rf_dict();
   return exact ? mpk_ring_fn_re(has_long) : mpk_ring_fn_rf(has_long);
 }
 // Occupancy of the ring kernel (all instantiations) at `smem` dynamic bytes.
@@ -361,8 +367,8 @@ static int group_static_smem(int* out) {
         cudaFuncAttributes fb;
         e = cudaFuncGetAttributes(&fb, ring_fn(c == 3, x != 0, false));
         fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
-        if (e == cudaSuccess && c == 2) {
-          e = cudaFuncGetAttributes(&fb, ring_fn(false, x != 0, false, true));
+        for (int u = 1; u <= 2 && e == cudaSuccess; ++u) {
+          e = cudaFuncGetAttributes(&fb, ring_fn(c == 3, x != 0, false, u));
           fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
         }
       }
@@ -1196,15 +1202,20 @@ static int launch_group(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx,
 }
 
 static int launch_ring(lmpk_ctx* ctx, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool has_long,
-                       bool all_dict, int grid, int smem, cudaStream_t st) {
+                       int uniform, int grid, int smem, cudaStream_t st) {
   void* args[] = {&Pm, &C};
-  const void* fn = ring_fn(cplx, exact, has_long, all_dict);
+  const void* fn = ring_fn(cplx, exact, has_long, uniform);
   {
-    static int last[16] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
-    const int idx = (all_dict ? 8 : 0) + (has_long ? 4 : 0) + (cplx ? 2 : 0) + (exact ? 1 : 0);
+    static int last[32];
+    static bool init = false;
+    if (!init) {
+      for (int& v : last) v = -1;
+      init = true;
+    }
+    const int idx = uniform * 8 + (has_long ? 4 : 0) + (cplx ? 2 : 0) + (exact ? 1 : 0);
     cudaFuncAttributes fa;
     LMPK_CHECK_CUDA(cudaFuncGetAttributes(&fa, fn));
-    static bool dyn_set[16] = {};
+    static bool dyn_set[32] = {};
     if (!dyn_set[idx]) {  // every variant may be launched without an occupancy query first
       LMPK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            ctx->max_smem_block - static_cast<int>(fa.sharedSizeBytes)));
@@ -1362,9 +1373,15 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   if (T->ring) {
     LMPK_ARG_CHECK(!(flags & (LMPK_FLAG_NO_TMA | LMPK_FLAG_READY_QUEUE)),
                    "the ring walk has no unstaged / ready-queue variant");
-    const bool all_dict = T->info.dict_tiles == T->info.n_tiles && T->staged_tiles == 0 &&
-                          getenv("LMPK_NO_DICT_KERNEL") == nullptr;
-    return launch_ring(ctx, Pm, C, cplx, exact, T->info.max_row_nnz > 8, all_dict, grid, T->info.smem_bytes, st);
+    // a kernel carrying one tile body when every tile has the same format
+    int uniform = 0;
+    if (T->staged_tiles == 0 && getenv("LMPK_NO_UNIFORM_KERNEL") == nullptr) {
+      if (T->info.dict_tiles == T->info.n_tiles)
+        uniform = 1;
+      else if (T->info.compressed_tiles == T->info.n_tiles && T->info.dict_tiles == 0)
+        uniform = 2;
+    }
+    return launch_ring(ctx, Pm, C, cplx, exact, T->info.max_row_nnz > 8, uniform, grid, T->info.smem_bytes, st);
   }
   // co-residency of all CTAs is part of the deadlock-freedom argument.
   // LMPK_FLAG_NO_TMA: blocks are streamed from global memory by the

@@ -6,6 +6,9 @@ const void* mpk_ring_fn_re(bool has_long) {
   return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, true>)
                   : reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false>);
 }
-const void* mpk_ring_fn_re_dict() { return reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false, true>); }
+const void* mpk_ring_fn_re_uniform(int u) {
+  return u == 1 ? reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false, 1>)
+                : reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false, 2>);
+}
 const void* mpk_group_fn_re() { return reinterpret_cast<const void*>(mpk_group_kernel<false, true, kConsumers>); }
 }  // namespace lmpk

@@ -6,6 +6,9 @@ const void* mpk_ring_fn_rf(bool has_long) {
   return has_long ? reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kRingConsumers, true>)
                   : reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kRingConsumers, false>);
 }
-const void* mpk_ring_fn_rf_dict() { return reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kRingConsumers, false, true>); }
+const void* mpk_ring_fn_rf_uniform(int u) {
+  return u == 1 ? reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kRingConsumers, false, 1>)
+                : reinterpret_cast<const void*>(mpk_ring_kernel<false, false, kRingConsumers, false, 2>);
+}
 const void* mpk_group_fn_rf() { return reinterpret_cast<const void*>(mpk_group_kernel<false, false, kConsumers>); }
 }  // namespace lmpk
