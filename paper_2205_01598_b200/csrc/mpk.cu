@@ -367,7 +367,7 @@ static int group_static_smem(int* out) {
         cudaFuncAttributes fb;
         e = cudaFuncGetAttributes(&fb, ring_fn(c == 3, x != 0, false));
         fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
-        for (int u = 1; u <= 2 && e == cudaSuccess; ++u) {
+        for (int u = 1; u <= (c == 3 ? 2 : 3) && e == cudaSuccess; ++u) {
           e = cudaFuncGetAttributes(&fb, ring_fn(c == 3, x != 0, false, u));
           fa.sharedSizeBytes = std::max(fa.sharedSizeBytes, fb.sharedSizeBytes);
         }
@@ -1376,8 +1376,10 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
     // a kernel carrying one tile body when every tile has the same format
     int uniform = 0;
     if (T->staged_tiles == 0 && getenv("LMPK_NO_UNIFORM_KERNEL") == nullptr) {
+      bool plain = !use_acc;
+      for (int i = 0; i < P; ++i) plain = plain && C.kernel[i] == LMPK_KERNEL_SPMV;
       if (T->info.dict_tiles == T->info.n_tiles)
-        uniform = 1;
+        uniform = (plain && !cplx) ? 3 : 1;
       else if (T->info.compressed_tiles == T->info.n_tiles && T->info.dict_tiles == 0)
         uniform = 2;
     }

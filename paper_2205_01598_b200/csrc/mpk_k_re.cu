@@ -7,6 +7,7 @@ const void* mpk_ring_fn_re(bool has_long) {
                   : reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false>);
 }
 const void* mpk_ring_fn_re_uniform(int u) {
+  if (u == 3) return reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false, 3>);
   return u == 1 ? reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false, 1>)
                 : reinterpret_cast<const void*>(mpk_ring_kernel<false, true, kRingConsumers, false, 2>);
 }

@@ -1756,6 +1756,7 @@ constexpr int kRingMax = 16;
 // width <= 8 without x-staging (cfg2: dictionary; cfg5: raw): the consumers
 // carry only that one tile body, which measured 3% faster on cfg2 than the
 // general kernel (better register allocation of the hot loop).
+// UNIFORM = 3: as 1, for plain powers only (no Chebyshev step, no accumulation).
 template <bool CPLX, bool EXACT, int NC, bool HASLONG, int UNIFORM = 0>
 __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P, PowerCfgDev C) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1915,8 +1916,10 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
       if constexpr (UNIFORM != 0) {
         const SmemBlk B{ring_base + uint32_t(slot) * uint32_t(P.smem_cap)};
         const GatherGlobal G{pt.yin};
-        constexpr bool VDU = UNIFORM == 1;
-        if (pt.general)
+        constexpr bool VDU = UNIFORM != 2;
+        if constexpr (UNIFORM == 3)
+          tile_power_c<CPLX, EXACT, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, tmode >> 8, 0, warp, NC, sch);
+        else if (pt.general)
           tile_power_c<CPLX, EXACT, true, VDU>(pt, P.acc, use_acc, B, G, r0, rows, E, tmode >> 8, 0, warp, NC, sch);
         else
           tile_power_c<CPLX, EXACT, false, VDU>(pt, P.acc, use_acc, B, G, r0, rows, E, tmode >> 8, 0, warp, NC, sch);
