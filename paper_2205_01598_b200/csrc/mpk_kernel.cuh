@@ -923,7 +923,8 @@ __device__ __forceinline__ double2 cslice_real_pair(const SmemBlk& B, CSlice a0,
 // One power step of one COMPRESSED tile (see tile_power for the contract).
 // LOCAL: the columns index the slot's staged x buffer (G = GatherSmem).
 // LONG: the tile has slices wider than 8 (long-row path compiled in).
-template <bool CPLX, bool EXACT, bool GENERAL, bool VD, bool LOCAL = false, bool LONG = false, class G>
+template <bool CPLX, bool EXACT, bool GENERAL, bool VD, bool LOCAL = false, bool LONG = false, bool DYN = false,
+          class G>
 __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base, bool use_acc, const SmemBlk& B,
                                              const G& g, int32_t r0, int32_t nrows, uint32_t E, int32_t nd,
                                              int32_t nseg, int wid, int nwarps, uint32_t sched = kSchedStatic) {
@@ -969,7 +970,7 @@ __device__ __forceinline__ void tile_power_c(const PowTab& pt, double* acc_base,
     // slices s and s2 (dynamic grabs: s + 1; static: s + nwarps): a
     // same-width pair keeps both slices' gathers in flight.  One loop so the
     // body is inlined once (two call sites made ptxas outline it to a stack frame).
-    const bool dyn = sched != kSchedStatic;
+    const bool dyn = DYN || sched != kSchedStatic;  // DYN: the caller always provides a counter
     for (int32_t s = dyn ? sched_grab(sched, 2) : wid; s < ns; s = dyn ? sched_grab(sched, 2) : s + 2 * nwarps) {
       const int32_t s2 = dyn ? s + 1 : s + nwarps;
       const int2 rec0 = B.i2(uint32_t(s) * 8);
@@ -1918,7 +1919,8 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
         const GatherGlobal G{pt.yin};
         constexpr bool VDU = UNIFORM != 2;
         if constexpr (UNIFORM == 3)
-          tile_power_c<CPLX, EXACT, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E, tmode >> 8, 0, warp, NC, sch);
+          tile_power_c<CPLX, EXACT, false, true, false, false, true>(pt, P.acc, use_acc, B, G, r0, rows, E,
+                                                                      tmode >> 8, 0, warp, NC, smem_u32(&d_ctr[slot]));
         else if (pt.general)
           tile_power_c<CPLX, EXACT, true, VDU>(pt, P.acc, use_acc, B, G, r0, rows, E, tmode >> 8, 0, warp, NC, sch);
         else
