@@ -1649,8 +1649,6 @@ __global__ void __launch_bounds__(32 * (NC + kMaxSlots), 1) mpk_group_kernel(Mpk
         const SmemBlk B{sb};
         const bool pairs = (P.flags & 0x800) == 0;  // internal A/B switch
         if (tmode != 0) {
-          const int32_t nd = tmode >> 8;
-          const bool vd = (tmode & kModeDict) != 0;
           if (!CPLX && nseg > 0) {  // x staging is planned for real-vector tilings only
             const uint32_t xb = sb + uint32_t(h_xoff[r]);
             if (P.xmode == 2) copy_x_segments<CPLX, NC>(B, pt, rows, nseg, xb, warp, lane);
@@ -1932,7 +1930,6 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
         if (P.xmode == 2) copy_x_segments<CPLX, NC>(B, pt, rows, nseg, xb, warp, lane);
         const GatherSmem G{xb};
         if constexpr (!CPLX) {
-          const int32_t nd = tmode >> 8;
           if (tmode == 0) {
             if (pt.general)
               tile_power<CPLX, EXACT, true, SmemBlk, decltype(G), HASLONG>(pt, P.acc, use_acc, B, G, r0, rows, E, nseg, warp, NC, true, sch);
