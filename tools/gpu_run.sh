@@ -1,4 +1,3 @@
 export PYTHONDONTWRITEBYTECODE=1
-for lib in liblmpk liblmpk_p28 liblmpk_p30; do echo "== $lib"
-LMPK_LIB=$PWD/paper_2205_01598_b200/_lib/$lib.so SPECS='[[1,2,0,0,0,1,0,0,1,1],[1,2,0,0,0,1,0,0,1,1]]' timeout 300 python tools/bench_modes.py 2>&1 | tail -2
-done
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | grep -E "passed|failed" | tail -2
+timeout 900 python tools/cheb_rate.py 2>&1 | tail -1
