@@ -1379,7 +1379,7 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
       bool plain = !use_acc;
       for (int i = 0; i < P; ++i) plain = plain && C.kernel[i] == LMPK_KERNEL_SPMV;
       if (T->info.dict_tiles == T->info.n_tiles)
-        uniform = (plain && !cplx) ? 3 : 1;
+        uniform = (plain && !cplx && T->slots == 2) ? 3 : 1;  // the plain kernel assumes the 2-piece ring
       else if (T->info.compressed_tiles == T->info.n_tiles && T->info.dict_tiles == 0)
         uniform = 2;
     }

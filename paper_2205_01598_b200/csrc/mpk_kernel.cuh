@@ -1766,7 +1766,9 @@ __global__ void __launch_bounds__(32 * (NC + 2), 1) mpk_ring_kernel(MpkParams P,
   __shared__ uint32_t d_done[kRingMax], d_ctr[kRingMax];
   __shared__ uint32_t trace_ctr;
   __shared__ PowTab s_pow[LMPK_MAX_POWERS];
-  const int NP = P.n_slots;
+  // the plain dictionary kernel runs only with the default 2-piece ring (the
+  // host checks), so its ring index arithmetic is shifts, not divisions
+  const int NP = UNIFORM == 3 ? 2 : P.n_slots;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   build_powtab(s_pow, P, C);
   if (threadIdx.x == 0) {
