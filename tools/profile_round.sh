@@ -2,7 +2,7 @@
 # ncu evidence for profiles/: plain run, launch list, one full capture of the
 # MPK kernel (run on the GPU box through gpurun; 1 GPU).
 set -u
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-clocks"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; tail -20 gpurun_out/plain.log; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -s 0 -c 200 --csv \
