@@ -219,6 +219,19 @@ int lmpk_symmetrized_pattern(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr,
                              const int32_t* col, int* is_symmetric, int64_t* sym_nnz,
                              int64_t* out_row_ptr, int32_t* out_col, int64_t cap, void* stream);
 
+/* CRS build from COO triplets (replaces CsrMatrix.from_triplets,
+ * csr.py:72-94): rows/cols int64[m], vals f64[m] (device).  Range errors
+ * ("row index out of range" / "column index out of range") return
+ * LMPK_ERR_ARG.  Entries are ordered by (row, col) stably; with
+ * sum_duplicates, repeated (row, col) entries are summed in numpy's
+ * np.add.reduceat order (bit-exact).  out_row_ptr holds n+1 entries,
+ * out_col/out_val m (capacity); *out_nnz (host) receives the entry count.
+ * Synchronises the stream. */
+int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const int64_t* rows,
+                           const int64_t* cols, const double* vals, int sum_duplicates,
+                           int32_t* out_row_ptr, int32_t* out_col, double* out_val,
+                           int64_t* out_nnz, void* stream);
+
 /* B[i,j] = A[perm[i], perm[j]], canonical (csr.py:169-187).  out arrays are
  * n+1 / nnz long.  Bit-exact with the reference. */
 int lmpk_permute_symmetric(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,

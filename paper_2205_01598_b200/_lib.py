@@ -101,6 +101,7 @@ SIGNATURES = {
     "lmpk_bfs_levels": (_int, [_vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _i64p, _vp]),
     "lmpk_symmetrized_pattern": (_int, [_vp, _i32, _vp, _vp, ctypes.POINTER(_int), _i64p,
                                         _vp, _vp, _i64, _vp]),
+    "lmpk_csr_from_triplets": (_int, [_vp, _i32, _i64, _vp, _vp, _vp, _int, _vp, _vp, _vp, _vp, _vp]),
     "lmpk_permute_symmetric": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lmpk_permute_vectors": (_int, [_vp, _i32, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _int, _vp]),
     "lmpk_level_nnz": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),

@@ -1,0 +1,213 @@
+// build.cu -- device CRS build from COO triplets (CsrMatrix.from_triplets,
+// pkg/src/levelmpk/csr.py:72-94): range checks, stable (row, col) order,
+// duplicate sums, row_ptr.  Bit-exact with the reference's numpy build:
+//   * order: np.lexsort((cols, rows)) is stable, so two stable LSD radix
+//     passes (col, then row) over the triplet ids give the same permutation;
+//   * sums: np.add.reduceat(vals, starts) (csr.py:88) adds, per segment
+//     [a0, a1 .. am], a0 + pairwise(a1 .. am) -- numpy's float64 reduce loop
+//     (IS_BINARY_REDUCE branch) with its 8-accumulator pairwise summation,
+//     restated in pw_sum below and pinned against numpy by
+//     tests/test_build.py (oracle/cpu_build.py is the same restatement);
+//   * row_ptr: counts of the unique rows, cumsum (csr.py:91-93).
+#include "radix_sort.cuh"
+
+namespace lmpk {
+namespace {
+
+__global__ void k_trip_check(int64_t m, const int64_t* rows, const int64_t* cols, int64_t n, int* bad) {
+  int local = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = rows[i], c = cols[i];
+    if (r < 0 || r >= n) local |= 1;
+    if (c < 0 || c >= n) local |= 2;
+  }
+  if (local) atomicOr(bad, local);
+}
+
+// pass 1 input: key = col, value = triplet id
+__global__ void k_trip_keys_col(int64_t m, const int64_t* cols, uint32_t* k, uint32_t* v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    k[i] = uint32_t(cols[i]);
+    v[i] = uint32_t(i);
+  }
+}
+
+// pass 2 input: key = row of the id at position i (ids already col-sorted)
+__global__ void k_trip_keys_row(int64_t m, const int64_t* rows, const uint32_t* ids, uint32_t* k) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+    k[i] = uint32_t(rows[ids[i]]);
+}
+
+// head[i] = 1 where (row, col) of sorted position i starts a new entry
+__global__ void k_trip_heads(int64_t m, const int64_t* rows, const int64_t* cols, const uint32_t* ids, int sum_dup,
+                             int32_t* head) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    int h = 1;
+    if (sum_dup && i > 0) {
+      const uint32_t a = ids[i - 1], b = ids[i];
+      h = (rows[a] != rows[b] || cols[a] != cols[b]) ? 1 : 0;
+    }
+    head[i] = h;
+  }
+}
+
+// numpy's pairwise float64 sum (loops_utils.h: DOUBLE_pairwise_sum) over
+// b[ids[0..n)], n >= 1: < 8 terms sequential (from -0.0, which is exact),
+// <= 128 terms eight strided accumulators, larger halves split at a multiple of 8.
+__device__ double pw_sum(const double* val, const uint32_t* ids, int64_t n) {
+  // explicit stack of (offset, length) halves, evaluated in the recursive order
+  struct Frame {
+    const uint32_t* p;
+    int64_t n;
+    int state;
+    double left;
+  };
+  Frame st[40];
+  int sp = 0;
+  st[0] = Frame{ids, n, 0, 0.0};
+  double ret = 0.0;
+  for (;;) {
+    Frame& f = st[sp];
+    if (f.n <= 128) {
+      double res;
+      if (f.n < 8) {
+        res = -0.0;
+        for (int64_t i = 0; i < f.n; ++i) res += val[f.p[i]];
+      } else {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = val[f.p[j]];
+        int64_t i = 8;
+        for (; i < f.n - (f.n % 8); i += 8) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) r[j] += val[f.p[i + j]];
+        }
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < f.n; ++i) res += val[f.p[i]];
+      }
+      // return to the parent
+      ret = res;
+      for (;;) {
+        if (sp == 0) return ret;
+        Frame& par = st[--sp];
+        if (par.state == 1) {  // left half done: evaluate the right half
+          par.left = ret;
+          par.state = 2;
+          int64_t n2 = par.n / 2;
+          n2 -= n2 % 8;
+          st[++sp] = Frame{par.p + n2, par.n - n2, 0, 0.0};
+          break;
+        }
+        ret = par.left + ret;  // right half done
+      }
+    } else {
+      int64_t n2 = f.n / 2;
+      n2 -= n2 % 8;
+      f.state = 1;
+      st[++sp] = Frame{f.p, n2, 0, 0.0};
+    }
+  }
+}
+
+// one thread per output entry: col, summed value and a row count
+__global__ void k_trip_emit(int64_t m, const int64_t* rows, const int64_t* cols, const double* vals,
+                            const uint32_t* ids, const int32_t* head, const int64_t* pos, int64_t n_out,
+                            int32_t* out_col, double* out_val, int32_t* row_cnt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    if (!head[i]) continue;
+    const int64_t o = pos[i];
+    int64_t e = i + 1;
+    while (e < m && !head[e]) ++e;  // duplicates of one entry are rare and short
+    const uint32_t id = ids[i];
+    double s = vals[id];
+    if (e - i > 1) s = s + pw_sum(vals, ids + i + 1, e - i - 1);
+    out_col[o] = int32_t(cols[id]);
+    out_val[o] = s;
+    atomicAdd(row_cnt + rows[id], 1);
+  }
+  (void)n_out;
+}
+
+inline int grid_trip(lmpk_ctx* ctx, int64_t m) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(int64_t(ctx->sm_count) * 8, (m + 255) / 256)));
+}
+
+}  // namespace
+}  // namespace lmpk
+
+using namespace lmpk;
+
+extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const int64_t* rows,
+                                      const int64_t* cols, const double* vals, int sum_duplicates,
+                                      int32_t* out_row_ptr, int32_t* out_col, double* out_val,
+                                      int64_t* out_nnz, void* stream) {
+  LMPK_ARG_CHECK(ctx && out_row_ptr && out_nnz, "lmpk_csr_from_triplets: NULL argument");
+  LMPK_ARG_CHECK(n >= 0 && m >= 0, "n and m must be >= 0");
+  LMPK_ARG_CHECK(m < (int64_t(1) << 31), "triplet count exceeds the 32-bit index range");
+  LMPK_ARG_CHECK(m == 0 || (rows && cols && vals && out_col && out_val), "lmpk_csr_from_triplets: NULL argument");
+  cudaStream_t st = as_stream(stream);
+  *out_nnz = 0;
+  if (m == 0) {
+    LMPK_CHECK_CUDA(cudaMemsetAsync(out_row_ptr, 0, (size_t(n) + 1) * 4, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+    return LMPK_OK;
+  }
+  const size_t M = size_t(m);
+  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head (u32/i32, m each) | row counts (i32, n)
+  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 5 + size_t(n) * 4 + 64));
+  int64_t* pos = reinterpret_cast<int64_t*>(ctx->s_a.ptr);
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(pos + M + 1);
+  uint32_t* v0 = k0 + M;
+  uint32_t* k1 = v0 + M;
+  uint32_t* v1 = k1 + M;
+  int32_t* head = reinterpret_cast<int32_t*>(v1 + M);
+  int32_t* cnt = head + M;
+  const int64_t cnt_len = radix_counts_len(m);
+  const int64_t tmp_len = scan_tmp_len(std::max<int64_t>(std::max<int64_t>(cnt_len, m), int64_t(n) + 1)) + 8;
+  LMPK_TRY(ctx->s_d.ensure(size_t(cnt_len) * 12 + size_t(tmp_len) * 8 + 4096));
+  int* bad = reinterpret_cast<int*>(ctx->s_d.ptr);
+  uint32_t* counts = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctx->s_d.ptr) + 256);
+  int64_t* offsets = reinterpret_cast<int64_t*>(counts + ((cnt_len + 1) & ~int64_t(1)));
+  int64_t* stmp = offsets + cnt_len;
+  const int g = grid_trip(ctx, m);
+  LMPK_CHECK_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+  k_trip_check<<<g, 256, 0, st>>>(m, rows, cols, int64_t(n), bad);
+  launch_count_add(ctx, 1);
+  int h_bad = 0;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  LMPK_ARG_CHECK(!(h_bad & 1), "row index out of range");
+  LMPK_ARG_CHECK(!(h_bad & 2), "column index out of range");
+  int bits = 0;
+  while (bits < 32 && (int64_t(1) << bits) < int64_t(n)) ++bits;
+  // pass 1: stable sort of the ids by col
+  k_trip_keys_col<<<g, 256, 0, st>>>(m, cols, k0, v0);
+  launch_count_add(ctx, 1);
+  bool first = true;
+  LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, m, bits, counts, offsets, stmp, &first, st));
+  uint32_t* ids = first ? v0 : v1;
+  uint32_t* kk = first ? k0 : k1;
+  uint32_t* ko = first ? k1 : k0;
+  uint32_t* vo = first ? v1 : v0;
+  // pass 2: stable sort by row (lexsort's primary key)
+  k_trip_keys_row<<<g, 256, 0, st>>>(m, rows, ids, kk);
+  launch_count_add(ctx, 1);
+  bool first2 = true;
+  LMPK_TRY(device_radix_sort(ctx, kk, ids, ko, vo, m, bits, counts, offsets, stmp, &first2, st));
+  const uint32_t* sorted = first2 ? ids : vo;
+  k_trip_heads<<<g, 256, 0, st>>>(m, rows, cols, sorted, sum_duplicates ? 1 : 0, head);
+  launch_count_add(ctx, 1);
+  LMPK_TRY(device_excl_scan<int32_t, int64_t>(ctx, head, m, pos, 0, true, stmp, st));
+  int64_t n_out = 0;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&n_out, pos + m, 8, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  LMPK_ARG_CHECK(n_out <= int64_t(INT32_MAX), "nnz exceeds the 32-bit index range");
+  LMPK_CHECK_CUDA(cudaMemsetAsync(cnt, 0, size_t(n) * 4, st));
+  k_trip_emit<<<g, 256, 0, st>>>(m, rows, cols, vals, sorted, head, pos, n_out, out_col, out_val, cnt);
+  launch_count_add(ctx, 1);
+  LMPK_TRY(device_excl_scan<int32_t, int32_t>(ctx, cnt, int64_t(n), out_row_ptr, 0, true, stmp, st));
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  *out_nnz = n_out;
+  return LMPK_OK;
+}

@@ -195,6 +195,31 @@ def symmetrized_pattern(a: DeviceCsr, stream=None):
     return rp, col[: int(nnz.value)]
 
 
+def csr_from_triplets(n, rows, cols, vals, sum_duplicates=True, stream=None) -> DeviceCsr:
+    """Device CRS build from COO triplets (csr.py:72-94, bit-exact): rows/cols
+    int64 and vals float64 CUDA tensors of one length.  Raises ValueError
+    ("row index out of range" / "column index out of range") like the reference."""
+    torch = _torch()
+    ctx = context()
+    rows = rows.to(torch.int64).contiguous()
+    cols = cols.to(torch.int64).contiguous()
+    vals = vals.to(torch.float64).contiguous()
+    m = int(rows.shape[0])
+    if int(cols.shape[0]) != m or int(vals.shape[0]) != m:
+        raise ValueError("rows, cols and vals must have the same length")
+    dev = rows.device
+    rp = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    col = torch.empty(m, dtype=torch.int32, device=dev)
+    val = torch.empty(m, dtype=torch.float64, device=dev)
+    nnz = ctypes.c_int64(0)
+    rc = ctx.lib.lmpk_csr_from_triplets(ctx.handle, int(n), m, ptr(rows), ptr(cols), ptr(vals),
+                                        1 if sum_duplicates else 0, ptr(rp), ptr(col), ptr(val),
+                                        ctypes.byref(nnz), stream_handle(stream))
+    check(rc, "csr_from_triplets")  # LMPK_ERR_ARG -> ValueError with the reference's message
+    k = int(nnz.value)
+    return DeviceCsr(int(n), rp, col[:k], val[:k])
+
+
 def permute_symmetric(a: DeviceCsr, perm, inv, stream=None) -> DeviceCsr:
     torch = _torch()
     ctx = context()
