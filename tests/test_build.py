@@ -115,3 +115,20 @@ def test_from_triplets_no_sum_and_empty():
 def test_from_triplets_range_errors(rows, cols, msg):
     with pytest.raises(ValueError, match=msg):
         _device_build(3, np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64), np.ones(2))
+
+
+@pytest.mark.gpu
+def test_csrmatrix_from_triplets_device_tensors():
+    import torch
+
+    import paper_2205_01598_b200 as lm
+
+    rows, cols, vals = _triplets(11, 500, 5000, 0.2)
+    host = lm.CsrMatrix.from_triplets(500, rows, cols, vals)
+    dev = lm.CsrMatrix.from_triplets(500, torch.from_numpy(rows).cuda(), torch.from_numpy(cols).cuda(),
+                                     torch.from_numpy(vals).cuda())
+    assert np.array_equal(dev.row_ptr, host.row_ptr) and np.array_equal(dev.col, host.col)
+    assert dev.val.tobytes() == host.val.tobytes()
+    with pytest.raises(ValueError, match="strictly increasing"):
+        lm.CsrMatrix.from_triplets(3, torch.tensor([0, 0]).cuda(), torch.tensor([1, 1]).cuda(),
+                                   torch.tensor([1.0, 2.0], dtype=torch.float64).cuda(), sum_duplicates=False)
