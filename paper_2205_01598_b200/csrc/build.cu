@@ -8,7 +8,8 @@
 //     (IS_BINARY_REDUCE branch) with its 8-accumulator pairwise summation,
 //     restated in pw_sum below and pinned against numpy by
 //     tests/test_build.py (oracle/cpu_build.py is the same restatement);
-//   * row_ptr: counts of the unique rows, cumsum (csr.py:91-93).
+//   * row_ptr: counts of the unique rows, cumsum (csr.py:91-93), here read
+//     off the sorted rows of the output entries.
 #include "radix_sort.cuh"
 
 namespace lmpk {
@@ -38,15 +39,18 @@ __global__ void k_trip_keys_row(int64_t m, const int64_t* rows, const uint32_t* 
     k[i] = uint32_t(rows[ids[i]]);
 }
 
+// sorted columns as u32 (the one random gather of cols), so the passes
+// below read (row, col) of neighbouring positions sequentially
+__global__ void k_trip_cols_sorted(int64_t m, const int64_t* cols, const uint32_t* ids, uint32_t* cs) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+    cs[i] = uint32_t(cols[ids[i]]);
+}
+
 // head[i] = 1 where (row, col) of sorted position i starts a new entry
-__global__ void k_trip_heads(int64_t m, const int64_t* rows, const int64_t* cols, const uint32_t* ids, int sum_dup,
-                             int32_t* head) {
+__global__ void k_trip_heads(int64_t m, const uint32_t* rk, const uint32_t* cs, int sum_dup, int32_t* head) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
     int h = 1;
-    if (sum_dup && i > 0) {
-      const uint32_t a = ids[i - 1], b = ids[i];
-      h = (rows[a] != rows[b] || cols[a] != cols[b]) ? 1 : 0;
-    }
+    if (sum_dup && i > 0) h = (rk[i] != rk[i - 1] || cs[i] != cs[i - 1]) ? 1 : 0;
     head[i] = h;
   }
 }
@@ -109,23 +113,33 @@ __device__ double pw_sum(const double* val, const uint32_t* ids, int64_t n) {
   }
 }
 
-// one thread per output entry: col, summed value and a row count
-__global__ void k_trip_emit(int64_t m, const int64_t* rows, const int64_t* cols, const double* vals,
-                            const uint32_t* ids, const int32_t* head, const int64_t* pos, int64_t n_out,
-                            int32_t* out_col, double* out_val, int32_t* row_cnt) {
+// one thread per output entry: col, summed value, its row
+__global__ void k_trip_emit(int64_t m, const uint32_t* rk, const uint32_t* cs, const double* vals,
+                            const uint32_t* ids, const int32_t* head, const int64_t* pos, int32_t* out_col,
+                            double* out_val, uint32_t* out_row) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
     if (!head[i]) continue;
     const int64_t o = pos[i];
     int64_t e = i + 1;
     while (e < m && !head[e]) ++e;  // duplicates of one entry are rare and short
-    const uint32_t id = ids[i];
-    double s = vals[id];
+    double s = vals[ids[i]];
     if (e - i > 1) s = s + pw_sum(vals, ids + i + 1, e - i - 1);
-    out_col[o] = int32_t(cols[id]);
+    out_col[o] = int32_t(cs[i]);
     out_val[o] = s;
-    atomicAdd(row_cnt + rows[id], 1);
+    out_row[o] = rk[i];
   }
-  (void)n_out;
+}
+
+// row_ptr from the (sorted) rows of the output entries: entry o opens rows
+// (row[o-1], row[o]]; the last entry closes the rows after it
+__global__ void k_trip_row_ptr(int64_t n_out, const uint32_t* orow, int32_t n, int32_t* row_ptr) {
+  for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < n_out; o += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = orow[o];
+    const int64_t prev = o == 0 ? -1 : int64_t(orow[o - 1]);
+    for (int64_t q = prev + 1; q <= r; ++q) row_ptr[q] = int32_t(o);
+    if (o == n_out - 1)
+      for (int64_t q = r + 1; q <= n; ++q) row_ptr[q] = int32_t(n_out);
+  }
 }
 
 inline int grid_trip(lmpk_ctx* ctx, int64_t m) {
@@ -153,15 +167,14 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
     return LMPK_OK;
   }
   const size_t M = size_t(m);
-  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head (u32/i32, m each) | row counts (i32, n)
-  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 5 + size_t(n) * 4 + 64));
+  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head (u32/i32, m each)
+  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 5 + 64));
   int64_t* pos = reinterpret_cast<int64_t*>(ctx->s_a.ptr);
   uint32_t* k0 = reinterpret_cast<uint32_t*>(pos + M + 1);
   uint32_t* v0 = k0 + M;
   uint32_t* k1 = v0 + M;
   uint32_t* v1 = k1 + M;
   int32_t* head = reinterpret_cast<int32_t*>(v1 + M);
-  int32_t* cnt = head + M;
   const int64_t cnt_len = radix_counts_len(m);
   const int64_t tmp_len = scan_tmp_len(std::max<int64_t>(std::max<int64_t>(cnt_len, m), int64_t(n) + 1)) + 8;
   LMPK_TRY(ctx->s_d.ensure(size_t(cnt_len) * 12 + size_t(tmp_len) * 8 + 4096));
@@ -195,17 +208,22 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   bool first2 = true;
   LMPK_TRY(device_radix_sort(ctx, kk, ids, ko, vo, m, bits, counts, offsets, stmp, &first2, st));
   const uint32_t* sorted = first2 ? ids : vo;
-  k_trip_heads<<<g, 256, 0, st>>>(m, rows, cols, sorted, sum_duplicates ? 1 : 0, head);
+  const uint32_t* rk = first2 ? kk : ko;  // rows in sorted order
+  uint32_t* cs = first2 ? ko : kk;        // the two free buffers of pass 2
+  uint32_t* orow = first2 ? vo : ids;
+  k_trip_cols_sorted<<<g, 256, 0, st>>>(m, cols, sorted, cs);
+  launch_count_add(ctx, 1);
+  k_trip_heads<<<g, 256, 0, st>>>(m, rk, cs, sum_duplicates ? 1 : 0, head);
   launch_count_add(ctx, 1);
   LMPK_TRY(device_excl_scan<int32_t, int64_t>(ctx, head, m, pos, 0, true, stmp, st));
   int64_t n_out = 0;
   LMPK_CHECK_CUDA(cudaMemcpyAsync(&n_out, pos + m, 8, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   LMPK_ARG_CHECK(n_out <= int64_t(INT32_MAX), "nnz exceeds the 32-bit index range");
-  LMPK_CHECK_CUDA(cudaMemsetAsync(cnt, 0, size_t(n) * 4, st));
-  k_trip_emit<<<g, 256, 0, st>>>(m, rows, cols, vals, sorted, head, pos, n_out, out_col, out_val, cnt);
+  k_trip_emit<<<g, 256, 0, st>>>(m, rk, cs, vals, sorted, head, pos, out_col, out_val, orow);
   launch_count_add(ctx, 1);
-  LMPK_TRY(device_excl_scan<int32_t, int32_t>(ctx, cnt, int64_t(n), out_row_ptr, 0, true, stmp, st));
+  k_trip_row_ptr<<<grid_trip(ctx, n_out), 256, 0, st>>>(n_out, orow, n, out_row_ptr);
+  launch_count_add(ctx, 1);
   LMPK_CHECK_CUDA(cudaGetLastError());
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   *out_nnz = n_out;
