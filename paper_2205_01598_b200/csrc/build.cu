@@ -15,35 +15,40 @@
 namespace lmpk {
 namespace {
 
-__global__ void k_trip_check(int64_t m, const int64_t* rows, const int64_t* cols, int64_t n, int* bad) {
+__global__ void k_trip_check(int64_t m, const int64_t* rows, const int64_t* cols, int64_t n, int* bad,
+                             uint32_t* r32, uint32_t* c32) {
+  // also narrows the indices to u32: the later gathers by triplet id then
+  // touch 4 B instead of 8 B per random access
   int local = 0;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = rows[i], c = cols[i];
     if (r < 0 || r >= n) local |= 1;
     if (c < 0 || c >= n) local |= 2;
+    r32[i] = uint32_t(r);
+    c32[i] = uint32_t(c);
   }
   if (local) atomicOr(bad, local);
 }
 
 // pass 1 input: key = col, value = triplet id
-__global__ void k_trip_keys_col(int64_t m, const int64_t* cols, uint32_t* k, uint32_t* v) {
+__global__ void k_trip_keys_col(int64_t m, const uint32_t* cols, uint32_t* k, uint32_t* v) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
-    k[i] = uint32_t(cols[i]);
+    k[i] = cols[i];
     v[i] = uint32_t(i);
   }
 }
 
 // pass 2 input: key = row of the id at position i (ids already col-sorted)
-__global__ void k_trip_keys_row(int64_t m, const int64_t* rows, const uint32_t* ids, uint32_t* k) {
+__global__ void k_trip_keys_row(int64_t m, const uint32_t* rows, const uint32_t* ids, uint32_t* k) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
-    k[i] = uint32_t(rows[ids[i]]);
+    k[i] = rows[ids[i]];
 }
 
 // sorted columns as u32 (the one random gather of cols), so the passes
 // below read (row, col) of neighbouring positions sequentially
-__global__ void k_trip_cols_sorted(int64_t m, const int64_t* cols, const uint32_t* ids, uint32_t* cs) {
+__global__ void k_trip_cols_sorted(int64_t m, const uint32_t* cols, const uint32_t* ids, uint32_t* cs) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
-    cs[i] = uint32_t(cols[ids[i]]);
+    cs[i] = cols[ids[i]];
 }
 
 // head[i] = 1 where (row, col) of sorted position i starts a new entry
@@ -167,14 +172,16 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
     return LMPK_OK;
   }
   const size_t M = size_t(m);
-  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head (u32/i32, m each)
-  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 5 + 64));
+  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head r32 c32 (u32/i32, m each)
+  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 7 + 64));
   int64_t* pos = reinterpret_cast<int64_t*>(ctx->s_a.ptr);
   uint32_t* k0 = reinterpret_cast<uint32_t*>(pos + M + 1);
   uint32_t* v0 = k0 + M;
   uint32_t* k1 = v0 + M;
   uint32_t* v1 = k1 + M;
   int32_t* head = reinterpret_cast<int32_t*>(v1 + M);
+  uint32_t* r32 = reinterpret_cast<uint32_t*>(head + M);
+  uint32_t* c32 = r32 + M;
   const int64_t cnt_len = radix_counts_len(m);
   const int64_t tmp_len = scan_tmp_len(std::max<int64_t>(std::max<int64_t>(cnt_len, m), int64_t(n) + 1)) + 8;
   LMPK_TRY(ctx->s_d.ensure(size_t(cnt_len) * 12 + size_t(tmp_len) * 8 + 4096));
@@ -184,7 +191,7 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   int64_t* stmp = offsets + cnt_len;
   const int g = grid_trip(ctx, m);
   LMPK_CHECK_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-  k_trip_check<<<g, 256, 0, st>>>(m, rows, cols, int64_t(n), bad);
+  k_trip_check<<<g, 256, 0, st>>>(m, rows, cols, int64_t(n), bad, r32, c32);
   launch_count_add(ctx, 1);
   int h_bad = 0;
   LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
@@ -194,7 +201,7 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   int bits = 0;
   while (bits < 32 && (int64_t(1) << bits) < int64_t(n)) ++bits;
   // pass 1: stable sort of the ids by col
-  k_trip_keys_col<<<g, 256, 0, st>>>(m, cols, k0, v0);
+  k_trip_keys_col<<<g, 256, 0, st>>>(m, c32, k0, v0);
   launch_count_add(ctx, 1);
   bool first = true;
   LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, m, bits, counts, offsets, stmp, &first, st));
@@ -203,7 +210,7 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   uint32_t* ko = first ? k1 : k0;
   uint32_t* vo = first ? v1 : v0;
   // pass 2: stable sort by row (lexsort's primary key)
-  k_trip_keys_row<<<g, 256, 0, st>>>(m, rows, ids, kk);
+  k_trip_keys_row<<<g, 256, 0, st>>>(m, r32, ids, kk);
   launch_count_add(ctx, 1);
   bool first2 = true;
   LMPK_TRY(device_radix_sort(ctx, kk, ids, ko, vo, m, bits, counts, offsets, stmp, &first2, st));
@@ -211,7 +218,7 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   const uint32_t* rk = first2 ? kk : ko;  // rows in sorted order
   uint32_t* cs = first2 ? ko : kk;        // the two free buffers of pass 2
   uint32_t* orow = first2 ? vo : ids;
-  k_trip_cols_sorted<<<g, 256, 0, st>>>(m, cols, sorted, cs);
+  k_trip_cols_sorted<<<g, 256, 0, st>>>(m, c32, sorted, cs);
   launch_count_add(ctx, 1);
   k_trip_heads<<<g, 256, 0, st>>>(m, rk, cs, sum_duplicates ? 1 : 0, head);
   launch_count_add(ctx, 1);
