@@ -16,7 +16,7 @@ namespace lmpk {
 namespace {
 
 __global__ void k_trip_check(int64_t m, const int64_t* rows, const int64_t* cols, int64_t n, int* bad,
-                             uint32_t* r32, uint32_t* c32) {
+                             uint32_t* r32, uint32_t* c32, int32_t* row_cnt) {
   // also narrows the indices to u32: the later gathers by triplet id then
   // touch 4 B instead of 8 B per random access
   int local = 0;
@@ -26,6 +26,7 @@ __global__ void k_trip_check(int64_t m, const int64_t* rows, const int64_t* cols
     if (c < 0 || c >= n) local |= 2;
     r32[i] = uint32_t(r);
     c32[i] = uint32_t(c);
+    if (r >= 0 && r < n) atomicAdd(row_cnt + r, 1);
   }
   if (local) atomicOr(bad, local);
 }
@@ -147,6 +148,45 @@ __global__ void k_trip_row_ptr(int64_t n_out, const uint32_t* orow, int32_t n, i
   }
 }
 
+// ---- short-row path (every row holds <= kShortRow triplets): rows are
+// bucketed by a counting sort, then each row's (col, id) pairs are sorted by
+// one thread -- the same order as the two stable radix passes (lexsort by
+// (row, col), ties by triplet id), without their 6 passes and id gathers.
+constexpr int kShortRow = 32;
+
+__global__ void k_trip_max(int32_t n, const int32_t* cnt, int* out) {
+  int v = 0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    v = max(v, cnt[i]);
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, v);
+}
+
+__global__ void k_trip_bucket(int64_t m, const uint32_t* r32, int32_t* cur, uint32_t* bucket) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x)
+    bucket[atomicAdd(cur + r32[i], 1)] = uint32_t(i);
+}
+
+__global__ void k_trip_row_sort(int32_t n, const int32_t* rstart, const uint32_t* c32, uint32_t* ids,
+                                uint32_t* rk, uint32_t* cs) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t b = rstart[r], L = rstart[r + 1] - b;
+    uint64_t key[kShortRow];
+    for (int j = 0; j < L; ++j) {
+      const uint32_t id = ids[b + j];
+      uint64_t k = (uint64_t(c32[id]) << 32) | id;
+      int q = j;
+      for (; q > 0 && key[q - 1] > k; --q) key[q] = key[q - 1];  // insertion sort
+      key[q] = k;
+    }
+    for (int j = 0; j < L; ++j) {
+      ids[b + j] = uint32_t(key[j]);
+      cs[b + j] = uint32_t(key[j] >> 32);
+      rk[b + j] = uint32_t(r);
+    }
+  }
+}
+
 inline int grid_trip(lmpk_ctx* ctx, int64_t m) {
   return int(std::max<int64_t>(1, std::min<int64_t>(int64_t(ctx->sm_count) * 8, (m + 255) / 256)));
 }
@@ -172,8 +212,9 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
     return LMPK_OK;
   }
   const size_t M = size_t(m);
-  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head r32 c32 (u32/i32, m each)
-  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 7 + 64));
+  // scratch: pos (i64, m+1) | k0 v0 k1 v1 head r32 c32 (u32/i32, m each) | cnt rstart cur (i32, n+1 each)
+  const size_t N1 = size_t(n) + 1;
+  LMPK_TRY(ctx->s_a.ensure((M + 1) * 8 + M * 4 * 7 + N1 * 4 * 3 + 64));
   int64_t* pos = reinterpret_cast<int64_t*>(ctx->s_a.ptr);
   uint32_t* k0 = reinterpret_cast<uint32_t*>(pos + M + 1);
   uint32_t* v0 = k0 + M;
@@ -182,6 +223,9 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   int32_t* head = reinterpret_cast<int32_t*>(v1 + M);
   uint32_t* r32 = reinterpret_cast<uint32_t*>(head + M);
   uint32_t* c32 = r32 + M;
+  int32_t* cnt = reinterpret_cast<int32_t*>(c32 + M);
+  int32_t* rstart = cnt + N1;
+  int32_t* cur = rstart + N1;
   const int64_t cnt_len = radix_counts_len(m);
   const int64_t tmp_len = scan_tmp_len(std::max<int64_t>(std::max<int64_t>(cnt_len, m), int64_t(n) + 1)) + 8;
   LMPK_TRY(ctx->s_d.ensure(size_t(cnt_len) * 12 + size_t(tmp_len) * 8 + 4096));
@@ -190,36 +234,61 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   int64_t* offsets = reinterpret_cast<int64_t*>(counts + ((cnt_len + 1) & ~int64_t(1)));
   int64_t* stmp = offsets + cnt_len;
   const int g = grid_trip(ctx, m);
-  LMPK_CHECK_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-  k_trip_check<<<g, 256, 0, st>>>(m, rows, cols, int64_t(n), bad, r32, c32);
+  LMPK_CHECK_CUDA(cudaMemsetAsync(bad, 0, 8, st));
+  LMPK_CHECK_CUDA(cudaMemsetAsync(cnt, 0, N1 * 4, st));
+  k_trip_check<<<g, 256, 0, st>>>(m, rows, cols, int64_t(n), bad, r32, c32, cnt);
   launch_count_add(ctx, 1);
-  int h_bad = 0;
-  LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+  k_trip_max<<<grid_trip(ctx, n), 256, 0, st>>>(n, cnt, bad + 1);
+  launch_count_add(ctx, 1);
+  int h_bad2[2] = {0, 0};
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(h_bad2, bad, 8, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  const int h_bad = h_bad2[0], max_row = h_bad2[1];
   LMPK_ARG_CHECK(!(h_bad & 1), "row index out of range");
   LMPK_ARG_CHECK(!(h_bad & 2), "column index out of range");
-  int bits = 0;
-  while (bits < 32 && (int64_t(1) << bits) < int64_t(n)) ++bits;
-  // pass 1: stable sort of the ids by col
-  k_trip_keys_col<<<g, 256, 0, st>>>(m, c32, k0, v0);
-  launch_count_add(ctx, 1);
-  bool first = true;
-  LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, m, bits, counts, offsets, stmp, &first, st));
-  uint32_t* ids = first ? v0 : v1;
-  uint32_t* kk = first ? k0 : k1;
-  uint32_t* ko = first ? k1 : k0;
-  uint32_t* vo = first ? v1 : v0;
-  // pass 2: stable sort by row (lexsort's primary key)
-  k_trip_keys_row<<<g, 256, 0, st>>>(m, r32, ids, kk);
-  launch_count_add(ctx, 1);
-  bool first2 = true;
-  LMPK_TRY(device_radix_sort(ctx, kk, ids, ko, vo, m, bits, counts, offsets, stmp, &first2, st));
-  const uint32_t* sorted = first2 ? ids : vo;
-  const uint32_t* rk = first2 ? kk : ko;  // rows in sorted order
-  uint32_t* cs = first2 ? ko : kk;        // the two free buffers of pass 2
-  uint32_t* orow = first2 ? vo : ids;
-  k_trip_cols_sorted<<<g, 256, 0, st>>>(m, c32, sorted, cs);
-  launch_count_add(ctx, 1);
+  const uint32_t* sorted;
+  const uint32_t* rk;
+  uint32_t* cs;
+  uint32_t* orow;
+  bool have_cols = false;
+  if (max_row <= kShortRow) {
+    LMPK_TRY(device_excl_scan<int32_t, int32_t>(ctx, cnt, int64_t(n), rstart, 0, true, stmp, st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(cur, rstart, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
+    k_trip_bucket<<<g, 256, 0, st>>>(m, r32, cur, v0);
+    launch_count_add(ctx, 1);
+    k_trip_row_sort<<<grid_trip(ctx, n), 256, 0, st>>>(n, rstart, c32, v0, k0, k1);
+    launch_count_add(ctx, 1);
+    sorted = v0;
+    rk = k0;
+    cs = k1;
+    orow = v1;
+    have_cols = true;
+  } else {
+    int bits = 0;
+    while (bits < 32 && (int64_t(1) << bits) < int64_t(n)) ++bits;
+    // pass 1: stable sort of the ids by col
+    k_trip_keys_col<<<g, 256, 0, st>>>(m, c32, k0, v0);
+    launch_count_add(ctx, 1);
+    bool first = true;
+    LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, m, bits, counts, offsets, stmp, &first, st));
+    uint32_t* ids = first ? v0 : v1;
+    uint32_t* kk = first ? k0 : k1;
+    uint32_t* ko = first ? k1 : k0;
+    uint32_t* vo = first ? v1 : v0;
+    // pass 2: stable sort by row (lexsort's primary key)
+    k_trip_keys_row<<<g, 256, 0, st>>>(m, r32, ids, kk);
+    launch_count_add(ctx, 1);
+    bool first2 = true;
+    LMPK_TRY(device_radix_sort(ctx, kk, ids, ko, vo, m, bits, counts, offsets, stmp, &first2, st));
+    sorted = first2 ? ids : vo;
+    rk = first2 ? kk : ko;  // rows in sorted order
+    cs = first2 ? ko : kk;  // the two free buffers of pass 2
+    orow = first2 ? vo : ids;
+  }
+  if (!have_cols) {
+    k_trip_cols_sorted<<<g, 256, 0, st>>>(m, c32, sorted, cs);
+    launch_count_add(ctx, 1);
+  }
   k_trip_heads<<<g, 256, 0, st>>>(m, rk, cs, sum_duplicates ? 1 : 0, head);
   launch_count_add(ctx, 1);
   LMPK_TRY(device_excl_scan<int32_t, int64_t>(ctx, head, m, pos, 0, true, stmp, st));

@@ -132,3 +132,20 @@ def test_csrmatrix_from_triplets_device_tensors():
     with pytest.raises(ValueError, match="strictly increasing"):
         lm.CsrMatrix.from_triplets(3, torch.tensor([0, 0]).cuda(), torch.tensor([1, 1]).cuda(),
                                    torch.tensor([1.0, 2.0], dtype=torch.float64).cuda(), sum_duplicates=False)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("row_len", [32, 33])  # 32: per-row sort path; 33: the two radix passes
+def test_from_triplets_short_row_boundary(row_len):
+    rng = np.random.default_rng(row_len)
+    n = 64
+    rows = np.repeat(np.arange(n), row_len)
+    cols = rng.integers(0, 8, size=rows.size)  # many duplicates inside each row
+    p = rng.permutation(rows.size)
+    rows, cols = rows[p].astype(np.int64), cols[p].astype(np.int64)
+    vals = rng.standard_normal(rows.size) * 10.0 ** rng.integers(-8, 9, size=rows.size)
+    rows[:3] = 5  # an uneven row next to the full ones
+    rp, col, val = _device_build(n, rows, cols, vals)
+    erp, ecol, ev = O.from_triplets(n, rows, cols, vals)
+    assert np.array_equal(rp.astype(np.int64), erp) and np.array_equal(col.astype(np.int64), ecol)
+    assert val.tobytes() == ev.tobytes()
