@@ -148,9 +148,10 @@ __global__ void k_trip_row_ptr(int64_t n_out, const uint32_t* orow, int32_t n, i
   }
 }
 
-// ---- short-row path (every row holds <= kShortRow triplets): rows are
-// bucketed by a counting sort, then each row's (col, id) pairs are sorted by
-// one thread -- the same order as the two stable radix passes (lexsort by
+// ---- row-bucket path (every row holds <= kLongRow triplets): rows are
+// bucketed by a counting sort, then each row's (col, id) pairs are sorted --
+// by one thread for rows of <= kShortRow, by one CTA (bitonic, smem) for
+// longer ones -- the same order as the two stable radix passes (lexsort by
 // (row, col), ties by triplet id), without their 6 passes and id gathers.
 constexpr int kShortRow = 32;
 
@@ -171,6 +172,7 @@ __global__ void k_trip_row_sort(int32_t n, const int32_t* rstart, const uint32_t
                                 uint32_t* rk, uint32_t* cs) {
   for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < n; r += int64_t(gridDim.x) * blockDim.x) {
     const int32_t b = rstart[r], L = rstart[r + 1] - b;
+    if (L > kShortRow) continue;  // k_trip_long_row_sort
     uint64_t key[kShortRow];
     for (int j = 0; j < L; ++j) {
       const uint32_t id = ids[b + j];
@@ -184,6 +186,52 @@ __global__ void k_trip_row_sort(int32_t n, const int32_t* rstart, const uint32_t
       cs[b + j] = uint32_t(key[j] >> 32);
       rk[b + j] = uint32_t(r);
     }
+  }
+}
+
+// rows of kShortRow < L <= kLongRow triplets: one CTA per row, bitonic sort
+// of the (col, id) keys in shared memory (keys are unique: ids differ)
+constexpr int kLongRow = 4096;
+
+__global__ void __launch_bounds__(256) k_trip_long_row_sort(int32_t n, const int32_t* rstart, const uint32_t* c32,
+                                                            uint32_t* ids, uint32_t* rk, uint32_t* cs) {
+  __shared__ uint64_t key[kLongRow];
+  for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+    const int32_t b = rstart[r], L = rstart[r + 1] - b;
+    if (L <= kShortRow) continue;  // uniform per CTA
+    int P = 1;
+    while (P < L) P <<= 1;
+    for (int j = threadIdx.x; j < P; j += blockDim.x) {
+      if (j < L) {
+        const uint32_t id = ids[b + j];
+        key[j] = (uint64_t(c32[id]) << 32) | id;
+      } else {
+        key[j] = ~uint64_t(0);  // padding sorts last
+      }
+    }
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          const int l = i ^ jj;
+          if (l > i) {
+            const uint64_t a = key[i], c = key[l];
+            const bool up = (i & k) == 0;
+            if ((a > c) == up) {
+              key[i] = c;
+              key[l] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+      ids[b + j] = uint32_t(key[j]);
+      cs[b + j] = uint32_t(key[j] >> 32);
+      rk[b + j] = uint32_t(r);
+    }
+    __syncthreads();
   }
 }
 
@@ -251,13 +299,18 @@ extern "C" int lmpk_csr_from_triplets(lmpk_ctx* ctx, int32_t n, int64_t m, const
   uint32_t* cs;
   uint32_t* orow;
   bool have_cols = false;
-  if (max_row <= kShortRow) {
+  if (max_row <= kLongRow) {
     LMPK_TRY(device_excl_scan<int32_t, int32_t>(ctx, cnt, int64_t(n), rstart, 0, true, stmp, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(cur, rstart, size_t(n) * 4, cudaMemcpyDeviceToDevice, st));
     k_trip_bucket<<<g, 256, 0, st>>>(m, r32, cur, v0);
     launch_count_add(ctx, 1);
     k_trip_row_sort<<<grid_trip(ctx, n), 256, 0, st>>>(n, rstart, c32, v0, k0, k1);
     launch_count_add(ctx, 1);
+    if (max_row > kShortRow) {
+      k_trip_long_row_sort<<<int(std::min<int64_t>(n, int64_t(ctx->sm_count) * 8)), 256, 0, st>>>(n, rstart, c32, v0,
+                                                                                                   k0, k1);
+      launch_count_add(ctx, 1);
+    }
     sorted = v0;
     rk = k0;
     cs = k1;

@@ -135,12 +135,14 @@ def test_csrmatrix_from_triplets_device_tensors():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("row_len", [32, 33])  # 32: per-row sort path; 33: the two radix passes
+# 32: one thread sorts each row; 33 and 4096: one CTA per row (bitonic);
+# 4097 and 5000: the two full radix passes
+@pytest.mark.parametrize("row_len", [32, 33, 4096, 4097, 5000])
 def test_from_triplets_short_row_boundary(row_len):
     rng = np.random.default_rng(row_len)
     n = 64
     rows = np.repeat(np.arange(n), row_len)
-    cols = rng.integers(0, 8, size=rows.size)  # many duplicates inside each row
+    cols = rng.integers(0, min(n, max(8, row_len // 4)), size=rows.size)  # many duplicates per row
     p = rng.permutation(rows.size)
     rows, cols = rows[p].astype(np.int64), cols[p].astype(np.int64)
     vals = rng.standard_normal(rows.size) * 10.0 ** rng.integers(-8, 9, size=rows.size)
