@@ -53,8 +53,11 @@ def _parse_header(rd: _Reader):
     return field, symmetry
 
 
-def load_matrix_market(path) -> CsrMatrix:
-    """Read a coordinate-format Matrix Market file into a canonical CsrMatrix."""
+def load_matrix_market(path, device=False) -> CsrMatrix:
+    """Read a coordinate-format Matrix Market file into a canonical CsrMatrix.
+
+    device=True builds the CRS in HBM (lmpk_csr_from_triplets, bit-exact with
+    the host build); parsing stays on the host (mmio.py:22-96)."""
     rd = _Reader(path)
     field, symmetry = _parse_header(rd)
     entries = rd.data_lines(1)
@@ -99,6 +102,10 @@ def load_matrix_market(path) -> CsrMatrix:
         mirror = r != c
         r, c, v = (np.concatenate([r, c[mirror]]), np.concatenate([c, r[mirror]]),
                    np.concatenate([v, v[mirror]]))
+    if device:
+        import torch
+
+        r, c, v = (torch.from_numpy(np.ascontiguousarray(t)).cuda() for t in (r, c, v))
     return CsrMatrix.from_triplets(n_rows, r, c, v)
 
 

@@ -151,3 +151,16 @@ def test_from_triplets_short_row_boundary(row_len):
     erp, ecol, ev = O.from_triplets(n, rows, cols, vals)
     assert np.array_equal(rp.astype(np.int64), erp) and np.array_equal(col.astype(np.int64), ecol)
     assert val.tobytes() == ev.tobytes()
+
+
+@pytest.mark.gpu
+def test_load_matrix_market_device_build(tmp_path):
+    import paper_2205_01598_b200 as lm
+
+    p = tmp_path / "s.mtx"
+    p.write_text("%%MatrixMarket matrix coordinate real symmetric\n4 4 6\n"
+                 "1 1 2.5\n2 1 -1e-17\n2 1 1.0\n3 3 4\n4 2 0.125\n4 4 1e16\n")
+    host = lm.load_matrix_market(p)
+    dev = lm.load_matrix_market(p, device=True)
+    assert np.array_equal(dev.row_ptr, host.row_ptr) and np.array_equal(dev.col, host.col)
+    assert dev.val.tobytes() == host.val.tobytes()
