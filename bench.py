@@ -250,7 +250,7 @@ def run_ours(args, cfgd):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     k = cfgd["k"]
     t0 = time.perf_counter()
-    a = lm.gen_stencil_3d(cfgd["n"], 2)
+    a = lm.gen_stencil_3d(cfgd["n"], 2, device=True)  # CRS built in HBM (bitwise = host build)
     t_gen = time.perf_counter() - t0
     n, nnz = a.n_rows, a.n_nz
     x = np.random.default_rng(0).uniform(-1.0, 1.0, n)

@@ -29,8 +29,11 @@ FD_WEIGHTS = {
 }
 
 
-def grid_operator(shape, couplings, periodic=False, diagonal=None) -> CsrMatrix:
+def grid_operator(shape, couplings, periodic=False, diagonal=None, device=False) -> CsrMatrix:
     """Operator on a lexicographic grid.
+
+    device=True builds the CRS from the triplets in HBM (lmpk_csr_from_triplets,
+    bit-exact with the host build).
 
     ``couplings`` is a list of (offset tuple, weight); a zero offset adds to the
     diagonal.  Off-grid neighbours are dropped (Dirichlet) or wrapped
@@ -56,7 +59,12 @@ def grid_operator(shape, couplings, periodic=False, diagonal=None) -> CsrMatrix:
         rows.append(ids)
         cols.append(ids)
         vals.append(np.asarray(diagonal, dtype=np.float64))
-    return CsrMatrix.from_triplets(n, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
+    r, c, v = np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
+    if device:
+        import torch
+
+        r, c, v = (torch.from_numpy(t).cuda() for t in (r, c, v))
+    return CsrMatrix.from_triplets(n, r, c, v)
 
 
 def gen_stencil_2d7pt(nx: int, ny: int) -> CsrMatrix:
@@ -68,7 +76,7 @@ def gen_stencil_2d7pt(nx: int, ny: int) -> CsrMatrix:
     return grid_operator((nx, ny), [((0, 0), 7.0)] + [(o, -1.0) for o in offs])
 
 
-def gen_stencil_3d(n: int, order: int = 2) -> CsrMatrix:
+def gen_stencil_3d(n: int, order: int = 2, device: bool = False) -> CsrMatrix:
     """Finite-difference -Laplacian of the given spatial order on an n^3 grid,
     Dirichlet truncation (stencils.py:53-80)."""
     if order not in FD_WEIGHTS:
@@ -83,7 +91,7 @@ def gen_stencil_3d(n: int, order: int = 2) -> CsrMatrix:
                 off = [0, 0, 0]
                 off[axis] = sign * dist
                 couplings.append((tuple(off), w[dist]))
-    return grid_operator((n, n, n), couplings)
+    return grid_operator((n, n, n), couplings, device=device)
 
 
 def stencil_3d_nnz(n: int, order: int = 2) -> int:

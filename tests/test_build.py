@@ -164,3 +164,14 @@ def test_load_matrix_market_device_build(tmp_path):
     dev = lm.load_matrix_market(p, device=True)
     assert np.array_equal(dev.row_ptr, host.row_ptr) and np.array_equal(dev.col, host.col)
     assert dev.val.tobytes() == host.val.tobytes()
+
+
+@pytest.mark.gpu
+def test_gen_stencil_3d_device_build():
+    import paper_2205_01598_b200 as lm
+
+    host = lm.gen_stencil_3d(20, 4)
+    dev = lm.gen_stencil_3d(20, 4, device=True)
+    assert dev.n_nz == host.n_nz == lm.stencil_3d_nnz(20, 4)
+    assert np.array_equal(dev.row_ptr, host.row_ptr) and np.array_equal(dev.col, host.col)
+    assert dev.val.tobytes() == host.val.tobytes()
