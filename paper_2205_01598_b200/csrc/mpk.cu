@@ -833,14 +833,19 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
 }
 
 // Ring walk: super-tiles (runs of consecutive tiles of ~tile_nnz_hint
-// nonzeros, default 64K), their dependency ranges in tiles, and the items
+// nonzeros, default 32K: cfg2's ~34K-nonzero tiles become one super-tile
+// each, 0.447 vs 0.470 ms for the former 64K default that paired them; cfg5
+// unchanged (309 vs 313 us), cfg1 67 -> 50 us; LMPK_SUPER_NNZ overrides), their
+// dependency ranges in tiles, and the items
 // (T, power) in skewed diagonal key order (T + g*M, g), M = D + slack with D
 // the max forward reach in super-tiles: every dependency of an item has a
 // smaller key (deadlock freedom, see mpk_ring_kernel).
 static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const lmpk_tiling_params& prm,
                               lmpk_tiling_info* info, lmpk_tiling** out, cudaStream_t st) {
   const int32_t nt = T->info.n_tiles;
-  const int64_t target = prm.tile_nnz_hint > 0 ? prm.tile_nnz_hint : 65536;
+  int64_t target = 32768;
+  if (prm.tile_nnz_hint > 0) target = prm.tile_nnz_hint;
+  else if (const char* e = getenv("LMPK_SUPER_NNZ")) target = std::max(1, atoi(e));
   std::vector<int32_t> tE(nt);
   LMPK_CHECK_CUDA(cudaMemcpyAsync(tE.data(), T->d_tile_E, size_t(nt) * 4, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
