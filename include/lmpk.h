@@ -148,6 +148,8 @@ typedef struct lmpk_tiling_info {
   int32_t dict_tiles;    /* compressed tiles with a value dictionary (<= 256)   */
   int32_t super_tiles;   /* ring walk (mode 3): work items per power = runs of  */
                          /* consecutive tiles streamed through the smem ring   */
+  int64_t lean_bytes;    /* ring walk: width-sorted lean copy of the blocks    */
+                         /* (0: the tiling runs the general ring kernel)      */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */

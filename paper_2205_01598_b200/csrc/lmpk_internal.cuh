@@ -113,6 +113,13 @@ struct lmpk_tiling {
   int32_t max_block = 0;           // largest tile block (bytes)
   int32_t slots = 1;               // staged items held per CTA
   std::vector<int32_t> h_tile_row, h_dep_lo, h_dep_hi;
+  // lean blocks (lean_kernel.cuh): width-sorted units, built when every tile
+  // is a compressed tile of width <= 8 with one value format
+  unsigned char* d_lean = nullptr;
+  int64_t* d_lean_ofs = nullptr;   // [n_tiles + 1]
+  uint8_t* d_rowlen = nullptr;     // [n] row lengths (slow path of padded rows)
+  int32_t lean_vd = -1;            // -1 none, 0 raw values, 1 dictionary
+  int64_t lean_bytes = 0;
 };
 
 namespace lmpk {

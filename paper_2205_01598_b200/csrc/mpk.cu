@@ -1,6 +1,6 @@
 // mpk.cu -- host side of the level-blocked MPK: tiling, block layout, launch.
 // The device code is in mpk_kernel.cuh (header comment there).
-#include "mpk_kernel.cuh"
+#include "lean_kernel.cuh"
 
 namespace lmpk {
 
@@ -276,6 +276,16 @@ static int dmalloc(T** p, size_t count) {
   return LMPK_OK;
 }
 
+// lean ring walk (mpk_lean.cu)
+int64_t lean_tile_bytes(const std::vector<int32_t>& width, int32_t s0, int32_t s1, bool vd);
+int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr, const int32_t* col,
+               const double* val, const std::vector<int32_t>& first, const std::vector<int32_t>& width,
+               const int32_t* d_wmin, const std::vector<int32_t>& tmode, const std::vector<int32_t>& tdict,
+               const uint64_t* d_dict_tab, const int32_t* d_width, int64_t cap, cudaStream_t st);
+void lean_free(lmpk_tiling* T);
+int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool gen,
+                int grid, cudaStream_t st);
+
 // one explicit instantiation per variant (mpk_k_*.cu: separate, parallel TUs)
 const void* mpk_group_fn_re();
 const void* mpk_group_fn_rf();
@@ -459,6 +469,7 @@ extern "C" int lmpk_tiling_destroy(lmpk_tiling* t) {
   cudaFree(t->d_items);
   cudaFree(t->d_progress);
   cudaFree(t->d_blocks);
+  lean_free(t);
   delete t;
   return LMPK_OK;
 }
@@ -571,7 +582,7 @@ static void partition_range(const std::vector<int32_t>& width, int32_t s0, int32
     while (s + ns < s1) {
       const int64_t e2 = E + int64_t(width[s + ns]) * 32;
       const size_t u = xc ? xc->add(s + ns) : 0;
-      const int64_t need = cost(ns + 1, e2) + (xc ? xc->bytes() : 0);
+      const int64_t need = cost(s, ns + 1, e2) + (xc ? xc->bytes() : 0);
       if (ns > 0 && (need > cap || e2 > e_cap)) {
         if (xc) xc->undo(u);
         break;
@@ -603,7 +614,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   std::vector<int32_t> tdict;   // per tile: index into the dictionary table (dict tiles)
   uint64_t* d_dict_tab = nullptr;
   int32_t* d_tile_dict = nullptr;
-  auto plain_cost = [](int32_t ns, int64_t E) { return blk_bytes(ns, E, 0); };
+  auto plain_cost = [](int32_t, int32_t ns, int64_t E) { return blk_bytes(ns, E, 0); };
   // x staging: a slot holds [block | x buffer] (per-tile split, see XCounter)
   XCounter xcnt;
   XCounter* xc = nullptr;
@@ -615,8 +626,22 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     xc = &xcnt;
   }
   if (fit16 && S > 0) {
-    auto dict_cost = [](int32_t ns, int64_t E) { return cblk_bytes(ns, kDictMax, E, true, 0); };
-    auto raw_cost = [](int32_t ns, int64_t E) { return cblk_bytes(ns, 0, E, false, 0); };
+    // a compressed tile must also fit the slot as a lean block (lean_kernel.cuh)
+    std::vector<int64_t> pre_d(S + 1, 0), pre_r(S + 1, 0);
+    for (int32_t s = 0; s < S; ++s) {
+      const int w = std::min(width[s], 9);
+      pre_d[s + 1] = pre_d[s] + lean_col_bytes(w) + lean_code_bytes(w);
+      pre_r[s + 1] = pre_r[s] + lean_col_bytes(w) + lean_raw_bytes(w);
+    }
+    auto lean_cost = [&](const std::vector<int64_t>& pre, int32_t s0, int32_t ns) {
+      return (int64_t(kLeanRec) + 16 * int64_t(ns) + pre[s0 + ns] - pre[s0] + 127) & ~int64_t(127);
+    };
+    auto dict_cost = [&](int32_t s0, int32_t ns, int64_t E) {
+      return std::max(cblk_bytes(ns, kDictMax, E, true, 0), lean_cost(pre_d, s0, ns));
+    };
+    auto raw_cost = [&](int32_t s0, int32_t ns, int64_t E) {
+      return std::max(cblk_bytes(ns, 0, E, false, 0), lean_cost(pre_r, s0, ns));
+    };
     // pass 1: runs of equal fit16, compressed runs cut for the dictionary format
     std::vector<int32_t> f1;
     std::vector<int64_t> E1;
@@ -671,7 +696,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
         continue;
       }
       const int32_t k = nd[li];
-      if (k >= 0 && dict_cost(s1 - s0, E1[t]) <= cap) {
+      if (k >= 0 && dict_cost(s0, s1 - s0, E1[t]) <= cap) {
         first.push_back(s0);
         Es.push_back(E1[t]);
         tmode.push_back(kModeC16 | kModeDict | (k << 8));
@@ -682,7 +707,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
         for (size_t i = b; i < first.size(); ++i) {
           const int32_t a0 = first[i], a1 = i + 1 < first.size() ? first[i + 1] : s1;
           // a single slice too large for a slot stays plain (read from global)
-          tmode.push_back(raw_cost(a1 - a0, Es[i]) <= cap ? kModeC16 : 0);
+          tmode.push_back(raw_cost(a0, a1 - a0, Es[i]) <= cap ? kModeC16 : 0);
           tdict.push_back(-1);
         }
       }
@@ -815,6 +840,11 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
                                                              T->d_dep_hi);
   launch_count_add(ctx, 1);
   LMPK_CHECK_CUDA(cudaGetLastError());
+  if (n_comp == nt && !xc) {
+    std::vector<int32_t> tfirst(first.begin(), first.begin() + nt);
+    LMPK_TRY(lean_build(ctx, T, n, row_ptr, col, val, tfirst, width, d_wmin, tmode, tdict, d_dict_tab, d_width, cap,
+                        st));
+  }
   T->h_dep_lo.resize(nt);
   T->h_dep_hi.resize(nt);
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->h_dep_lo.data(), T->d_dep_lo, nt * 4, cudaMemcpyDeviceToHost, st));
@@ -880,10 +910,17 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
   T->info.max_fwd_reach = D;
   T->info.super_tiles = ns;
   const int64_t M = int64_t(D) + slack;
+  // power passes: the powers run in passes of qp consecutive powers, each
+  // pass a diagonal wavefront of its own (key pass * BIG + s + (g mod qp) M):
+  // fewer powers in flight shrink the window of blocks and vectors the L2
+  // must hold between a tile's consecutive powers
+  int32_t qp = G;
+  if (const char* e = getenv("LMPK_PASS_POWERS")) qp = std::max(1, std::min(G, atoi(e)));
+  const int64_t BIG = int64_t(ns) + int64_t(qp) * M + 1;
   std::vector<int64_t> keys;
   keys.reserve(int64_t(ns) * G);
   for (int32_t s = 0; s < ns; ++s)
-    for (int32_t g = 0; g < G; ++g) keys.push_back(((s + g * M) << 8) | g);
+    for (int32_t g = 0; g < G; ++g) keys.push_back((((g / qp) * BIG + s + (g % qp) * M) << 8) | g);
   std::vector<int32_t> order(keys.size());
   std::iota(order.begin(), order.end(), 0);
   std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return keys[a] < keys[b]; });
@@ -1387,6 +1424,11 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
         uniform = (plain && !cplx && T->slots == 2) ? 3 : 1;  // the plain kernel assumes the 2-piece ring
       else if (T->info.compressed_tiles == T->info.n_tiles && T->info.dict_tiles == 0)
         uniform = 2;
+    }
+    if (T->d_lean && T->staged_tiles == 0 && T->slots == 2 && !getenv("LMPK_NO_LEAN_RUN")) {
+      bool plain = !use_acc;
+      for (int i = 0; i < P; ++i) plain = plain && C.kernel[i] == LMPK_KERNEL_SPMV;
+      return launch_lean(ctx, T, Pm, C, cplx, exact, !plain, grid, st);
     }
     return launch_ring(ctx, Pm, C, cplx, exact, T->info.max_row_nnz > 8, uniform, grid, T->info.smem_bytes, st);
   }
