@@ -200,6 +200,9 @@ int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* tiling, double* y, int64_t ld
  * launches (watchdog: a dependency spin exceeded its bound, the analogue of
  * the reference's join watchdog executor.py:173-179). */
 int lmpk_ctx_check(lmpk_ctx* ctx, void* stream);
+/* Test hook: set the ctx's epoch counter (the next MPK launch uses epoch + 1;
+ * values >= 2^24 - 1 make it wrap).  Returns the previous value. */
+int64_t lmpk_ctx_set_epoch(lmpk_ctx* ctx, int64_t epoch);
 
 /* ---------------------------------------------------------------- BFS levels + permutation
  * Level construction of levels.py:48-114: BFS distance classes of the

@@ -89,6 +89,7 @@ SIGNATURES = {
     "lmpk_ctx_destroy": (_int, [_vp]),
     "lmpk_ctx_launch_count": (_i64, [_vp]),
     "lmpk_ctx_check": (_int, [_vp, _vp]),
+    "lmpk_ctx_set_epoch": (_i64, [_vp, _i64]),
     "lmpk_ctx_profile": (_int, [_vp, _vp, _int]),
     "lmpk_ctx_trace": (_int, [_vp, _vp, _i64]),
     "lmpk_spmv_rows": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _int, _vp]),
@@ -108,8 +109,6 @@ SIGNATURES = {
     "lmpk_level_nnz": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "lmpk_segment_col_range": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     # micro-benchmarks (not part of the reference-facing ABI)
-    "lmpk_probe_read_bw": (_int, [_vp, _i64, _int, _int, ctypes.POINTER(ctypes.c_double)]),
-    "lmpk_probe_flag_latency": (_int, [_vp, _int, ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None

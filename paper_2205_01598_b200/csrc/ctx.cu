@@ -140,6 +140,7 @@ extern "C" int lmpk_ctx_destroy(lmpk_ctx* c) {
                       &c->s_d,     &c->s_e, &c->s_f, &c->s_g, &c->s_heavy};
   for (Scratch* s : pools) s->release();
   if (c->queue_ctr) cudaFree(c->queue_ctr);
+  if (c->heavy_ev) cudaEventDestroy(c->heavy_ev);
   if (c->prof) cudaFree(c->prof);
   if (c->err.host) cudaFreeHost(const_cast<int*>(c->err.host));
   delete c;

@@ -71,9 +71,11 @@ struct lmpk_ctx {
   lmpk::DeviceFlags err;   // watchdog / device error word
   // MPK synchronisation state (epoch-tagged counters, never memset per call)
   uint32_t epoch = 0;
+  uint32_t wrap_gen = 0;   // bumped when the epoch counter wraps
   // scratch pools
   lmpk::Scratch s_small, s_a, s_b, s_c, s_d, s_e, s_f, s_g;
   lmpk::Scratch s_heavy;  // CRS kernel: list of heavy rows (count + indices)
+  cudaEvent_t heavy_ev = nullptr;  // recorded after the last kernel reading s_heavy
   uint64_t* queue_ctr = nullptr;  // monotone work-queue counter (device)
   uint64_t queue_base = 0;        // host mirror of the counter value
   unsigned long long* prof = nullptr;  // phase counters when LMPK_PROFILE is set
@@ -120,6 +122,7 @@ struct lmpk_tiling {
   uint8_t* d_rowlen = nullptr;     // [n] row lengths (slow path of padded rows)
   int32_t lean_vd = -1;            // -1 none, 0 raw values, 1 dictionary
   int64_t lean_bytes = 0;
+  uint32_t wrap_gen = 0;           // ctx wrap generation its progress words belong to
 };
 
 namespace lmpk {

@@ -1384,9 +1384,16 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
     return LMPK_OK;
   }
   ctx->epoch += 1;
-  if (ctx->epoch >= (1u << 24)) {  // counter wrap: reset progress words
-    LMPK_CHECK_CUDA(cudaMemsetAsync(Tm->d_progress, 0, size_t(T->info.n_tiles) * 4, st));
+  if (ctx->epoch >= (1u << 24)) {  // counter wrap: a new generation of epochs
     ctx->epoch = 1;
+    ctx->wrap_gen += 1;
+  }
+  // a tiling whose progress words predate the last wrap (possibly many
+  // launches of other tilings ago) would hold tags up to 2^31 that pass
+  // every wait of the new generation: clear them first
+  if (Tm->wrap_gen != ctx->wrap_gen) {
+    LMPK_CHECK_CUDA(cudaMemsetAsync(Tm->d_progress, 0, size_t(T->info.n_tiles) * 4, st));
+    Tm->wrap_gen = ctx->wrap_gen;
   }
   Pm.epoch_base = ctx->epoch * kEpochStride;
   Pm.queue_base = ctx->queue_base;
@@ -1437,6 +1444,13 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
   // consumers, so no slot buffers -- the unified L1 is left to the gathers.
   const bool no_tma = (flags & LMPK_FLAG_NO_TMA) != 0;
   return launch_group(ctx, Pm, C, cplx, exact, true, grid, no_tma ? 0 : T->info.smem_bytes, st);
+}
+
+extern "C" int64_t lmpk_ctx_set_epoch(lmpk_ctx* ctx, int64_t epoch) {
+  if (!ctx) return -1;
+  const int64_t old = ctx->epoch;
+  ctx->epoch = static_cast<uint32_t>(std::max<int64_t>(0, std::min<int64_t>(epoch, (1 << 24) - 1)));
+  return old;
 }
 
 // Host-side check after the caller synchronized the stream.

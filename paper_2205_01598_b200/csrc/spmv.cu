@@ -96,6 +96,11 @@ static int spmv_launch(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col
 // heavy-row list of [r0, r1) in the ctx scratch (count, then row indices)
 static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t r1, int32_t** out,
                       int32_t* n_heavy, cudaStream_t st) {
+  // the list is shared ctx scratch: a call on another stream may still be
+  // reading it -- order this call (and any reallocation) after that reader
+  if (!ctx->heavy_ev) LMPK_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->heavy_ev, cudaEventDisableTiming));
+  if (ctx->s_heavy.bytes < (size_t(r1 - r0) + 1) * 4) LMPK_CHECK_CUDA(cudaEventSynchronize(ctx->heavy_ev));
+  LMPK_CHECK_CUDA(cudaStreamWaitEvent(st, ctx->heavy_ev, 0));
   LMPK_TRY(ctx->s_heavy.ensure((size_t(r1 - r0) + 1) * 4));
   int32_t* list = reinterpret_cast<int32_t*>(ctx->s_heavy.ptr);
   LMPK_CHECK_CUDA(cudaMemsetAsync(list, 0, 4, st));
@@ -127,7 +132,9 @@ extern "C" int lmpk_spmv_rows(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, 
   int32_t* heavy = nullptr;
   int32_t n_heavy = 0;
   LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, &n_heavy, st));
-  return spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, n_heavy, st);
+  LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, n_heavy, st));
+  LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
+  return LMPK_OK;
 }
 
 extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr,
@@ -145,5 +152,6 @@ extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_pt
   for (int32_t p = 1; p <= p_m; ++p)
     LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy,
                          n_heavy, st));
+  LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
   return LMPK_OK;
 }

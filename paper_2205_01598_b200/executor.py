@@ -122,18 +122,15 @@ def _schedule(plan: ExecPlan, til, yv, cfg, av, use_acc, cplx, flags):
     pays when the level window fits the L2 (cfg2, cfg5 shapes); for very wide
     levels (cfg3 27-point 160^3: 20 MB per level) the blocks are re-read from
     HBM at every power anyway and the dependency-free sweep is faster.  Chosen
-    once per plan by timing one call of each on scratch copies; LMPK_SCHEDULE=
-    walk|sweep|crs forces it."""
+    once per (plan, complex, plain) by timing each candidate on scratch copies
+    (min of 3 calls); LMPK_SCHEDULE=walk|sweep|crs forces it."""
     forced = os.environ.get("LMPK_SCHEDULE", "auto")
     plain = not cplx and not use_acc and not np.any(plan.kernel != 0) and K.EXACT_DEFAULT
     if forced in ("walk", "sweep") or (forced == "crs" and plain):
         return forced
-    got = plan.schedule_choice(cplx)
+    got = plan.schedule_choice(cplx, plain)
     if got is not None:
         return got
-    if plan.a.n_nz < 4_000_000:  # small problems: latency-bound either way, keep the walk
-        plan.set_schedule_choice(cplx, "walk")
-        return "walk"
     torch = _torch()
     ys = yv.clone()
     as_ = av.clone() if av is not None else None
@@ -149,21 +146,27 @@ def _schedule(plan: ExecPlan, til, yv, cfg, av, use_acc, cplx, flags):
                 K.mpk_run(til, ys, cfg, acc=as_, use_acc=use_acc, complex_state=cplx, flags=flags | f,
                           check_errors=False)
         once()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        once()
-        e1.record()
-        e1.synchronize()
-        times[name] = e0.elapsed_time(e1)
+        best = None
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            once()
+            e1.record()
+            e1.synchronize()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        times[name] = best
     del ys, as_
     choice = min(times, key=times.get)
-    plan.set_schedule_choice(cplx, choice)
+    plan.set_schedule_choice(cplx, choice, plain)
     return choice
 
 
-def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
-    """Run one plan on device buffers; returns device seconds."""
+def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0, sync=True):
+    """Run one plan on device buffers; returns device seconds (with
+    ``sync=False``: a callable that waits for the launches and returns them,
+    so the caller can queue copies behind the kernel first)."""
     torch = _torch()
     cplx = yd.is_complex()
     yv = torch.view_as_real(yd).reshape(yd.shape[0], -1) if cplx else yd
@@ -197,10 +200,14 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0):
                 f = flags | (_lib.FLAG_SWEEP if sched == "sweep" else 0)
                 K.mpk_run(til, yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=f)
     e1.record()
-    e1.synchronize()
-    ctx = _lib.context()
-    _lib.check(ctx.lib.lmpk_ctx_check(ctx.handle, _lib.stream_handle()), "run_plan")
-    return e0.elapsed_time(e1) * 1e-3
+
+    def finish():
+        e1.synchronize()
+        ctx = _lib.context()
+        _lib.check(ctx.lib.lmpk_ctx_check(ctx.handle, _lib.stream_handle()), "run_plan")
+        return e0.elapsed_time(e1) * 1e-3
+
+    return finish() if sync else finish
 
 
 _PLAN_FIELDS = ("variant", "p_m", "workers", "n_rows", "items", "barrier", "row_start", "row_end",
@@ -231,13 +238,45 @@ def adopt_plan(ref_plan) -> ExecPlan:
     return ExecPlan(**kw)
 
 
+def _slot_roles(plan: ExecPlan, n_slots):
+    """(input slots, output slots) of a plan's per-power configuration: a
+    slot is an input when some power reads it (in_slot / prev_slot) before
+    any earlier power wrote it; outputs are the out_slots."""
+    cfg = plan.power_config()
+    written, inputs = set(), set()
+    for i in range(cfg.n_powers):
+        for sl in (cfg.in_slot[i], cfg.prev_slot[i] if cfg.kernel[i] == 1 else None):
+            if sl is not None and sl not in written:
+                inputs.add(int(sl))
+        written.add(int(cfg.out_slot[i]))
+    inputs.add(0)
+    return sorted(s_ for s_ in inputs if s_ < n_slots), sorted(s_ for s_ in written if s_ < n_slots)
+
+
+def _host_pinned(shape, dtype):
+    """A numpy array in page-locked host memory (torch's caching host
+    allocator), so device<->host copies of it run at full PCIe rate."""
+    torch = _torch()
+    tdt = torch.complex128 if np.dtype(dtype) == np.complex128 else torch.float64
+    t = torch.empty(shape, dtype=tdt, pin_memory=True)
+    return t, t.numpy()
+
+
 def run_plan(plan: ExecPlan, x=None, y=None, acc=None, use_acc=False, timeout=None):
     """Execute a plan on the GPU; returns an MpkResult with the power vectors.
 
     Semantics of executor.py:213-230: with ``y=None`` a PowerVectors is
-    allocated and y[0] = x; otherwise ``y`` (host or device) is updated in
-    place.  ``acc`` (with use_acc) is accumulated in place.  The device
-    watchdog (8 s without progress) replaces the reference's join timeout.
+    allocated and y[0] = x; otherwise ``y`` (any object with a ``data``
+    array of shape (slots, n): this package's PowerVectors, the reference's,
+    a numpy array or a CUDA tensor) is updated in place.  ``acc`` (with
+    use_acc) is accumulated in place.  The device watchdog (8 s without
+    progress) replaces the reference's join timeout.
+
+    Host data moves only where the plan needs it: the input slots go up
+    (slot 0 = x, plus Chebyshev state slots), the output slots come down,
+    asynchronously on the launch stream; a host PowerVectors that run_plan
+    allocates lives in page-locked memory, and its copy of x is written on
+    the CPU while the device works.
     """
     del timeout  # device-side watchdog
     torch = _torch()
@@ -246,26 +285,61 @@ def run_plan(plan: ExecPlan, x=None, y=None, acc=None, use_acc=False, timeout=No
     if y is None:
         if x is None:
             raise ValueError("either x or y must be given")
-        xa = x if isinstance(x, torch.Tensor) else np.asarray(x, dtype=np.float64)
-        on_dev = isinstance(xa, torch.Tensor)
-        dt = np.complex128 if (on_dev and xa.is_complex()) or (not on_dev and np.iscomplexobj(xa)) else np.float64
-        pv = PowerVectors(n, plan.p_m, device=on_dev, dtype=dt)
-        pv.data[0] = xa
+        on_dev = isinstance(x, torch.Tensor) and x.is_cuda
+        if on_dev:
+            dt = np.complex128 if x.is_complex() else np.float64
+            pv = PowerVectors(n, plan.p_m, device=True, dtype=dt)
+            pv.data[0] = x
+            host_x = None
+        else:
+            xa = x.numpy() if isinstance(x, torch.Tensor) else np.asarray(x)
+            dt = np.complex128 if np.iscomplexobj(xa) else np.float64
+            xa = np.ascontiguousarray(xa, dtype=dt)
+            if xa.shape != (n,):
+                raise ValueError(f"x length {xa.shape} must equal n_rows {n}")
+            pin_t, arr = _host_pinned((plan.p_m + 1, n), dt)
+            pv = PowerVectors(n, plan.p_m, data=arr)
+            pv._pinned = pin_t
+            host_x = xa
     else:
         pv = y
-    if pv.on_device:
-        yd = pv.data
-    else:
-        yd = _to_device_f64(pv.data)
+        host_x = None
+    data = pv if isinstance(pv, (np.ndarray, torch.Tensor)) else pv.data
+    on_dev = isinstance(data, torch.Tensor) and data.is_cuda
     accd = None
     if use_acc:
         if acc is None:
             raise ValueError("use_acc requires acc")
-        accd = acc if isinstance(acc, torch.Tensor) else _to_device_f64(acc)
-    seconds = _launch(plan, yd, accd, use_acc)
-    if not pv.on_device:
-        pv.data[...] = yd.cpu().numpy()
-    if use_acc and not isinstance(acc, torch.Tensor):
+        accd = acc if isinstance(acc, torch.Tensor) and acc.is_cuda else _to_device_f64(np.asarray(acc))
+    if on_dev:
+        seconds = _launch(plan, data, accd, use_acc)
+    else:
+        host = data if isinstance(data, np.ndarray) else np.asarray(data)
+        slots = host.shape[0]
+        ins, outs = _slot_roles(plan, slots)
+        yd = torch.empty(host.shape, dtype=torch.complex128 if np.iscomplexobj(host) else torch.float64,
+                         device="cuda")
+        rest = [s_ for s_ in range(slots) if s_ not in ins and s_ not in outs]
+        for s_ in ins:  # slot 0 straight from the caller's x when run_plan allocated y
+            src = host_x if (s_ == 0 and host_x is not None) else host[s_]
+            yd[s_].copy_(torch.from_numpy(np.ascontiguousarray(src)), non_blocking=True)
+        if rest:
+            yd[rest] = torch.from_numpy(host[rest]).cuda(non_blocking=True)
+        seconds = _launch(plan, yd, accd, use_acc, sync=False)
+        pinned = getattr(pv, "_pinned", None)
+        if pinned is not None:
+            for s_ in outs:
+                pinned[s_].copy_(yd[s_], non_blocking=True)
+            if host_x is not None:
+                host[0] = host_x  # the reference's y[0] = x, on the CPU while the copies run
+            seconds = seconds()
+            torch.cuda.current_stream().synchronize()
+        else:
+            seconds = seconds()
+            out_h = yd[outs].cpu().numpy()
+            for i, s_ in enumerate(outs):
+                host[s_] = out_h[i]
+    if use_acc and not (isinstance(acc, torch.Tensor) and acc.is_cuda):
         acc[...] = accd.cpu().numpy()
     e2e = time.perf_counter() - t_start
     return MpkResult(pv, seconds, plan.variant, plan.workers, plan, e2e_seconds=e2e)

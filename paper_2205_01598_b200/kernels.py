@@ -277,17 +277,3 @@ def segment_col_range(a: DeviceCsr, seg_ptr, stream=None):
                                          ptr(mn), ptr(mx), stream_handle(stream)),
           "segment_col_range")
     return mn[:G].cpu().numpy(), mx[:G].cpu().numpy()
-
-
-def probe_read_bw(nbytes, reps=10, trials=5):
-    ctx = context()
-    g = ctypes.c_double()
-    check(ctx.lib.lmpk_probe_read_bw(ctx.handle, int(nbytes), int(reps), int(trials), ctypes.byref(g)))
-    return g.value
-
-
-def probe_flag_latency(iters=10000):
-    ctx = context()
-    g = ctypes.c_double()
-    check(ctx.lib.lmpk_probe_flag_latency(ctx.handle, int(iters), ctypes.byref(g)))
-    return g.value

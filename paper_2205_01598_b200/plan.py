@@ -112,16 +112,19 @@ class ExecPlan:
                 self._tiling[key] = None
         return self._tiling[key]
 
-    def schedule_choice(self, complex_state=False):
-        """'walk' (level-blocked wavefront) or 'sweep' (dependency-free power
-        sweeps on the same tiles) -- identical bits, chosen per plan by timing
-        both once (executor._launch); None until measured."""
-        return (self._sched or {}).get(bool(complex_state))
+    def schedule_choice(self, complex_state=False, plain=False):
+        """'walk' (level-blocked wavefront), 'sweep' (dependency-free power
+        sweeps on the same tiles) or, for plain real MPK only, 'crs' (the CRS
+        sweeps of run_baseline) -- identical bits, chosen per plan and per
+        call kind by timing once (executor._launch); None until measured.
+        The key includes ``plain``: a plan re-used with Chebyshev slots or an
+        accumulator never inherits the plain-only 'crs' choice."""
+        return (self._sched or {}).get((bool(complex_state), bool(plain)))
 
-    def set_schedule_choice(self, complex_state, choice):
+    def set_schedule_choice(self, complex_state, choice, plain=False):
         if self._sched is None:
             self._sched = {}
-        self._sched[bool(complex_state)] = choice
+        self._sched[(bool(complex_state), bool(plain))] = choice
 
     def power_config(self, acc_coef_im=None):
         """Per-power kernel configuration for liblmpk.  The reference stores it

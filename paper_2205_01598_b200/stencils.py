@@ -110,13 +110,13 @@ def gen_laplace_2d5pt(nx: int, ny: int) -> CsrMatrix:
     return grid_operator((nx, ny), [((0, 0), 4.0)] + [(o, -1.0) for o in offs])
 
 
-def gen_stencil_3d27pt(n: int, perturb: float = 0.01, seed: int = 0) -> CsrMatrix:
+def gen_stencil_3d27pt(n: int, perturb: float = 0.01, seed: int = 0, device: bool = False) -> CsrMatrix:
     """Config 3: 27-point stencil on n^3 (Dirichlet), diag 26.0, off -1.0, plus a
     seeded uniform[-perturb, perturb] perturbation added to every stored entry
     in canonical CRS order (pattern symmetric, values not)."""
     couplings = [(o, 26.0 if o == (0, 0, 0) else -1.0)
                  for o in itertools.product((-1, 0, 1), repeat=3)]
-    a = grid_operator((n, n, n), couplings)
+    a = grid_operator((n, n, n), couplings, device=device)
     if perturb:
         rng = np.random.default_rng(seed)
         a = CsrMatrix(a.n_rows, a.row_ptr, a.col, a.val + rng.uniform(-perturb, perturb, a.n_nz))
@@ -124,7 +124,7 @@ def gen_stencil_3d27pt(n: int, perturb: float = 0.01, seed: int = 0) -> CsrMatri
 
 
 def gen_rmat(scale: int, edge_factor: int = 8, a: float = 0.57, b: float = 0.19,
-             c: float = 0.19, seed: int = 1) -> CsrMatrix:
+             c: float = 0.19, seed: int = 1, device: bool = False) -> CsrMatrix:
     """Config 4: R-MAT graph (2**scale vertices, edge_factor * 2**scale edges),
     symmetrised with duplicates merged, self-loops added, values uniform[0,1]
     (seeded, canonical CRS order) then each row normalised to sum 1."""
@@ -141,17 +141,23 @@ def gen_rmat(scale: int, edge_factor: int = 8, a: float = 0.57, b: float = 0.19,
         dst |= right.astype(np.int64) << bit
     rows = np.concatenate([src, dst, np.arange(n)])
     cols = np.concatenate([dst, src, np.arange(n)])
-    pat = CsrMatrix.from_triplets(n, rows, cols, np.ones(rows.size))
+    ones = np.ones(rows.size)
+    if device:
+        import torch
+
+        rows, cols, ones = (torch.from_numpy(t).cuda() for t in (rows, cols, ones))
+    pat = CsrMatrix.from_triplets(n, rows, cols, ones)
     v = rng.uniform(0.0, 1.0, pat.n_nz)
     rs = np.add.reduceat(v, pat.row_ptr[:-1]) if pat.n_nz else np.zeros(n)
     v = v / np.repeat(rs, np.diff(pat.row_ptr))
     return CsrMatrix(n, pat.row_ptr, pat.col, v)
 
 
-def gen_anderson_3d(n: int, disorder: float = 16.5, seed: int = 0, hopping: float = -1.0) -> CsrMatrix:
+def gen_anderson_3d(n: int, disorder: float = 16.5, seed: int = 0, hopping: float = -1.0,
+                    device: bool = False) -> CsrMatrix:
     """Config 5: 3D Anderson Hamiltonian on an n^3 periodic grid: hopping to the
     six wrapped neighbours, on-site energies uniform[-W/2, W/2] (seeded)."""
     rng = np.random.default_rng(seed)
     eps = rng.uniform(-disorder / 2, disorder / 2, n**3)
     offs = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
-    return grid_operator((n, n, n), [(o, hopping) for o in offs], periodic=True, diagonal=eps)
+    return grid_operator((n, n, n), [(o, hopping) for o in offs], periodic=True, diagonal=eps, device=device)

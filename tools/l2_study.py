@@ -8,12 +8,14 @@ from oracle import levelmpk_oracle as O
 N = int(os.environ.get("N", "200")); k = int(os.environ.get("K", "8"))
 ctx = _lib.context()
 if os.environ.get("PROBES", "1") == "1":
+    # micro-benchmarks live outside the product library: make -C tools/ubench
+    probe = ctypes.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "ubench", "libprobe.so"))
     for mb in (8, 16, 32, 48, 64, 96, 128, 256, 1024):
         g = ctypes.c_double()
-        ctx.lib.lmpk_probe_read_bw(ctx.handle, mb << 20, 20 if mb < 512 else 3, 3, ctypes.byref(g))
+        probe.lmpk_probe_read_bw(ctypes.c_void_p(ctx.handle.value if hasattr(ctx.handle, 'value') else ctx.handle), ctypes.c_int64(mb << 20), 20 if mb < 512 else 3, 3, ctypes.byref(g))
         print(f"read bw {mb:5d} MB: {g.value:8.0f} GB/s", flush=True)
     lat = ctypes.c_double()
-    ctx.lib.lmpk_probe_flag_latency(ctx.handle, 2000, ctypes.byref(lat))
+    probe.lmpk_probe_flag_latency(ctypes.c_void_p(ctx.handle.value if hasattr(ctx.handle, 'value') else ctx.handle), 2000, ctypes.byref(lat))
     print(f"flag latency one-way {lat.value:.0f} ns", flush=True)
 rp, c, v = O.gen_stencil_3d(N); n = rp.shape[0] - 1
 a = K.DeviceCsr.from_host(rp, c, v)
