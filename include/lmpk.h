@@ -251,6 +251,22 @@ int lmpk_permute_vectors(lmpk_ctx* ctx, int32_t n, const int32_t* perm, const do
                          int64_t ld_in, double* out, int64_t ld_out, int32_t n_vec, int32_t width,
                          int scatter, void* stream);
 
+/* One rank's window of a level-permuted matrix (multi-GPU, dist.py
+ * window_csr; no reference counterpart -- the reference has no multi-process
+ * code): rows [lo, hi), columns outside [lo, hi) dropped, the
+ * rest shifted by -lo, entry order kept.  out_row_ptr[hi-lo+1]; out_col /
+ * out_val need room for row_ptr[hi] - row_ptr[lo] entries (may be NULL when
+ * that is 0).  *out_nnz = kept entries.  Synchronizes the stream. */
+int lmpk_csr_window(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                    const double* val, int32_t lo, int32_t hi, int32_t* out_row_ptr, int32_t* out_col,
+                    double* out_val, int64_t* out_nnz, void* stream);
+
+/* out = c * x over n entries (complex_state: interleaved (re, im) pairs and
+ * re = c_re x_re - c_im x_im, im = c_re x_im + c_im x_re) -- the accumulator
+ * start acc = c_0 T_0 of ChebPropagator.step (cheb.py:229). */
+int lmpk_vec_scale(lmpk_ctx* ctx, int64_t n, const double* x, double c_re, double c_im, int complex_state,
+                   double* out, void* stream);
+
 /* Per-level nonzero counts: out[i] = row_ptr[level_ptr[i+1]] - row_ptr[level_ptr[i]]
  * (groups.py:257-262 _level_nnz on the permuted matrix). */
 int lmpk_level_nnz(lmpk_ctx* ctx, const int32_t* row_ptr, const int64_t* level_ptr,

@@ -90,6 +90,8 @@ SIGNATURES = {
     "lmpk_ctx_launch_count": (_i64, [_vp]),
     "lmpk_ctx_check": (_int, [_vp, _vp]),
     "lmpk_ctx_set_epoch": (_i64, [_vp, _i64]),
+    "lmpk_csr_window": (_int, [_vp, _i32, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, ctypes.POINTER(_i64), _vp]),
+    "lmpk_vec_scale": (_int, [_vp, _i64, _vp, ctypes.c_double, ctypes.c_double, _int, _vp, _vp]),
     "lmpk_ctx_profile": (_int, [_vp, _vp, _int]),
     "lmpk_ctx_trace": (_int, [_vp, _vp, _i64]),
     "lmpk_spmv_rows": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _int, _vp]),

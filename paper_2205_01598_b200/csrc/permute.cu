@@ -307,3 +307,95 @@ extern "C" int lmpk_segment_col_range(lmpk_ctx* ctx, const int32_t* row_ptr, con
   launch_count_add(ctx, 1);
   return LMPK_OK;
 }
+
+// ------------------------------------------------------------------ windows
+// Rows [lo, hi) of a CRS matrix with the columns outside [lo, hi) dropped and
+// the rest shifted by -lo, entry order kept (dist.py window_csr): one rank's
+// level-range window, cut in HBM.
+namespace lmpk {
+__global__ void k_win_count(const int32_t* row_ptr, const int32_t* col, int32_t lo, int32_t hi, int32_t* cnt) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(hi) - lo;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t r = lo + int32_t(i);
+    int32_t c = 0;
+    for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) c += (col[e] >= lo && col[e] < hi) ? 1 : 0;
+    cnt[i] = c;
+  }
+}
+__global__ void k_win_emit(const int32_t* row_ptr, const int32_t* col, const double* val, int32_t lo, int32_t hi,
+                           const int32_t* out_rp, int32_t* out_col, double* out_val) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < int64_t(hi) - lo;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t r = lo + int32_t(i);
+    int32_t o = out_rp[i];
+    for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+      const int32_t c = col[e];
+      if (c >= lo && c < hi) {
+        out_col[o] = c - lo;
+        out_val[o] = val[e];
+        ++o;
+      }
+    }
+  }
+}
+// out = c * x in the reference's order (complex: re = cr xr - ci xi, im = cr xi + ci xr)
+template <bool CPLX>
+__global__ void k_vec_scale(int64_t n, const double* x, double cr, double ci, double* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    if constexpr (CPLX) {
+      const double xr = x[2 * i], xi = x[2 * i + 1];
+      out[2 * i] = __dsub_rn(__dmul_rn(cr, xr), __dmul_rn(ci, xi));
+      out[2 * i + 1] = __dadd_rn(__dmul_rn(cr, xi), __dmul_rn(ci, xr));
+    } else {
+      out[i] = __dmul_rn(cr, x[i]);
+    }
+  }
+}
+}  // namespace lmpk
+
+extern "C" int lmpk_csr_window(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                               const double* val, int32_t lo, int32_t hi, int32_t* out_row_ptr, int32_t* out_col,
+                               double* out_val, int64_t* out_nnz, void* stream) {
+  LMPK_ARG_CHECK(ctx && row_ptr && out_row_ptr && out_nnz, "lmpk_csr_window: NULL argument");
+  LMPK_ARG_CHECK(0 <= lo && lo <= hi && hi <= n, "window [%d, %d) out of bounds for n=%d", lo, hi, n);
+  cudaStream_t st = as_stream(stream);
+  const int32_t w = hi - lo;
+  if (w == 0) {
+    LMPK_CHECK_CUDA(cudaMemsetAsync(out_row_ptr, 0, 4, st));
+    *out_nnz = 0;
+    return LMPK_OK;
+  }
+  LMPK_TRY(ctx->s_a.ensure(size_t(w) * 4 + 64));
+  int32_t* cnt = reinterpret_cast<int32_t*>(ctx->s_a.ptr);
+  const int64_t tmp_len = scan_tmp_len(int64_t(w) + 1) + 8;
+  LMPK_TRY(ctx->s_small.ensure(4096 + size_t(tmp_len) * 8));
+  int64_t* stmp = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(ctx->s_small.ptr) + 4096);
+  k_win_count<<<grid_n(ctx, w), 256, 0, st>>>(row_ptr, col, lo, hi, cnt);
+  launch_count_add(ctx, 1);
+  LMPK_TRY(device_excl_scan<int32_t, int32_t>(ctx, cnt, w, out_row_ptr, 0, true, stmp, st));
+  int32_t total = 0;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&total, out_row_ptr + w, 4, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  *out_nnz = total;
+  if (total > 0) {
+    LMPK_ARG_CHECK(out_col && out_val, "lmpk_csr_window: NULL output arrays");
+    k_win_emit<<<grid_n(ctx, w), 256, 0, st>>>(row_ptr, col, val, lo, hi, out_row_ptr, out_col, out_val);
+    launch_count_add(ctx, 1);
+  }
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  return LMPK_OK;
+}
+
+extern "C" int lmpk_vec_scale(lmpk_ctx* ctx, int64_t n, const double* x, double c_re, double c_im, int complex_state,
+                              double* out, void* stream) {
+  LMPK_ARG_CHECK(ctx && x && out, "lmpk_vec_scale: NULL argument");
+  if (n == 0) return LMPK_OK;
+  cudaStream_t st = as_stream(stream);
+  if (complex_state)
+    k_vec_scale<true><<<grid_n(ctx, n), 256, 0, st>>>(n, x, c_re, c_im, out);
+  else
+    k_vec_scale<false><<<grid_n(ctx, n), 256, 0, st>>>(n, x, c_re, 0.0, out);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 1);
+  return LMPK_OK;
+}

@@ -185,6 +185,22 @@ def halo_exchange(shards: "LevelShards", rank: int, group, vecs):
         req.wait()
 
 
+def _is_device_csr(a) -> bool:
+    from .kernels import DeviceCsr
+
+    return isinstance(a, DeviceCsr)
+
+
+def _window(row_ptr, col, val, lo, hi):
+    """The window matrix: cut in HBM (lmpk_csr_window) when the permuted
+    matrix is a DeviceCsr, else on the host (window_csr)."""
+    if _is_device_csr(row_ptr):
+        from . import kernels as K
+
+        return K.csr_window(row_ptr, lo, hi)
+    return window_csr(row_ptr, col, val, lo, hi)
+
+
 class CudaWindowMpk:
     """Local MPK on one rank's window: the single-GPU level-blocked kernel."""
 
@@ -193,7 +209,7 @@ class CudaWindowMpk:
 
         self.K = K
         self.k = k
-        self.a = K.DeviceCsr.from_host(rp, col, val)
+        self.a = rp if _is_device_csr(rp) else K.DeviceCsr.from_host(rp, col, val)
         self.tiling = K.Tiling(self.a, k, **tiling_kw)
         self.cfg = K.mpk_power_cfg(k)
 
@@ -220,10 +236,13 @@ class DistMpk:
         self.shards = LevelShards(level_ptr, level_nnz, world, k)
         self.shard = self.shards[rank]
         s = self.shard
-        rp, c, v = window_csr(row_ptr, col, val, s.win_lo, s.win_hi)
-        self.window = (rp, c, v)
+        win = _window(row_ptr, col, val, s.win_lo, s.win_hi)
+        self.window = win
         self.device = torch.device("cpu") if device is None else torch.device(device)
-        self.local = local if local is not None else CudaWindowMpk(rp, c, v, k, **tiling_kw)
+        if local is None:
+            local = CudaWindowMpk(win, None, None, k, **tiling_kw) if _is_device_csr(win) \
+                else CudaWindowMpk(*win, k, **tiling_kw)
+        self.local = local
         self.y = torch.zeros((k + 1, s.n_win), dtype=torch.float64, device=self.device)
 
     def exchange(self, *vecs):
@@ -267,7 +286,7 @@ class CudaWindowCheb:
         from . import kernels as K
 
         self.K, self._lib = K, _lib
-        self.a = K.DeviceCsr.from_host(rp, col, val)
+        self.a = rp if _is_device_csr(rp) else K.DeviceCsr.from_host(rp, col, val)
         flags = int(tiling_kw.pop("mode_flags", 0)) | (_lib.FLAG_COMPLEX if complex_state else 0)
         self.tiling = K.Tiling(self.a, p_b, mode_flags=flags, **tiling_kw)
         self.complex = complex_state
@@ -305,9 +324,12 @@ class DistCheb:
         self.rank, self.world, self.group = rank, world, group
         self.shards = LevelShards(level_ptr, level_nnz, world, self.p_b)
         s = self.shard = self.shards[rank]
-        rp, c, v = window_csr(row_ptr, col, val, s.win_lo, s.win_hi)
+        win = _window(row_ptr, col, val, s.win_lo, s.win_hi)
         self.device = torch.device("cpu") if device is None else torch.device(device)
-        self.local = local if local is not None else CudaWindowCheb(rp, c, v, self.p_b, self.complex, **tiling_kw)
+        if local is None:
+            local = CudaWindowCheb(win, None, None, self.p_b, self.complex, **tiling_kw) if _is_device_csr(win) \
+                else CudaWindowCheb(*win, self.p_b, self.complex, **tiling_kw)
+        self.local = local
         dt = torch.complex128 if self.complex else torch.float64
         self.ring = torch.zeros((self.p_b + 2, s.n_win), dtype=dt, device=self.device)
 
@@ -321,13 +343,16 @@ class DistCheb:
         ring[0, o0:o1].copy_(torch.as_tensor(x_own, device=self.device).to(ring.dtype))
         halo_exchange(self.shards, self.rank, self.group, [ring[0]])
         c0 = complex(self.c[0]) if self.complex else float(np.real(self.c[0]))
-        if self.complex:
-            # acc = c_0 * T_0 with the product spelled out (oracle order)
-            acc = torch.empty_like(ring[0])
+        acc = torch.empty_like(ring[0])
+        if ring.is_cuda:  # acc = c_0 T_0 by liblmpk (oracle order)
+            from . import kernels as K
+
+            K.vec_scale(ring[0], c0, acc)
+        elif self.complex:  # CPU ranks of the gloo tests: the same products spelled out
             acc.real.copy_(ring[0].real * c0.real - ring[0].imag * c0.imag)
             acc.imag.copy_(ring[0].imag * c0.real + ring[0].real * c0.imag)
         else:
-            acc = ring[0] * c0
+            acc.copy_(ring[0] * c0)
         k = 0
         while k < self.m:
             pb = min(self.p_b, self.m - k)

@@ -210,6 +210,31 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0, sync=True):
     return finish() if sync else finish
 
 
+def plan_launcher(plan: ExecPlan, yd, accd=None, use_acc=False, flags=0):
+    """(launch, schedule): a callable that queues exactly what run_plan
+    launches for this plan on device buffers -- the chosen walk / sweep / CRS
+    schedule -- without synchronizing or checking errors (timed loops; call
+    lmpk_ctx_check afterwards), and the schedule's name."""
+    torch = _torch()
+    cplx = yd.is_complex()
+    yv = torch.view_as_real(yd).reshape(yd.shape[0], -1) if cplx else yd
+    av = None
+    if use_acc:
+        av = torch.view_as_real(accd).reshape(-1) if accd.is_complex() else accd
+    cfg = plan.power_config()
+    if plan.variant == "baseline":
+        return (lambda: K.mpk_baseline(plan.a.device(), yv, plan.p_m)), "crs"
+    til = plan.tiling(complex_state=cplx)
+    if til is None:
+        return (lambda: K.mpk_baseline(plan.a.device(), yv, plan.p_m)), "crs"
+    sched = _schedule(plan, til, yv, cfg, av, use_acc, cplx, flags)
+    if sched == "crs":
+        return (lambda: K.mpk_baseline(plan.a.device(), yv, plan.p_m)), sched
+    f = flags | (_lib.FLAG_SWEEP if sched == "sweep" else 0)
+    return (lambda: K.mpk_run(til, yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx, flags=f,
+                              check_errors=False)), sched
+
+
 _PLAN_FIELDS = ("variant", "p_m", "workers", "n_rows", "items", "barrier", "row_start", "row_end",
                 "power", "chunks", "bnd_point", "check_ptr", "check_item", "check_kind",
                 "out_slot", "in_slot", "prev_slot", "kernel", "acc_coef")

@@ -277,3 +277,36 @@ def segment_col_range(a: DeviceCsr, seg_ptr, stream=None):
                                          ptr(mn), ptr(mx), stream_handle(stream)),
           "segment_col_range")
     return mn[:G].cpu().numpy(), mx[:G].cpu().numpy()
+
+
+def csr_window(a: DeviceCsr, lo, hi, stream=None) -> DeviceCsr:
+    """Rows [lo, hi) of a device matrix, columns outside the range dropped and
+    shifted by -lo (one rank's level-range window, cut in HBM)."""
+    torch = _torch()
+    ctx = context()
+    w = int(hi) - int(lo)
+    dev = a.row_ptr.device
+    rp = torch.empty(w + 1, dtype=torch.int32, device=dev)
+    cap = int(a.row_ptr[int(hi)].item()) - int(a.row_ptr[int(lo)].item()) if w > 0 else 0
+    col = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    val = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+    nnz = ctypes.c_int64()
+    check(ctx.lib.lmpk_csr_window(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val), int(lo), int(hi),
+                                  ptr(rp), ptr(col), ptr(val), ctypes.byref(nnz), stream_handle(stream)),
+          "csr_window")
+    k = int(nnz.value)
+    return DeviceCsr(w, rp, col[:k].clone() if k < col.shape[0] else col, val[:k].clone() if k < val.shape[0] else val)
+
+
+def vec_scale(x, c, out, stream=None):
+    """out = c * x (float64 or complex128 tensors of equal shape) in the
+    reference's arithmetic (the ChebPropagator accumulator start c_0 T_0)."""
+    torch = _torch()
+    ctx = context()
+    cplx = x.is_complex()
+    xv = torch.view_as_real(x).reshape(-1) if cplx else x.reshape(-1)
+    ov = torch.view_as_real(out).reshape(-1) if cplx else out.reshape(-1)
+    n = xv.shape[0] // 2 if cplx else xv.shape[0]
+    check(ctx.lib.lmpk_vec_scale(ctx.handle, int(n), ptr(xv), float(np.real(c)), float(np.imag(c)),
+                                 1 if cplx else 0, ptr(ov), stream_handle(stream)), "vec_scale")
+    return out

@@ -104,10 +104,10 @@ def stencil_3d_nnz(n: int, order: int = 2) -> int:
 
 
 # ----------------------------------------------------------------- BASELINE configs
-def gen_laplace_2d5pt(nx: int, ny: int) -> CsrMatrix:
+def gen_laplace_2d5pt(nx: int, ny: int, device: bool = False) -> CsrMatrix:
     """Config 1: 2D 5-point Laplacian, Dirichlet, diag 4.0 / off -1.0, ids ix*ny + iy."""
     offs = [(-1, 0), (1, 0), (0, -1), (0, 1)]
-    return grid_operator((nx, ny), [((0, 0), 4.0)] + [(o, -1.0) for o in offs])
+    return grid_operator((nx, ny), [((0, 0), 4.0)] + [(o, -1.0) for o in offs], device=device)
 
 
 def gen_stencil_3d27pt(n: int, perturb: float = 0.01, seed: int = 0, device: bool = False) -> CsrMatrix:

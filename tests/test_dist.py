@@ -7,6 +7,7 @@ gpu test runs every shard's window through the CUDA kernel in one process
 (the shards never wait on each other, so this is not a multi-rank stand-in)."""
 
 import os
+import pathlib
 import socket
 
 import numpy as np
@@ -280,3 +281,63 @@ def test_gpu_dist_cheb_window_runner_vs_oracle(cplx, p_b):
     got = dc.step(torch.from_numpy(np.asarray(x)).cuda()).cpu().numpy()
     ref = O.cheb_batches(prp, pcol, pval, x, np.real(coeffs), np.imag(coeffs) if cplx else None)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_device_windows_match_host_windows(world):
+    """lmpk_csr_window (the window cut in HBM that bench.py's ranks use) is
+    bitwise the host window_csr; DistMpk built from the device matrix
+    computes the owned rows bitwise like the single-GPU MPK."""
+    import torch
+
+    from paper_2205_01598_b200 import kernels as K
+    from paper_2205_01598_b200.dist import CudaWindowMpk, _window
+
+    k = 3
+    prp, pcol, pval, lp, lnnz = _level_permuted(20)
+    n = prp.shape[0] - 1
+    a = K.DeviceCsr.from_host(prp, pcol, pval)
+    x = np.random.default_rng(8).uniform(-1, 1, n)
+    ref = O.mpk_powers(prp, pcol, pval, x, k)
+    sh = LevelShards(lp, lnnz, world, k)
+    for s in sh.shards:
+        rp, c, v = window_csr(prp, pcol, pval, s.win_lo, s.win_hi)
+        d = _window(a, None, None, s.win_lo, s.win_hi)
+        assert d.n == s.n_win
+        assert np.array_equal(d.row_ptr.cpu().numpy(), rp) and np.array_equal(d.col.cpu().numpy(), c)
+        assert np.array_equal(d.val.cpu().numpy(), v)
+        loc = CudaWindowMpk(d, None, None, k)
+        yw = torch.zeros((k + 1, s.n_win), dtype=torch.float64, device="cuda")
+        yw[0] = torch.from_numpy(x[s.win_lo:s.win_hi].copy())  # the exchanged halo
+        loc(yw)
+        got = yw[:, s.own_offset:s.own_offset + s.n_own].cpu().numpy()
+        assert np.array_equal(got, ref[:, s.own_lo:s.own_hi])
+
+
+def test_bench_self_launch_command(monkeypatch):
+    """bench.py --gpus N without WORLD_SIZE re-launches itself with one rank
+    per GPU under torch.distributed.run on 127.0.0.1 (NCCL init logging on)."""
+    import importlib
+    import subprocess
+    import sys
+
+    sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+    bench = importlib.import_module("bench")
+    seen = {}
+
+    def fake_call(cmd, env=None):
+        seen["cmd"], seen["env"] = cmd, env
+        return 0
+
+    monkeypatch.setattr(subprocess, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3", "--config", "cfg2"])
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "3", "--config", "cfg2"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
