@@ -150,6 +150,7 @@ typedef struct lmpk_tiling_info {
                          /* consecutive tiles streamed through the smem ring   */
   int64_t lean_bytes;    /* ring walk: width-sorted lean copy of the blocks    */
                          /* (0: the tiling runs the general ring kernel)      */
+  int32_t lean_pattern_tiles; /* lean tiles storing each slice's distinct rows once */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */

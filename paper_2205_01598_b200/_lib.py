@@ -55,7 +55,7 @@ class TilingInfo(ctypes.Structure):
         ("queue_slack", _i32), ("nnz", _i64), ("block_bytes", _i64),
         ("powers_per_item", _i32), ("slots", _i32), ("x_staged_tiles", _i32),
         ("compressed_tiles", _i32), ("dict_tiles", _i32), ("super_tiles", _i32),
-        ("lean_bytes", _i64),
+        ("lean_bytes", _i64), ("lean_pattern_tiles", _i32),
     ]
 
     def as_dict(self):

@@ -43,7 +43,7 @@ constexpr int kLeanConsumers = LMPK_LEAN_NC;
 constexpr int kLeanHdr = 16;          // [nu, nrows, flags, 0]
 constexpr int kLeanDict = 16;         // dictionary byte offset in the block
 constexpr int kLeanRec = 16 + 256;    // first unit record
-constexpr uint32_t kLeanPair = 1u << 8, kLeanPadded = 1u << 9;
+constexpr uint32_t kLeanPair = 1u << 8, kLeanPadded = 1u << 9, kLeanPattern = 1u << 10;
 
 __host__ __device__ constexpr int lean_wc(int w) { return w <= 0 ? 0 : (w <= 4 ? 4 : 8); }
 // bytes of one slice's column offsets / dictionary codes / raw values
@@ -58,48 +58,90 @@ struct LeanParams {
 };
 
 // ---------------------------------------------------------------- row sums
-// Chunk loads of lane's entries (smem byte addresses).
+// Shared-memory reads by 32-bit address.  They are plain (non-volatile) asm
+// so the scheduler may batch them; every address derives from the piece's
+// base, which is an OUTPUT of the piece's mbarrier wait (lean_wait), so no
+// read can move above the wait or be reused across pieces.
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_b8(uint32_t a) {
+  uint32_t v;
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s16(uint32_t a) {
+  int16_t v;
+  asm("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_d(uint32_t a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+
+// Lane's W column offsets (lane-contiguous Wc int16 at p).
 template <int W>
-__device__ __forceinline__ void lean_cols(const unsigned char* p, int32_t (&c)[W]) {
+__device__ __forceinline__ void lean_cols(uint32_t p, int32_t (&c)[W]) {
   if constexpr (lean_wc(W) == 8) {
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    const uint4 v = lds_v4(p);
     const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int j = 0; j < W; ++j) c[j] = (j & 1) ? (int32_t(w4[j >> 1]) >> 16) : int32_t(int16_t(w4[j >> 1] & 0xffffu));
   } else {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    const uint2 v = lds_v2(p);
     const uint32_t w2[2] = {v.x, v.y};
 #pragma unroll
     for (int j = 0; j < W; ++j) c[j] = (j & 1) ? (int32_t(w2[j >> 1]) >> 16) : int32_t(int16_t(w2[j >> 1] & 0xffffu));
   }
 }
+// Lane's W dictionary values: byte codes (premultiplied by 8) at p, the
+// dictionary at dict.
 template <int W>
-__device__ __forceinline__ void lean_codes(const unsigned char* p, uint32_t (&k)[W]) {
+__device__ __forceinline__ void lean_dvals(uint32_t p, uint32_t dict, double (&v)[W]) {
   if constexpr (lean_wc(W) == 8) {
-    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    const uint2 k = lds_v2(p);
 #pragma unroll
-    for (int j = 0; j < W; ++j) k[j] = __byte_perm(j < 4 ? v.x : v.y, 0u, 0x4440u + uint32_t(j & 3));
+    for (int j = 0; j < W; ++j) v[j] = lds_d(dict + __byte_perm(j < 4 ? k.x : k.y, 0u, 0x4440u + uint32_t(j & 3)));
   } else {
-    const uint32_t v = *reinterpret_cast<const uint32_t*>(p);
+    const uint32_t k = lds_u32(p);
 #pragma unroll
-    for (int j = 0; j < W; ++j) k[j] = __byte_perm(v, 0u, 0x4440u + uint32_t(j));
+    for (int j = 0; j < W; ++j) v[j] = lds_d(dict + __byte_perm(k, 0u, 0x4440u + uint32_t(j)));
   }
 }
 // raw values of lane's W entries, chunked (quads, pair, single; see chunk_entry)
 template <int W>
-__device__ __forceinline__ void lean_raw(const unsigned char* p, uint32_t lane, double (&v)[W]) {
+__device__ __forceinline__ void lean_raw(uint32_t p, uint32_t lane, double (&v)[W]) {
   constexpr int Q = W >> 2, PR = (W >> 1) & 1, SG = W & 1;
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
-    const double2 a = *reinterpret_cast<const double2*>(p + q * 1024 + lane * 32);
-    const double2 b = *reinterpret_cast<const double2*>(p + q * 1024 + lane * 32 + 16);
+    const double2 a = lds_d2(p + q * 1024 + lane * 32);
+    const double2 b = lds_d2(p + q * 1024 + lane * 32 + 16);
     v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = b.x, v[4 * q + 3] = b.y;
   }
   if constexpr (PR) {
-    const double2 a = *reinterpret_cast<const double2*>(p + Q * 1024 + lane * 16);
+    const double2 a = lds_d2(p + Q * 1024 + lane * 16);
     v[4 * Q] = a.x, v[4 * Q + 1] = a.y;
   }
-  if constexpr (SG) v[W - 1] = *reinterpret_cast<const double*>(p + Q * 1024 + PR * 512 + lane * 8);
+  if constexpr (SG) v[W - 1] = lds_d(p + Q * 1024 + PR * 512 + lane * 8);
 }
 
 template <bool CPLX>
@@ -130,14 +172,28 @@ struct LeanSum {
   double r, i;
 };
 
+template <int W, bool CPLX, bool EXACT>
+__device__ __forceinline__ LeanSum<CPLX> lean_chain(const double (&v)[W], const typename LeanX<CPLX>::T (&x)[W]) {
+  LeanSum<CPLX> s{0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    if constexpr (CPLX) {
+      s.r = madd<EXACT>(s.r, v[j], x[j].x);
+      s.i = madd<EXACT>(s.i, v[j], x[j].y);
+    } else {
+      s.r = madd<EXACT>(s.r, v[j], x[j]);
+    }
+  }
+  return s;
+}
+
 // One slice of width W: lane's row sum in storage order (real or complex x).
 // cp/vp: lane's column-offset / code (or slice-base raw value) addresses.
 template <int W, bool CPLX, bool EXACT, bool VD>
-__device__ __forceinline__ LeanSum<CPLX> lean_slice(const unsigned char* cp, const unsigned char* vp,
-                                                    const unsigned char* dict, uint32_t lane, const char* rp) {
-  LeanSum<CPLX> s{0.0, 0.0};
+__device__ __forceinline__ LeanSum<CPLX> lean_slice(uint32_t cp, uint32_t vp, uint32_t dict, uint32_t lane,
+                                                    const char* rp) {
   if constexpr (W == 0) {
-    return s;
+    return LeanSum<CPLX>{0.0, 0.0};
   } else {
     int32_t c[W];
     lean_cols<W>(cp, c);
@@ -145,35 +201,22 @@ __device__ __forceinline__ LeanSum<CPLX> lean_slice(const unsigned char* cp, con
 #pragma unroll
     for (int j = 0; j < W; ++j) x[j] = lean_gather<CPLX>(rp, c[j]);
     double v[W];
-    if constexpr (VD) {
-      uint32_t k[W];
-      lean_codes<W>(vp, k);
-#pragma unroll
-      for (int j = 0; j < W; ++j) v[j] = *reinterpret_cast<const double*>(dict + k[j]);
-    } else {
+    if constexpr (VD)
+      lean_dvals<W>(vp, dict, v);
+    else
       lean_raw<W>(vp, lane, v);
-    }
-#pragma unroll
-    for (int j = 0; j < W; ++j) {
-      if constexpr (CPLX) {
-        s.r = madd<EXACT>(s.r, v[j], x[j].x);
-        s.i = madd<EXACT>(s.i, v[j], x[j].y);
-      } else {
-        s.r = madd<EXACT>(s.r, v[j], x[j]);
-      }
-    }
-    return s;
+    return lean_chain<W, CPLX, EXACT>(v, x);
   }
 }
 
 // Two slices of the same width: every gather of both in flight at once.
 template <int W, bool CPLX, bool EXACT, bool VD>
-__device__ __forceinline__ void lean_pair(const unsigned char* cp0, const unsigned char* vp0, const unsigned char* cp1,
-                                          const unsigned char* vp1, const unsigned char* dict, uint32_t lane,
-                                          const char* rp0, const char* rp1, LeanSum<CPLX>& s0, LeanSum<CPLX>& s1) {
-  s0 = LeanSum<CPLX>{0.0, 0.0};
-  s1 = LeanSum<CPLX>{0.0, 0.0};
-  if constexpr (W > 0) {
+__device__ __forceinline__ void lean_pair(uint32_t cp0, uint32_t vp0, uint32_t cp1, uint32_t vp1, uint32_t dict,
+                                          uint32_t lane, const char* rp0, const char* rp1, LeanSum<CPLX>& s0,
+                                          LeanSum<CPLX>& s1) {
+  if constexpr (W == 0) {
+    s0 = s1 = LeanSum<CPLX>{0.0, 0.0};
+  } else {
     int32_t c0[W], c1[W];
     lean_cols<W>(cp0, c0);
     lean_cols<W>(cp1, c1);
@@ -184,43 +227,19 @@ __device__ __forceinline__ void lean_pair(const unsigned char* cp0, const unsign
     for (int j = 0; j < W; ++j) x1[j] = lean_gather<CPLX>(rp1, c1[j]);
     {
       double v[W];
-      if constexpr (VD) {
-        uint32_t k[W];
-        lean_codes<W>(vp0, k);
-#pragma unroll
-        for (int j = 0; j < W; ++j) v[j] = *reinterpret_cast<const double*>(dict + k[j]);
-      } else {
+      if constexpr (VD)
+        lean_dvals<W>(vp0, dict, v);
+      else
         lean_raw<W>(vp0, lane, v);
-      }
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        if constexpr (CPLX) {
-          s0.r = madd<EXACT>(s0.r, v[j], x0[j].x);
-          s0.i = madd<EXACT>(s0.i, v[j], x0[j].y);
-        } else {
-          s0.r = madd<EXACT>(s0.r, v[j], x0[j]);
-        }
-      }
+      s0 = lean_chain<W, CPLX, EXACT>(v, x0);
     }
     {
       double v[W];
-      if constexpr (VD) {
-        uint32_t k[W];
-        lean_codes<W>(vp1, k);
-#pragma unroll
-        for (int j = 0; j < W; ++j) v[j] = *reinterpret_cast<const double*>(dict + k[j]);
-      } else {
+      if constexpr (VD)
+        lean_dvals<W>(vp1, dict, v);
+      else
         lean_raw<W>(vp1, lane, v);
-      }
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        if constexpr (CPLX) {
-          s1.r = madd<EXACT>(s1.r, v[j], x1[j].x);
-          s1.i = madd<EXACT>(s1.i, v[j], x1[j].y);
-        } else {
-          s1.r = madd<EXACT>(s1.r, v[j], x1[j]);
-        }
-      }
+      s1 = lean_chain<W, CPLX, EXACT>(v, x1);
     }
   }
 }
@@ -228,17 +247,15 @@ __device__ __forceinline__ void lean_pair(const unsigned char* cp0, const unsign
 // Slow path of a padded row whose sum came out NaN: the row again with its
 // true length (padding entries skipped), exactly as the reference sums it.
 template <bool CPLX, bool EXACT, bool VD>
-__device__ __noinline__ LeanSum<CPLX> lean_row_exact(const unsigned char* cp, const unsigned char* vp,
-                                                     const unsigned char* dict, uint32_t lane, const char* rp, int w,
-                                                     int len) {
+__device__ __noinline__ LeanSum<CPLX> lean_row_exact(uint32_t cp, uint32_t vp, uint32_t dict, uint32_t lane,
+                                                     const char* rp, int w, int len) {
   LeanSum<CPLX> s{0.0, 0.0};
-  const int wc = lean_wc(w);
   const int Q = w >> 2, PR = (w >> 1) & 1;
   for (int j = 0; j < len; ++j) {
-    const int32_t c = int32_t(*reinterpret_cast<const int16_t*>(cp + 2 * j));
+    const int32_t c = lds_s16(cp + 2 * j);
     double v;
     if constexpr (VD) {
-      v = *reinterpret_cast<const double*>(dict + vp[j]);
+      v = lds_d(dict + lds_b8(vp + j));
     } else {
       // vp is the slice's raw-value base here: chunk position of entry j
       uint32_t e;
@@ -248,7 +265,7 @@ __device__ __noinline__ LeanSum<CPLX> lean_row_exact(const unsigned char* cp, co
         e = uint32_t(Q) * 128u + lane * 2u + uint32_t(j - 4 * Q);
       else
         e = uint32_t(Q) * 128u + (PR ? 64u : 0u) + lane;
-      v = *reinterpret_cast<const double*>(vp + e * 8u);
+      v = lds_d(vp + e * 8u);
     }
     const typename LeanX<CPLX>::T x = lean_gather<CPLX>(rp, c);
     if constexpr (CPLX) {
@@ -258,7 +275,6 @@ __device__ __noinline__ LeanSum<CPLX> lean_row_exact(const unsigned char* cp, co
       s.r = madd<EXACT>(s.r, v, x);
     }
   }
-  (void)wc;
   return s;
 }
 
@@ -299,22 +315,50 @@ __device__ __forceinline__ void lean_store(const PowTab& pt, double* acc, bool u
   }
 }
 
+// Lane's column-offset / code addresses of one slice.  Plain lean slices
+// hold every lane's entries (lane-contiguous); PATTERN slices (dictionary
+// tiles) hold the slice's distinct rows once -- [32 u8 row pattern ids]
+// [P x 2Wc B offsets][P x Wc B codes] -- and a lane reads its pattern's record.
+template <int W, bool VD>
+__device__ __forceinline__ void lean_ptrs(uint32_t blk, uint32_t off, uint32_t np, bool pat, uint32_t lane,
+                                          uint32_t& cp, uint32_t& vp, uint32_t vo) {
+  if (VD && pat) {
+    const uint32_t sl = blk + off;
+    const uint32_t id = lds_b8(sl + lane);
+    cp = sl + 32 + id * (2 * lean_wc(W));
+    vp = sl + 32 + np * (2 * lean_wc(W)) + id * lean_wc(W);
+  } else {
+    cp = blk + off + lane * (2 * lean_wc(W));
+    vp = VD ? blk + vo + lane * lean_wc(W) : blk + vo;
+  }
+}
+
 // One unit of width W (compile time): a pair or a single slice.
+// Record: plain {col off, value off, W | flags, slice ids}; pattern
+// {slice a off, slice b off, W | flags | Pa << 16 | Pb << 24, slice ids}.
 template <int W, bool CPLX, bool EXACT, bool VD, bool GEN>
-__device__ __forceinline__ void lean_unit(const unsigned char* blk, uint4 rec, uint32_t lane, int32_t r0, int32_t nrows,
+__device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane, int32_t r0, int32_t nrows,
                                           const PowTab& pt, double* acc, bool use_acc, const uint8_t* rowlen) {
   constexpr int cw = CPLX ? 16 : 8;
-  const unsigned char* dict = blk + kLeanDict;
+  const uint32_t dict = blk + kLeanDict;
   const int32_t s0 = int32_t(rec.w & 0xffffu), s1 = int32_t(rec.w >> 16);
   const int32_t l0 = s0 * 32 + int32_t(lane), l1 = s1 * 32 + int32_t(lane);
-  const char* rp0 = pt.yin + int64_t(r0 + l0) * cw;
-  const unsigned char* cp0 = blk + rec.x + lane * (2 * lean_wc(W));
-  const unsigned char* vp0 = VD ? blk + rec.y + lane * lean_wc(W) : blk + rec.y;
+  const bool pat = VD && (rec.z & kLeanPattern) != 0;
+  // lanes past the tile (last slice) use the last valid lane's pattern: gather
+  // around that row (their sums are discarded)
+  const char* rp0 = pt.yin + int64_t(r0 + (pat ? min(l0, nrows - 1) : l0)) * cw;
+  uint32_t cp0, vp0;
+  lean_ptrs<W, VD>(blk, rec.x, (rec.z >> 16) & 255u, pat, lane, cp0, vp0, rec.y);
   const bool padded = (rec.z & kLeanPadded) != 0;
   if (rec.z & kLeanPair) {
-    const char* rp1 = pt.yin + int64_t(r0 + l1) * cw;
-    const unsigned char* cp1 = cp0 + lean_col_bytes(W);
-    const unsigned char* vp1 = vp0 + (VD ? lean_code_bytes(W) : lean_raw_bytes(W));
+    const char* rp1 = pt.yin + int64_t(r0 + (pat ? min(l1, nrows - 1) : l1)) * cw;
+    uint32_t cp1, vp1;
+    if (pat) {
+      lean_ptrs<W, VD>(blk, rec.y, rec.z >> 24, true, lane, cp1, vp1, 0u);
+    } else {
+      cp1 = cp0 + lean_col_bytes(W);
+      vp1 = vp0 + (VD ? lean_code_bytes(W) : lean_raw_bytes(W));
+    }
     LeanSum<CPLX> a, b;
     lean_pair<W, CPLX, EXACT, VD>(cp0, vp0, cp1, vp1, dict, lane, rp0, rp1, a, b);
     if (padded) {
@@ -333,14 +377,23 @@ __device__ __forceinline__ void lean_unit(const unsigned char* blk, uint4 rec, u
   }
 }
 
+// Wait for a piece and return its base address: the base is an asm output of
+// the completed wait, so every shared read addressed from it stays below it.
+__device__ __forceinline__ uint32_t lean_wait(uint64_t* bar, uint32_t parity, uint32_t base) {
+  while (!mbar_try_wait_sleep(bar, parity, 1000000u)) {
+  }
+  uint32_t out;
+  asm volatile("mov.u32 %0, %1;" : "=r"(out) : "r"(base) : "memory");
+  return out;
+}
+
 // ---------------------------------------------------------------- kernel
 // Same launch contract as mpk_ring_kernel (cooperative, one CTA per SM, a
 // 2-piece ring): warp NC is the producer, warp NC + 1 the publisher.
-template <bool CPLX, bool EXACT, bool VD, bool GEN>
+template <bool CPLX, bool EXACT, bool VD, bool GEN, int NP>
 __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
     mpk_lean_kernel(MpkParams P, PowerCfgDev C, LeanParams L) {
   constexpr int NC = kLeanConsumers;
-  constexpr int NP = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ uint64_t full_bar[NP], empty_bar[NP], done_bar[NP];
   __shared__ int32_t d_t[NP], d_p[NP], d_r0[NP], d_rows[NP];
@@ -364,8 +417,8 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
   if (warp == NC + 1) {
     // ------------------------------------------------ publisher (ring order)
     for (uint32_t k = 0;; ++k) {
-      const int slot = int(k & 1u);
-      mbar_wait_sleep(&done_bar[slot], (k >> 1) & 1);
+      const int slot = int(k % NP);
+      mbar_wait_sleep(&done_bar[slot], (k / NP) & 1);
       const int32_t t = d_t[slot], p = d_p[slot];
       __syncwarp();
       if (t < 0) break;
@@ -398,8 +451,8 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
       }
       if (lane == 0) trace_ev(P, &trace_ctr, 4, 0, uint32_t(T) << 8 | uint32_t(p));
       for (int32_t m = m0; m < m1; ++m) {
-        const int slot = int(k & 1u);
-        if (k >= 2u && !mbar_wait_bounded(&empty_bar[slot], ((k >> 1) - 1) & 1, P)) {
+        const int slot = int(k % NP);
+        if (k >= uint32_t(NP) && !mbar_wait_bounded(&empty_bar[slot], (k / NP - 1) & 1, P)) {
           abort = true;
           break;
         }
@@ -422,11 +475,11 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
       if (abort) break;
     }
     if (lane == 0) {
-      const int slot = int(k & 1u);
+      const int slot = int(k % NP);
       bool ok = true;
-      if (k >= 2u) {
+      if (k >= uint32_t(NP)) {
         unsigned long long t0 = globaltimer();
-        while (!mbar_try_wait(&empty_bar[slot], ((k >> 1) - 1) & 1)) {
+        while (!mbar_try_wait(&empty_bar[slot], (k / NP - 1) & 1)) {
           if (globaltimer() - t0 > kWatchdogNs || *(volatile unsigned long long*)(P.queue + 1) != 0ull) {
             ok = false;
             break;
@@ -442,24 +495,24 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
   } else {
     // ------------------------------------------------ consumers
     const bool use_acc = P.use_acc != 0;
+    const uint32_t ring = smem_u32(smem_raw);
     for (uint32_t k = 0;; ++k) {
-      const int slot = int(k & 1u);
-      mbar_wait_sleep(&full_bar[slot], (k >> 1) & 1);
+      const int slot = int(k % NP);
+      const uint32_t blk = lean_wait(&full_bar[slot], (k / NP) & 1, ring + uint32_t(slot) * uint32_t(cap));
       const int32_t t = d_t[slot];
       if (t < 0) {
         if (warp == 0 && lane == 0) mbar_arrive(&done_bar[slot]);
         break;
       }
       const int32_t p = d_p[slot], r0 = d_r0[slot], nrows = d_rows[slot];
-      const unsigned char* blk = smem_raw + slot * cap;
-      const int32_t nu = *reinterpret_cast<const int32_t*>(blk);
+      const int32_t nu = int32_t(lds_u32(blk));
       const PowTab& pt = s_pow[p - 1];
       if (lane == 0 && (warp == 0 || warp == NC - 1)) trace_ev(P, &trace_ctr, 10, uint32_t(slot), uint32_t(t) << 8 | uint32_t(p));
       // static striding, rotated by the piece counter
       int32_t u = warp + int32_t(k % uint32_t(NC));
       if (u >= NC) u -= NC;
       for (; u < nu; u += NC) {
-        const uint4 rec = *reinterpret_cast<const uint4*>(blk + kLeanRec + u * 16);
+        const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);
         switch (rec.z & 15u) {
 #define LMPK_LEAN_CASE(Wv) \
   case Wv: lean_unit<Wv, CPLX, EXACT, VD, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen); break;

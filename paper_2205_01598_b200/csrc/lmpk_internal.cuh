@@ -122,6 +122,7 @@ struct lmpk_tiling {
   uint8_t* d_rowlen = nullptr;     // [n] row lengths (slow path of padded rows)
   int32_t lean_vd = -1;            // -1 none, 0 raw values, 1 dictionary
   int64_t lean_bytes = 0;
+  int32_t lean_piece = 0;          // bytes of the largest lean block (the lean ring's piece)
   uint32_t wrap_gen = 0;           // ctx wrap generation its progress words belong to
 };
 

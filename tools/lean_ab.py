@@ -43,7 +43,7 @@ for name in os.environ.get("CASES", "cfg2").split(","):
             os.environ.pop("LMPK_PASS_POWERS", None)
         t = K.Tiling(b, k, queue_slack=slack)
         out = {"case": name, "n": n, "nnz": nnz, "k": k, "crs_ms": round(tc[0], 4), "tiles": t.info["n_tiles"],
-               "lean_MB": round(t.info["lean_bytes"] / 1e6, 1), "block_MB": round(t.info["block_bytes"] / 1e6, 1),
+               "lean_MB": round(t.info["lean_bytes"] / 1e6, 1), "pat_tiles": t.info["lean_pattern_tiles"], "block_MB": round(t.info["block_bytes"] / 1e6, 1),
                "slack": t.info["queue_slack"], "qp": qp, "D": t.info["max_fwd_reach"]}
         qro = 12 * nnz + 4 * (n + 1) + 8 * n * (k + 1)
         arms = (("ring", "1"), ("lean", None))
