@@ -130,12 +130,14 @@ def q_cheb_batch(n, nnz):
 
 
 def traffic_for(key):
-    """ncu DRAM bytes per launch of the dominant kernel, this build and config
-    (profiles/traffic.json from tools/profile_round.sh)."""
+    """ncu DRAM bytes (read + write) per launch of the dominant kernel of this
+    config, from the round's `ncu --set full` capture (profiles/traffic.json,
+    written by tools/summarize_profiles.py from tools/profile_round.sh)."""
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            return json.loads(tf.read_text()).get(key)
+            ent = json.loads(tf.read_text()).get(key)
+            return int(ent["dram_bytes_per_launch"]) if ent else None
         except Exception:
             return None
     return None
@@ -465,6 +467,11 @@ def run_ours(args, cfgd):
         step()
     torch.cuda.synchronize()
     _lib.check(ctx.lib.lmpk_ctx_check(ctx.handle, _lib.stream_handle()), "bench warm-up")
+    if args.profile_step:  # one steady-state step between cudaProfilerStart/Stop (ncu --profile-from-start off)
+        torch.cuda.cudart().cudaProfilerStart()
+        step()
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -831,6 +838,8 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="wrap one steady-state step in cudaProfilerStart/Stop (for ncu --profile-from-start off)")
     ap.add_argument("--no-clocks", action="store_true",
                     help="skip the nvidia-smi sampler and its load phase (ncu runs)")
     args = ap.parse_args()

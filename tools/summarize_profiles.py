@@ -27,27 +27,44 @@ s.write("kernel,launches,total_us,mean_us,share\n")
 for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     s.write(f"{name},{len(v)},{sum(v):.1f},{sum(v) / len(v):.1f},{sum(v) / tot:.3f}\n")
 (out / f"{tag}_launches_summary.csv").write_text(s.getvalue())
-# ---- full capture of the MPK launch
-rep = src / "prof_mpk.ncu-rep"
-summ = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(rep)], capture_output=True, text=True).stdout
-raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(raw.splitlines()))
-d = dict(zip(rr[0], rr[2]))
-def num(k):
-    return float(d[k].replace(",", ""))
-unit = dict(zip(rr[0], rr[1]))
-def to_bytes(k):
-    u = unit[k].lower()
-    return num(k) * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(u, 1)
-rd, wr = to_bytes("dram__bytes_read.sum"), to_bytes("dram__bytes_write.sum")
-dur = num("gpu__time_duration.sum") * ({"usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}.get(unit["gpu__time_duration.sum"], 1e-3))
-kname = d.get("Kernel Name", "")
-(out / f"{tag}_mpk_ring_kernel_ncu.txt").write_text(
-    f"# ncu --set full --clock-control none --import-source on -k regex:mpk_ring -s 4 -c 1 (bench.py cfg2)\n" + summ)
-nnz, n, k = 55_760_000, 8_000_000, 8
-Q = 12 * nnz + 4 * (n + 1) + 8 * n * (k + 1)
-(out / "traffic.json").write_text(json.dumps({
-    "round": int(tag[1:]), "kernel": kname, "source": f"ncu --set full --clock-control none, profiles/{tag}_mpk_ring_kernel_ncu.txt",
-    "dram_read_bytes": int(rd), "dram_write_bytes": int(wr), "dram_bytes_per_launch": int(rd + wr),
-    "algorithmic_bytes_per_launch": Q, "ncu_duration_ms": dur}, indent=2) + "\n")
-print(s.getvalue()); print(summ); print("traffic", rd + wr, "dur ms", dur)
+# ---- one full capture per config: the dominant kernel of one steady-state step
+CFG = {  # n, nnz, algorithmic bytes per launch of the dominant kernel
+    "cfg1": (65_536, 326_656, lambda n, z: 12 * z + 4 * (n + 1) + 8 * n * 5),
+    "cfg2": (8_000_000, 55_760_000, lambda n, z: 12 * z + 4 * (n + 1) + 8 * n * 9),
+    "cfg3": (4_096_000, 109_215_352, lambda n, z: 12 * z + 4 * (n + 1) + 8 * n * 9),
+    "cfg4": (4_194_304, 69_438_612, lambda n, z: 12 * z + 4 * (n + 1) + 16 * n),
+    "cfg5": (2_097_152, 14_680_064, lambda n, z: 12 * z + 4 * (n + 1) + 16 * n * 6),
+}
+traffic = {"round": int(tag[1:])}
+allsumm = ""
+for rep in sorted(src.glob("prof_cfg*.ncu-rep")):
+    cfg = rep.stem.split("_", 1)[1]
+    summ = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), str(rep)],
+                          capture_output=True, text=True).stdout
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    if len(rr) < 3:
+        continue
+    d = dict(zip(rr[0], rr[2]))
+    unit = dict(zip(rr[0], rr[1]))
+
+    def num(k):
+        return float(d[k].replace(",", ""))
+
+    def to_bytes(k):
+        return num(k) * {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}.get(unit[k].lower(), 1)
+
+    rd, wr = to_bytes("dram__bytes_read.sum"), to_bytes("dram__bytes_write.sum")
+    dur = num("gpu__time_duration.sum") * {"usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}.get(
+        unit["gpu__time_duration.sum"], 1e-3)
+    n, z, qf = CFG[cfg]
+    fn = f"{tag}_{cfg}_ncu.txt"
+    (out / fn).write_text(
+        f"# ncu --set full --clock-control none --import-source on --profile-from-start off -c 1:\n"
+        f"# the dominant kernel of one steady-state step of `python bench.py --config {cfg} --profile-step`\n" + summ)
+    traffic[cfg] = {"kernel": d.get("Kernel Name", ""), "source": f"profiles/{fn}",
+                    "dram_read_bytes": int(rd), "dram_write_bytes": int(wr), "dram_bytes_per_launch": int(rd + wr),
+                    "algorithmic_bytes_per_launch": qf(n, z), "ncu_duration_ms": dur}
+    allsumm += f"== {cfg}\n{summ}\n"
+(out / "traffic.json").write_text(json.dumps(traffic, indent=2) + "\n")
+print(s.getvalue()); print(allsumm); print(json.dumps(traffic, indent=1))
