@@ -280,6 +280,25 @@ int lmpk_segment_col_range(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t*
                            int64_t n_seg, const int64_t* seg_ptr, int32_t* out_min,
                            int32_t* out_max, void* stream);
 
+/* The item queue of a tiling as int32 triples (tile, first power (1-based),
+ * number of powers) in the order the kernel's producers take them; out may be
+ * NULL to query the count.  Host arrays.  Feeds the traffic oracle below with
+ * the schedule the GPU really walks. */
+int lmpk_tiling_items(const lmpk_tiling* t, int32_t* out, int64_t cap, int64_t* n_out);
+
+/* Software cache oracle (HOST pointers, no GPU work): replays the per-row
+ * accesses of a plan's items (row_start/row_end/power/in_slot/out_slot, int64
+ * [n_items]) in list order through a fully associative LRU of cap_lines lines
+ * of line_bytes; by_power int64[n_powers][4] receives the bytes missed per
+ * power and stream (val, col, row_ptr, y).  bypass != 0: no cache, every
+ * access counts its own size.  Replaces _sim_numba / _sim_python
+ * (pkg/src/levelmpk/traffic.py:78-189). */
+int lmpk_simulate_traffic(int64_t n_rows, const int32_t* row_ptr, const int32_t* col,
+                          int64_t n_items, const int64_t* row_start, const int64_t* row_end,
+                          const int64_t* power, const int64_t* in_slot, const int64_t* out_slot,
+                          int64_t n_powers, int64_t cap_lines, int64_t line_bytes, int bypass,
+                          int64_t* by_power);
+
 #ifdef __cplusplus
 }
 #endif

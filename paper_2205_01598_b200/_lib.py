@@ -110,7 +110,9 @@ SIGNATURES = {
     "lmpk_permute_vectors": (_int, [_vp, _i32, _vp, _vp, _i64, _vp, _i64, _i32, _i32, _int, _vp]),
     "lmpk_level_nnz": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "lmpk_segment_col_range": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
-    # micro-benchmarks (not part of the reference-facing ABI)
+    "lmpk_tiling_items": (_int, [_vp, _vp, _i64, _i64p]),
+    "lmpk_simulate_traffic": (_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                     _int, _vp]),
 }
 
 _lib = None

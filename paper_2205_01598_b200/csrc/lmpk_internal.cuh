@@ -115,6 +115,7 @@ struct lmpk_tiling {
   int32_t max_block = 0;           // largest tile block (bytes)
   int32_t slots = 1;               // staged items held per CTA
   std::vector<int32_t> h_tile_row, h_dep_lo, h_dep_hi;
+  std::vector<int32_t> h_items, h_st_first;  // host copies of the item queue (lmpk_tiling_items)
   // lean blocks (lean_kernel.cuh): width-sorted units, built when every tile
   // is a compressed tile of width <= 8 with one value format
   unsigned char* d_lean = nullptr;

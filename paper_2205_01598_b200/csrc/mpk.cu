@@ -927,6 +927,8 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
   std::vector<int32_t> items(order.size());
   for (size_t i = 0; i < order.size(); ++i) items[i] = ((order[i] / G) << 8) | (order[i] % G);
   T->n_items = static_cast<int32_t>(items.size());
+  T->h_items = items;
+  T->h_st_first = first;
   LMPK_TRY(dmalloc(&T->d_items, items.size()));
   LMPK_TRY(dmalloc(&T->d_st_first, ns + 1));
   LMPK_TRY(dmalloc(&T->d_st_lo, ns));
@@ -1160,6 +1162,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     items[i] = (t << 8) | g;
   }
   T->n_items = static_cast<int32_t>(items.size());
+  T->h_items = items;
   // reverse dependencies for the ready-queue walk (q = 1): u depends on t
   // iff t lies in [dep_lo(u), dep_hi(u)]
   if (q_used == 1) {
@@ -1193,6 +1196,28 @@ extern "C" int lmpk_tiling_geometry(const lmpk_tiling* t, int32_t* tile_row, int
   if (tile_row) memcpy(tile_row, t->h_tile_row.data(), (nt + 1) * 4);
   if (dep_lo) memcpy(dep_lo, t->h_dep_lo.data(), nt * 4);
   if (dep_hi) memcpy(dep_hi, t->h_dep_hi.data(), nt * 4);
+  return LMPK_OK;
+}
+
+// The item queue as (tile, first power, powers) triples in queue order: ring
+// tilings expand a super-tile item into its tiles; the group walk's items
+// cover powers_per_item consecutive powers of one tile.
+extern "C" int lmpk_tiling_items(const lmpk_tiling* t, int32_t* out, int64_t cap, int64_t* n_out) {
+  LMPK_ARG_CHECK(t != nullptr && n_out != nullptr, "lmpk_tiling_items: NULL argument");
+  const int32_t q = t->ring ? 1 : std::max(1, t->info.powers_per_item);
+  int64_t k = 0;
+  for (int32_t it : t->h_items) {
+    const int32_t s = it >> 8, g = it & 0xff;
+    const int32_t t0 = t->ring ? t->h_st_first[s] : s, t1 = t->ring ? t->h_st_first[s + 1] : s + 1;
+    const int32_t p0 = g * q + 1, np_ = std::min(q, t->info.p_m - g * q);
+    for (int32_t tt = t0; tt < t1; ++tt, ++k)
+      if (out && k < cap) {
+        out[3 * k] = tt;
+        out[3 * k + 1] = p0;
+        out[3 * k + 2] = np_;
+      }
+  }
+  *n_out = k;
   return LMPK_OK;
 }
 

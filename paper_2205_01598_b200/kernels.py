@@ -103,6 +103,20 @@ class Tiling:
             hi.ctypes.data_as(ctypes.c_void_p)))
         return tr, lo, hi
 
+    def item_order(self):
+        """int32 [n, 2] (tile, power) pairs in the order the kernel's item queue
+        hands them out (an item of q powers expands to q rows)."""
+        n = ctypes.c_int64()
+        check(self.ctx.lib.lmpk_tiling_items(self.handle, None, 0, ctypes.byref(n)))
+        raw = np.empty((int(n.value), 3), dtype=np.int32)
+        check(self.ctx.lib.lmpk_tiling_items(self.handle, raw.ctypes.data_as(ctypes.c_void_p),
+                                             int(n.value), ctypes.byref(n)))
+        reps = raw[:, 2]
+        tiles = np.repeat(raw[:, 0], reps)
+        first = np.repeat(raw[:, 1], reps)
+        offs = np.arange(int(reps.sum())) - np.repeat(np.cumsum(reps) - reps, reps)
+        return np.stack([tiles, first + offs], axis=1).astype(np.int64)
+
     def close(self):
         if getattr(self, "handle", None):
             self.ctx.lib.lmpk_tiling_destroy(self.handle)
