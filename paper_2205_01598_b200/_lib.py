@@ -111,6 +111,15 @@ SIGNATURES = {
     "lmpk_level_nnz": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "lmpk_segment_col_range": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "lmpk_tiling_items": (_int, [_vp, _vp, _i64, _i64p]),
+    # include/lmpk_plan.h
+    "lmpk_level_nnz_perm": (_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "lmpk_refine_span": (_int, [_vp, _i32, _vp, _int, _vp, _vp, _i32, _i32, _vp, _i64p, _vp]),
+    "lmpk_halo_seed": (_int, [_vp, _i32, _vp, _i64, _vp, _vp, _vp]),
+    "lmpk_halo_level_sort": (_int, [_vp, _i32, _vp, _int, _vp, _vp, _vp, _i32, _i32, _vp, _vp]),
+    "lmpk_invert_perm": (_int, [_vp, _i32, _vp, _vp, _vp]),
+    "lmpk_item_deps": (_int, [_vp, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp), _vp]),
+    "lmpk_host_free": (None, [_vp]),
+    "lmpk_item_col_max_in_range": (_int, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "lmpk_simulate_traffic": (_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
                                      _int, _vp]),
 }

@@ -571,3 +571,250 @@ extern "C" int lmpk_level_nnz(lmpk_ctx* ctx, const int32_t* row_ptr, const int64
   launch_count_add(ctx, 1);
   return LMPK_OK;
 }
+
+// ===================================================================
+// Recursive refinement (lmpk_plan.h): induced-subgraph BFS of a span and the
+// diamond-halo key sort, pkg/src/levelmpk/groups.py:238-335.
+#include "lmpk_plan.h"
+
+namespace lmpk {
+
+struct TmpBuf {  // cudaMalloc'ed scratch of one planning call
+  void* p = nullptr;
+  ~TmpBuf() {
+    if (p) cudaFree(p);
+  }
+  int alloc(size_t bytes) {
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(bytes, 16));
+    if (e != cudaSuccess) {
+      set_error("planning scratch cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+      p = nullptr;
+      return LMPK_ERR_NOMEM;
+    }
+    return LMPK_OK;
+  }
+  template <typename T>
+  T* as() {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_level_nnz_perm(const int32_t* row_ptr, const int32_t* perm, const int64_t* level_ptr,
+                                 int64_t L, int64_t* out) {
+  // one warp per level
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= L) return;
+  int64_t s = 0;
+  for (int64_t r = level_ptr[w] + lane; r < level_ptr[w + 1]; r += 32) {
+    const int32_t o = perm[r];
+    s += int64_t(row_ptr[o + 1]) - int64_t(row_ptr[o]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s;
+}
+
+__global__ void k_local_of(const int32_t* perm, int32_t r0, int32_t m, int32_t* local_of) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    local_of[perm[r0 + i]] = i;
+}
+
+// induced pattern: count (out_col == nullptr) or fill the kept neighbours of
+// local row i, in the order of the original row (groups.py:244-254)
+template <typename RP>
+__global__ void k_induced(const RP* sp, const int32_t* sc, const int32_t* perm, int32_t r0, int32_t m,
+                          const int32_t* local_of, int64_t* cnt, const int64_t* ptr, int32_t* out_col) {
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= m) return;
+  const int32_t o = perm[r0 + w];
+  const int64_t b = sp[o], e = sp[o + 1];
+  int64_t base = ptr ? ptr[w] : 0, total = 0;
+  for (int64_t k0 = b; k0 < e; k0 += 32) {
+    const int64_t k = k0 + lane;
+    const int32_t l = k < e ? local_of[sc[k]] : -1;
+    const uint32_t mask = __ballot_sync(0xffffffffu, l >= 0);
+    if (out_col && l >= 0) out_col[base + total + __popc(mask & ((1u << lane) - 1u))] = l;
+    total += __popc(mask);
+  }
+  if (!out_col && lane == 0) cnt[w] = total;
+}
+
+__global__ void k_apply_order(const int32_t* src, const int32_t* order, int32_t m, int32_t* dst) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    dst[i] = src[order[i]];
+}
+
+template <typename RP>
+static int refine_span(lmpk_ctx* ctx, int32_t n, const RP* sp, const int32_t* sc, int32_t* perm, int32_t r0,
+                       int32_t r1, int64_t* level_ptr_out, int64_t* n_levels, cudaStream_t st) {
+  const int32_t m = r1 - r0;
+  const size_t M = size_t(m);
+  TmpBuf b_local, b_cnt, b_col, b_perm;
+  LMPK_TRY(b_local.alloc(size_t(n) * 4));
+  LMPK_TRY(b_cnt.alloc((M + 2) * 8 * 2 + (scan_tmp_len(int64_t(m) + 1) + 8) * 8));
+  LMPK_TRY(b_perm.alloc(M * 4 * 3));
+  int32_t* local_of = b_local.as<int32_t>();
+  int64_t* cnt = b_cnt.as<int64_t>();
+  int64_t* ptr = cnt + M + 2;
+  int64_t* stmp = ptr + M + 2;
+  int32_t* perm_l = b_perm.as<int32_t>();
+  int32_t* inv_l = perm_l + M;
+  int32_t* old = inv_l + M;
+  k_fill_i32<<<grid_for(ctx, n), 256, 0, st>>>(local_of, n, -1);
+  k_local_of<<<grid_for(ctx, m), 256, 0, st>>>(perm, r0, m, local_of);
+  const int wgrid = int((int64_t(m) * 32 + 255) / 256);
+  k_induced<RP><<<wgrid, 256, 0, st>>>(sp, sc, perm, r0, m, local_of, cnt, nullptr, nullptr);
+  launch_count_add(ctx, 3);
+  LMPK_TRY(device_excl_scan<int64_t, int64_t>(ctx, cnt, m, ptr, 0, true, stmp, st));
+  int64_t total = 0;
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(&total, ptr + m, 8, cudaMemcpyDeviceToHost, st));
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  LMPK_TRY(b_col.alloc(size_t(total) * 4));
+  k_induced<RP><<<wgrid, 256, 0, st>>>(sp, sc, perm, r0, m, local_of, nullptr, ptr, b_col.as<int32_t>());
+  launch_count_add(ctx, 1);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  LMPK_TRY(bfs_core<int64_t>(ctx, m, ptr, b_col.as<int32_t>(), 0, perm_l, inv_l, level_ptr_out, n_levels, st));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(old, perm + r0, M * 4, cudaMemcpyDeviceToDevice, st));
+  k_apply_order<<<grid_for(ctx, m), 256, 0, st>>>(old, perm_l, m, perm + r0);
+  launch_count_add(ctx, 1);
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  return LMPK_OK;
+}
+
+__global__ void k_halo_seed(const int32_t* perm, int64_t G, const int64_t* gp, int32_t* key_orig) {
+  // one block per group
+  for (int64_t g = blockIdx.x; g < G; g += gridDim.x)
+    for (int64_t r = gp[g] + threadIdx.x; r < gp[g + 1]; r += blockDim.x) key_orig[perm[r]] = int32_t(g);
+}
+
+template <typename RP>
+__global__ void k_halo_keys(const RP* sp, const int32_t* sc, const int32_t* perm, int32_t lo, int32_t m,
+                            const int32_t* key_orig, uint32_t* keys, uint32_t* vals) {
+  const int64_t w = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= m) return;
+  const int32_t o = perm[lo + w];
+  int32_t best = -1;
+  for (int64_t k = int64_t(sp[o]) + lane; k < int64_t(sp[o + 1]); k += 32) best = max(best, key_orig[sc[k]]);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, s));
+  if (lane == 0) {
+    keys[w] = uint32_t(best + 1);
+    vals[w] = uint32_t(w);
+  }
+}
+
+__global__ void k_halo_apply(const int32_t* old, const uint32_t* skeys, const uint32_t* svals, int32_t m,
+                             int32_t* perm_lo, int32_t* key_orig, int32_t* keys_out) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int32_t v = old[svals[i]];
+    const int32_t k = int32_t(skeys[i]) - 1;
+    perm_lo[i] = v;
+    key_orig[v] = k;
+    keys_out[i] = k;
+  }
+}
+
+template <typename RP>
+static int halo_level_sort(lmpk_ctx* ctx, const RP* sp, const int32_t* sc, int32_t* perm, int32_t* key_orig,
+                           int32_t lo, int32_t hi, int32_t* keys_out, cudaStream_t st) {
+  const int32_t m = hi - lo;
+  if (m <= 0) return LMPK_OK;
+  const size_t M = size_t(m);
+  const int64_t cnt_len = radix_counts_len(m);
+  const int64_t tmp_len = scan_tmp_len(cnt_len) + 8;
+  TmpBuf b;
+  LMPK_TRY(b.alloc(M * 4 * 5 + size_t(cnt_len) * 12 + size_t(tmp_len) * 8 + 256));
+  uint32_t* k0 = b.as<uint32_t>();
+  uint32_t* v0 = k0 + M;
+  uint32_t* k1 = v0 + M;
+  uint32_t* v1 = k1 + M;
+  int32_t* old = reinterpret_cast<int32_t*>(v1 + M);
+  uintptr_t q = (reinterpret_cast<uintptr_t>(old + M) + 15) & ~uintptr_t(15);
+  int64_t* offsets = reinterpret_cast<int64_t*>(q);
+  int64_t* stmp = offsets + cnt_len;
+  uint32_t* counts = reinterpret_cast<uint32_t*>(stmp + tmp_len);
+  const int wgrid = int((int64_t(m) * 32 + 255) / 256);
+  k_halo_keys<RP><<<wgrid, 256, 0, st>>>(sp, sc, perm, lo, m, key_orig, k0, v0);
+  launch_count_add(ctx, 1);
+  bool in_first = true;
+  // keys are child group indices + 1: the child tree never has more groups than the matrix has rows
+  LMPK_TRY(device_radix_sort(ctx, k0, v0, k1, v1, m, 32, counts, offsets, stmp, &in_first, st));
+  LMPK_CHECK_CUDA(cudaMemcpyAsync(old, perm + lo, M * 4, cudaMemcpyDeviceToDevice, st));
+  k_halo_apply<<<grid_for(ctx, m), 256, 0, st>>>(old, in_first ? k0 : k1, in_first ? v0 : v1, m, perm + lo,
+                                                 key_orig, keys_out);
+  launch_count_add(ctx, 1);
+  LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  return LMPK_OK;
+}
+
+__global__ void k_invert_perm(int32_t n, const int32_t* perm, int32_t* inv) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) inv[perm[i]] = i;
+}
+
+}  // namespace lmpk
+
+extern "C" int lmpk_level_nnz_perm(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* perm,
+                                   const int64_t* level_ptr, int64_t n_levels, int64_t* out, void* stream) {
+  LMPK_ARG_CHECK(ctx && row_ptr && perm && level_ptr && out, "lmpk_level_nnz_perm: NULL argument");
+  if (n_levels <= 0) return LMPK_OK;
+  k_level_nnz_perm<<<int((n_levels * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(row_ptr, perm, level_ptr,
+                                                                                   n_levels, out);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 1);
+  return LMPK_OK;
+}
+
+extern "C" int lmpk_refine_span(lmpk_ctx* ctx, int32_t n, const void* sym_ptr, int ptr64, const int32_t* sym_col,
+                                int32_t* perm, int32_t r0, int32_t r1, int64_t* level_ptr_out, int64_t* n_levels,
+                                void* stream) {
+  LMPK_ARG_CHECK(ctx && sym_ptr && sym_col && perm && level_ptr_out && n_levels, "lmpk_refine_span: NULL argument");
+  LMPK_ARG_CHECK(0 <= r0 && r0 < r1 && r1 <= n, "span [%d, %d) out of range for n=%d", r0, r1, n);
+  cudaStream_t st = as_stream(stream);
+  if (ptr64)
+    return refine_span<int64_t>(ctx, n, static_cast<const int64_t*>(sym_ptr), sym_col, perm, r0, r1, level_ptr_out,
+                                n_levels, st);
+  return refine_span<int32_t>(ctx, n, static_cast<const int32_t*>(sym_ptr), sym_col, perm, r0, r1, level_ptr_out,
+                              n_levels, st);
+}
+
+extern "C" int lmpk_halo_seed(lmpk_ctx* ctx, int32_t n, const int32_t* perm, int64_t n_groups,
+                              const int64_t* group_ptr, int32_t* key_orig, void* stream) {
+  LMPK_ARG_CHECK(ctx && perm && group_ptr && key_orig, "lmpk_halo_seed: NULL argument");
+  cudaStream_t st = as_stream(stream);
+  k_fill_i32<<<grid_for(ctx, n), 256, 0, st>>>(key_orig, n, -1);
+  if (n_groups > 0)
+    k_halo_seed<<<int(std::min<int64_t>(n_groups, 4096)), 256, 0, st>>>(perm, n_groups, group_ptr, key_orig);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 2);
+  return LMPK_OK;
+}
+
+extern "C" int lmpk_halo_level_sort(lmpk_ctx* ctx, int32_t n, const void* sym_ptr, int ptr64,
+                                    const int32_t* sym_col, int32_t* perm, int32_t* key_orig, int32_t lo,
+                                    int32_t hi, int32_t* keys_out, void* stream) {
+  LMPK_ARG_CHECK(ctx && sym_ptr && sym_col && perm && key_orig && keys_out, "lmpk_halo_level_sort: NULL argument");
+  LMPK_ARG_CHECK(0 <= lo && lo <= hi && hi <= n, "level [%d, %d) out of range for n=%d", lo, hi, n);
+  cudaStream_t st = as_stream(stream);
+  if (ptr64)
+    return halo_level_sort<int64_t>(ctx, static_cast<const int64_t*>(sym_ptr), sym_col, perm, key_orig, lo, hi,
+                                    keys_out, st);
+  return halo_level_sort<int32_t>(ctx, static_cast<const int32_t*>(sym_ptr), sym_col, perm, key_orig, lo, hi,
+                                  keys_out, st);
+}
+
+extern "C" int lmpk_invert_perm(lmpk_ctx* ctx, int32_t n, const int32_t* perm, int32_t* inv, void* stream) {
+  LMPK_ARG_CHECK(ctx && perm && inv, "lmpk_invert_perm: NULL argument");
+  if (n <= 0) return LMPK_OK;
+  k_invert_perm<<<grid_for(ctx, n), 256, 0, as_stream(stream)>>>(n, perm, inv);
+  LMPK_CHECK_CUDA(cudaGetLastError());
+  launch_count_add(ctx, 1);
+  return LMPK_OK;
+}

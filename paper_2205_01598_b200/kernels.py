@@ -324,3 +324,102 @@ def vec_scale(x, c, out, stream=None):
     check(ctx.lib.lmpk_vec_scale(ctx.handle, int(n), ptr(xv), float(np.real(c)), float(np.imag(c)),
                                  1 if cplx else 0, ptr(ov), stream_handle(stream)), "vec_scale")
     return out
+
+
+# ---------------------------------------------------------------- planning (include/lmpk_plan.h)
+def _np_ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def sym_pattern_device(a: DeviceCsr):
+    """(ptr tensor, col tensor, ptr64) of A|A^T in HBM; A's own arrays when the
+    pattern is already symmetric (levels.py:48-61)."""
+    res = symmetrized_pattern(a)
+    if res is None:
+        return a.row_ptr, a.col, 0
+    return res[0], res[1], 1
+
+
+def level_nnz_perm(a: DeviceCsr, perm, level_ptr, stream=None):
+    """nnz per level of rows perm[level_ptr[i]:level_ptr[i+1]] of the original matrix."""
+    torch = _torch()
+    ctx = context()
+    lp = torch.as_tensor(np.ascontiguousarray(level_ptr, dtype=np.int64), device=a.row_ptr.device)
+    L = int(lp.shape[0] - 1)
+    out = torch.empty(max(L, 1), dtype=torch.int64, device=a.row_ptr.device)
+    check(ctx.lib.lmpk_level_nnz_perm(ctx.handle, ptr(a.row_ptr), ptr(perm), ptr(lp), L, ptr(out),
+                                      stream_handle(stream)), "level_nnz_perm")
+    return out[:L].cpu().numpy()
+
+
+def refine_span(n, sym, perm, r0, r1, stream=None):
+    """Induced-subgraph BFS of permuted rows [r0, r1); reorders perm[r0:r1] in
+    place and returns the child level_ptr (numpy int64, relative to r0)."""
+    torch = _torch()
+    ctx = context()
+    sp, sc, ptr64 = sym
+    lp = torch.empty(int(r1) - int(r0) + 1, dtype=torch.int64, device=perm.device)
+    nl = ctypes.c_int64()
+    check(ctx.lib.lmpk_refine_span(ctx.handle, int(n), ptr(sp), int(ptr64), ptr(sc), ptr(perm), int(r0), int(r1),
+                                   ptr(lp), ctypes.byref(nl), stream_handle(stream)), "refine_span")
+    return lp[: int(nl.value) + 1].cpu().numpy()
+
+
+def halo_seed(n, perm, group_ptr, key_orig, stream=None):
+    torch = _torch()
+    ctx = context()
+    gp = torch.as_tensor(np.ascontiguousarray(group_ptr, dtype=np.int64), device=perm.device)
+    check(ctx.lib.lmpk_halo_seed(ctx.handle, int(n), ptr(perm), int(gp.shape[0] - 1), ptr(gp), ptr(key_orig),
+                                 stream_handle(stream)), "halo_seed")
+
+
+def halo_level_sort(n, sym, perm, key_orig, lo, hi, stream=None):
+    """Stable key sort of the halo level [lo, hi) of perm; returns the sorted keys (numpy)."""
+    torch = _torch()
+    ctx = context()
+    sp, sc, ptr64 = sym
+    keys = torch.empty(max(int(hi) - int(lo), 1), dtype=torch.int32, device=perm.device)
+    check(ctx.lib.lmpk_halo_level_sort(ctx.handle, int(n), ptr(sp), int(ptr64), ptr(sc), ptr(perm), ptr(key_orig),
+                                       int(lo), int(hi), ptr(keys), stream_handle(stream)), "halo_level_sort")
+    return keys[: int(hi) - int(lo)].cpu().numpy()
+
+
+def invert_perm(perm, stream=None):
+    torch = _torch()
+    ctx = context()
+    inv = torch.empty_like(perm)
+    check(ctx.lib.lmpk_invert_perm(ctx.handle, int(perm.shape[0]), ptr(perm), ptr(inv), stream_handle(stream)),
+          "invert_perm")
+    return inv
+
+
+def item_deps(a: DeviceCsr, row_start, row_end, power, stream=None):
+    """True dependencies of a flat item list (plan.py:103-129) as (dep_ptr, dep)
+    numpy int64 arrays: item u depends on dep[dep_ptr[u]:dep_ptr[u+1]] (ascending)."""
+    ctx = context()
+    rs = np.ascontiguousarray(row_start, dtype=np.int64)
+    re = np.ascontiguousarray(row_end, dtype=np.int64)
+    pw = np.ascontiguousarray(power, dtype=np.int64)
+    n_items = int(rs.shape[0])
+    dep_ptr = np.zeros(n_items + 1, dtype=np.int64)
+    out = ctypes.c_void_p()
+    check(ctx.lib.lmpk_item_deps(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), n_items, _np_ptr(rs), _np_ptr(re),
+                                 _np_ptr(pw), _np_ptr(dep_ptr), ctypes.byref(out), stream_handle(stream)),
+          "item_deps")
+    try:
+        total = int(dep_ptr[-1])
+        dep = np.ctypeslib.as_array(ctypes.cast(out, ctypes.POINTER(ctypes.c_int64)), shape=(max(total, 1),))[:total].copy()
+    finally:
+        ctx.lib.lmpk_host_free(out)
+    return dep_ptr, dep
+
+
+def item_col_max_in_range(a: DeviceCsr, row_start, row_end, col_lo, col_hi, stream=None):
+    """Largest column of each item's rows inside [col_lo, col_hi) (-1: none)."""
+    ctx = context()
+    arrs = [np.ascontiguousarray(v, dtype=np.int64) for v in (row_start, row_end, col_lo, col_hi)]
+    out = np.full(arrs[0].shape[0], -1, dtype=np.int32)
+    check(ctx.lib.lmpk_item_col_max_in_range(ctx.handle, ptr(a.row_ptr), ptr(a.col), int(arrs[0].shape[0]),
+                                             *[_np_ptr(v) for v in arrs], _np_ptr(out), stream_handle(stream)),
+          "item_col_max_in_range")
+    return out

@@ -11,6 +11,15 @@ chunks and checks) and additionally owns the GPU execution geometry:
 ``plan.tiling()`` builds (once) the tile-SELL-32 blocks and the tile
 dependency ranges that liblmpk's level-blocked kernel walks.
 
+Refined spans (recursion): a SubgraphCall expands into the child schedule's
+items merged with the diamond pieces of the neighbouring outer groups
+(plan.py:73-181).  The merge is list scheduling against the true data
+dependencies; those come from the GPU (lmpk_item_deps: one bitmap row per
+item over the previous power's row intervals) instead of the reference's
+per-item ``np.unique`` over every read column, and the runtime checks of such
+plans (plan.py:322-370) use the same dependency lists plus one
+lmpk_item_col_max_in_range reduction for the boundary-granular decision.
+
 Runtime checks for whole level groups (s_m = 0) are derived from group
 geometry instead of the reference's per-item ``np.unique`` over all columns
 (plan.py:73-130, 15.6 s on cfg2): by level confinement, item (i, p) depends
@@ -20,6 +29,7 @@ per-group column range (one GPU reduction, lmpk_segment_col_range).  The
 result is identical to the reference's _runtime_checks for these plans.
 """
 
+import heapq
 from dataclasses import dataclass
 
 import numpy as np
@@ -28,7 +38,7 @@ from . import _lib
 from . import kernels as K
 from .csr import CsrMatrix
 from .groups import Preprocessed
-from .schedule import LpSchedule, build_schedule
+from .schedule import LpNode, LpSchedule, SubgraphCall, build_schedule
 
 CHECK_FULL = 0
 CHECK_BOUNDARY = 1
@@ -207,13 +217,7 @@ def build_plan(pre: Preprocessed, variant: str, workers: int,
         items = [FlatItem(0, n, p, 0, "group", 0, label=("baseline",)) for p in range(1, p_m + 1)]
     else:
         schedule = build_schedule(pre.tree, p_m)
-        groups = pre.tree.groups
-        items = [
-            FlatItem(groups[it.group].row_start, groups[it.group].row_end, it.power,
-                     schedule.stage, "group", groups[it.group].boundary_left_end,
-                     label=(schedule.stage, it.group))
-            for it in schedule.items
-        ]
+        items = _flatten(schedule, pre.tree, a)
     _validate_coverage(items, n, p_m)
     barrier = variant in BARRIER_VARIANTS
     n_items = len(items)
@@ -227,7 +231,10 @@ def build_plan(pre: Preprocessed, variant: str, workers: int,
     check_item = np.empty(0, dtype=np.int64)
     check_kind = np.empty(0, dtype=np.int64)
     if not barrier:
-        check_ptr, check_item, check_kind = _runtime_checks(pre, schedule, items)
+        if pre.tree.spans:
+            check_ptr, check_item, check_kind = _runtime_checks_general(items, a)
+        else:
+            check_ptr, check_item, check_kind = _runtime_checks(pre, schedule, items)
     return ExecPlan(
         variant=variant, p_m=p_m, workers=workers, n_rows=n, items=items, barrier=barrier,
         row_start=row_start, row_end=row_end, power=power, chunks=chunks, bnd_point=bnd_point,
@@ -236,6 +243,129 @@ def build_plan(pre: Preprocessed, variant: str, workers: int,
         prev_slot=np.maximum(power - 2, 0), kernel=np.zeros(n_items, dtype=np.int64),
         acc_coef=np.zeros(n_items, dtype=np.float64),
     )
+
+
+def _flatten(sched: LpSchedule, tree, a_perm):
+    """Flat items of a schedule; SubgraphCalls expand recursively (plan.py:52-70)."""
+    out = []
+    for it in sched.items:
+        if isinstance(it, LpNode):
+            g = tree.groups[it.group]
+            out.append(FlatItem(g.row_start, g.row_end, it.power, sched.stage, "group",
+                                g.boundary_left_end, label=(sched.stage, it.group)))
+        else:
+            inner = _flatten(it.child, it.span.tree, a_perm)
+            out.extend(_merge_diamond(inner, _diamond_pieces(it), a_perm))
+    return out
+
+
+def _diamond_pieces(call: SubgraphCall):
+    """(item, priority) of every outer diamond piece of one subgraph step: halo
+    group at distance delta runs its powers delta+1 .. p_m-delta in level /
+    key-portion pieces (plan.py:73-100); priority = (power, side, delta, level,
+    key, portion)."""
+    p_m = call.child.p_m
+    out = []
+    for side, split in enumerate((call.span.left_split, call.span.right_split)):
+        if split is None:
+            continue
+        for gi, delta in split.groups:
+            for p in range(delta + 1, p_m - delta + 1):
+                for li, lev in enumerate(split.levels_by_group[gi]):
+                    for k, ((lo, hi), key) in enumerate(zip(lev.portions, lev.keys)):
+                        if hi > lo:
+                            out.append((FlatItem(lo, hi, p, call.stage, "outer", lo, label=(call.stage, gi, li, k)),
+                                        (p, side, delta, li, key, k)))
+    return out
+
+
+def _item_dep_lists(items, a_perm):
+    """dep_ptr, dep of a flat item list from the GPU (plan.py:103-129)."""
+    return K.item_deps(a_perm.device(), [it.row_start for it in items], [it.row_end for it in items],
+                       [it.power for it in items])
+
+
+def _merge_diamond(inner, pieces, a_perm):
+    """List-schedule child items and outer pieces against their true
+    dependencies (plan.py:132-175): a ready outer piece always goes first
+    (lowest priority tuple), otherwise the ready child item that comes first
+    in the child walk."""
+    if not pieces:
+        return inner
+    items = list(inner) + [it for it, _ in pieces]
+    n_in, n = len(inner), len(items)
+    dep_ptr, dep = _item_dep_lists(items, a_perm)
+    unmet = np.diff(dep_ptr).astype(np.int64)
+    users = [[] for _ in range(n)]
+    for u in range(n):
+        for d in dep[dep_ptr[u]:dep_ptr[u + 1]]:
+            users[int(d)].append(u)
+    ready_in, ready_out = [], []
+
+    def release(u):
+        if u < n_in:
+            heapq.heappush(ready_in, u)
+        else:
+            heapq.heappush(ready_out, (pieces[u - n_in][1], u))
+
+    for u in np.flatnonzero(unmet == 0):
+        release(int(u))
+    order = []
+    while ready_in or ready_out:
+        u = heapq.heappop(ready_out)[1] if ready_out else heapq.heappop(ready_in)
+        order.append(u)
+        for v in users[u]:
+            unmet[v] -= 1
+            if unmet[v] == 0:
+                release(v)
+    if len(order) != n:
+        raise RuntimeError("cyclic dependencies in diamond merge (bug)")
+    return [items[u] for u in order]
+
+
+def _runtime_checks_general(items, a_perm):
+    """Spin checks of an arbitrary flat plan (plan.py:322-370): condition (A) =
+    the latest dependency overlapping the item's own rows (else the latest
+    dependency), FULL; one more check on the latest dependency after it,
+    BOUNDARY-granular when the item's columns inside that target stay left
+    of its boundary_end.  Also validates the topological order."""
+    n = len(items)
+    dep_ptr, dep = _item_dep_lists(items, a_perm)
+    rs = np.array([it.row_start for it in items], dtype=np.int64)
+    re = np.array([it.row_end for it in items], dtype=np.int64)
+    first = np.full(n, -1, dtype=np.int64)
+    second = np.full(n, -1, dtype=np.int64)
+    for u in range(n):
+        d = dep[dep_ptr[u]:dep_ptr[u + 1]]
+        if not d.size:
+            continue
+        if d[-1] >= u:
+            bad = items[int(d[-1])]
+            raise RuntimeError(
+                f"schedule order violates dependency: item {u} {items[u].label} "
+                f"p={items[u].power} needs later item {bad.label} p={bad.power}")
+        own = d[(rs[d] < re[u]) & (re[d] > rs[u])]
+        first[u] = own[-1] if own.size else d[-1]
+        if d[-1] > first[u]:
+            second[u] = d[-1]
+    has2 = second >= 0
+    tgt = np.where(has2, second, 0)
+    col_lo = np.where(has2, rs[tgt], 0)
+    col_hi = np.where(has2, re[tgt], 0)
+    cmax = K.item_col_max_in_range(a_perm.device(), rs, re, col_lo, col_hi) if has2.any() else None
+    bnd = np.array([it.boundary_end for it in items], dtype=np.int64)
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    out_item, out_kind = [], []
+    for u in range(n):
+        if first[u] >= 0:
+            out_item.append(int(first[u]))
+            out_kind.append(CHECK_FULL)
+            if has2[u]:
+                m = int(second[u])
+                out_item.append(m)
+                out_kind.append(CHECK_BOUNDARY if 0 <= cmax[u] < bnd[m] else CHECK_FULL)
+        ptr[u + 1] = len(out_item)
+    return ptr, np.asarray(out_item, dtype=np.int64), np.asarray(out_kind, dtype=np.int64)
 
 
 def _runtime_checks(pre: Preprocessed, schedule: LpSchedule, items):

@@ -12,19 +12,21 @@ import pytest
 from paper_2205_01598_b200 import _lib
 
 ROOT = pathlib.Path(__file__).resolve().parent.parent
-HEADER = ROOT / "include" / "lmpk.h"
+HEADERS = sorted((ROOT / "include").glob("*.h"))  # lmpk.h, lmpk_plan.h
 
 
 def declared_functions():
-    text = HEADER.read_text()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(lmpk_\w+)\s*\(", text, re.M)))
+    names = set()
+    for header in HEADERS:
+        text = re.sub(r"/\*.*?\*/", "", header.read_text(), flags=re.S)
+        names |= set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(lmpk_\w+)\s*\(", text, re.M))
+    return sorted(names)
 
 
 def test_library_exports_every_declared_symbol():
     lib = _lib.load_library()
     names = declared_functions()
-    assert len(names) >= 18
+    assert len(names) >= 34
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
