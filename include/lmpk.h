@@ -151,6 +151,10 @@ typedef struct lmpk_tiling_info {
   int64_t lean_bytes;    /* ring walk: width-sorted lean copy of the blocks    */
                          /* (0: the tiling runs the general ring kernel)      */
   int32_t lean_pattern_tiles; /* lean tiles storing each slice's distinct rows once */
+  int32_t lean_xstaged;  /* 1: the lean walk stages the gathered runs of y_{p-1} */
+                         /* in shared memory (a piece = lean block + x buffer)  */
+  int32_t lean_ring;     /* staged lean walk: pieces in the shared-memory ring   */
+  int32_t lean_piece;    /* staged lean walk: bytes of one piece                 */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */

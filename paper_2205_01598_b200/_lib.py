@@ -56,6 +56,7 @@ class TilingInfo(ctypes.Structure):
         ("powers_per_item", _i32), ("slots", _i32), ("x_staged_tiles", _i32),
         ("compressed_tiles", _i32), ("dict_tiles", _i32), ("super_tiles", _i32),
         ("lean_bytes", _i64), ("lean_pattern_tiles", _i32),
+        ("lean_xstaged", _i32), ("lean_ring", _i32), ("lean_piece", _i32),
     ]
 
     def as_dict(self):

@@ -55,7 +55,17 @@ struct LeanParams {
   const unsigned char* blocks;  // lean tile blocks
   const int64_t* ofs;           // [n_tiles + 1] byte offset of each lean block
   const uint8_t* rowlen;        // [n] row lengths (slow path only)
+  // x staging (mpk_xlean_kernel): per tile the runs of y_{p-1} its rows gather,
+  // bulk-copied behind the block; column fields then hold (buffer index - lane)
+  const int4* runs;             // [n_tiles * kLeanMaxRuns] {first entry, entries, buffer entry, 0}
+  const int2* xinfo;            // [n_tiles] {runs, staged entries}
+  int32_t xoff;                 // byte offset of the x buffer inside a piece
+  int32_t np;                   // ring depth (pieces) of the staged kernel
+  const int4* wl;               // per-CTA static work lists (2 x int4 per piece), or null: ticket queue
+  const int32_t* wl_ptr;        // [grid + 1]
+  int32_t pub_batch;            // pieces the publisher makes visible per gpu-scope fence (1..8)
 };
+constexpr int kLeanMaxRuns = 32;  // one bulk copy per producer lane
 
 // ---------------------------------------------------------------- row sums
 // Shared-memory reads by 32-bit address.  They are plain (non-volatile) asm
@@ -153,10 +163,26 @@ struct LeanX<true> {
   using T = double2;
 };
 
+// Row pointer of the gathers: &x[row] in global memory, or (x staging) the
+// 32-bit shared address of the lane's base entry in the piece's x buffer.
+template <bool XS>
+struct LeanRp {
+  using T = const char*;
+};
+template <>
+struct LeanRp<true> {
+  using T = uint32_t;
+};
+
 // gather of x[row + d] (row pointer rp = &x[row])
-template <bool CPLX>
-__device__ __forceinline__ typename LeanX<CPLX>::T lean_gather(const char* rp, int32_t d) {
-  if constexpr (CPLX) {
+template <bool CPLX, bool XS = false>
+__device__ __forceinline__ typename LeanX<CPLX>::T lean_gather(typename LeanRp<XS>::T rp, int32_t d) {
+  if constexpr (XS) {
+    if constexpr (CPLX)
+      return lds_d2(rp + uint32_t(d) * 16u);
+    else
+      return lds_d(rp + uint32_t(d) * 8u);
+  } else if constexpr (CPLX) {
     double2 v;
     asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(rp + int64_t(d) * 16));
     return v;
@@ -189,9 +215,9 @@ __device__ __forceinline__ LeanSum<CPLX> lean_chain(const double (&v)[W], const 
 
 // One slice of width W: lane's row sum in storage order (real or complex x).
 // cp/vp: lane's column-offset / code (or slice-base raw value) addresses.
-template <int W, bool CPLX, bool EXACT, bool VD>
+template <int W, bool CPLX, bool EXACT, bool VD, bool XS = false>
 __device__ __forceinline__ LeanSum<CPLX> lean_slice(uint32_t cp, uint32_t vp, uint32_t dict, uint32_t lane,
-                                                    const char* rp) {
+                                                    typename LeanRp<XS>::T rp) {
   if constexpr (W == 0) {
     return LeanSum<CPLX>{0.0, 0.0};
   } else {
@@ -199,7 +225,7 @@ __device__ __forceinline__ LeanSum<CPLX> lean_slice(uint32_t cp, uint32_t vp, ui
     lean_cols<W>(cp, c);
     typename LeanX<CPLX>::T x[W];
 #pragma unroll
-    for (int j = 0; j < W; ++j) x[j] = lean_gather<CPLX>(rp, c[j]);
+    for (int j = 0; j < W; ++j) x[j] = lean_gather<CPLX, XS>(rp, c[j]);
     double v[W];
     if constexpr (VD)
       lean_dvals<W>(vp, dict, v);
@@ -210,10 +236,10 @@ __device__ __forceinline__ LeanSum<CPLX> lean_slice(uint32_t cp, uint32_t vp, ui
 }
 
 // Two slices of the same width: every gather of both in flight at once.
-template <int W, bool CPLX, bool EXACT, bool VD>
+template <int W, bool CPLX, bool EXACT, bool VD, bool XS = false>
 __device__ __forceinline__ void lean_pair(uint32_t cp0, uint32_t vp0, uint32_t cp1, uint32_t vp1, uint32_t dict,
-                                          uint32_t lane, const char* rp0, const char* rp1, LeanSum<CPLX>& s0,
-                                          LeanSum<CPLX>& s1) {
+                                          uint32_t lane, typename LeanRp<XS>::T rp0, typename LeanRp<XS>::T rp1,
+                                          LeanSum<CPLX>& s0, LeanSum<CPLX>& s1) {
   if constexpr (W == 0) {
     s0 = s1 = LeanSum<CPLX>{0.0, 0.0};
   } else {
@@ -222,9 +248,9 @@ __device__ __forceinline__ void lean_pair(uint32_t cp0, uint32_t vp0, uint32_t c
     lean_cols<W>(cp1, c1);
     typename LeanX<CPLX>::T x0[W], x1[W];
 #pragma unroll
-    for (int j = 0; j < W; ++j) x0[j] = lean_gather<CPLX>(rp0, c0[j]);
+    for (int j = 0; j < W; ++j) x0[j] = lean_gather<CPLX, XS>(rp0, c0[j]);
 #pragma unroll
-    for (int j = 0; j < W; ++j) x1[j] = lean_gather<CPLX>(rp1, c1[j]);
+    for (int j = 0; j < W; ++j) x1[j] = lean_gather<CPLX, XS>(rp1, c1[j]);
     {
       double v[W];
       if constexpr (VD)
@@ -246,9 +272,9 @@ __device__ __forceinline__ void lean_pair(uint32_t cp0, uint32_t vp0, uint32_t c
 
 // Slow path of a padded row whose sum came out NaN: the row again with its
 // true length (padding entries skipped), exactly as the reference sums it.
-template <bool CPLX, bool EXACT, bool VD>
+template <bool CPLX, bool EXACT, bool VD, bool XS = false>
 __device__ __noinline__ LeanSum<CPLX> lean_row_exact(uint32_t cp, uint32_t vp, uint32_t dict, uint32_t lane,
-                                                     const char* rp, int w, int len) {
+                                                     typename LeanRp<XS>::T rp, int w, int len) {
   LeanSum<CPLX> s{0.0, 0.0};
   const int Q = w >> 2, PR = (w >> 1) & 1;
   for (int j = 0; j < len; ++j) {
@@ -267,7 +293,7 @@ __device__ __noinline__ LeanSum<CPLX> lean_row_exact(uint32_t cp, uint32_t vp, u
         e = uint32_t(Q) * 128u + (PR ? 64u : 0u) + lane;
       v = lds_d(vp + e * 8u);
     }
-    const typename LeanX<CPLX>::T x = lean_gather<CPLX>(rp, c);
+    const typename LeanX<CPLX>::T x = lean_gather<CPLX, XS>(rp, c);
     if constexpr (CPLX) {
       s.r = madd<EXACT>(s.r, v, x.x);
       s.i = madd<EXACT>(s.i, v, x.y);
@@ -336,22 +362,34 @@ __device__ __forceinline__ void lean_ptrs(uint32_t blk, uint32_t off, uint32_t n
 // One unit of width W (compile time): a pair or a single slice.
 // Record: plain {col off, value off, W | flags, slice ids}; pattern
 // {slice a off, slice b off, W | flags | Pa << 16 | Pb << 24, slice ids}.
-template <int W, bool CPLX, bool EXACT, bool VD, bool GEN>
+// XS (x staging): the column fields hold (x-buffer entry - lane) and the
+// gathers read the piece's x buffer at shared address xb.
+template <int W, bool CPLX, bool EXACT, bool VD, bool GEN, bool XS = false>
 __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane, int32_t r0, int32_t nrows,
-                                          const PowTab& pt, double* acc, bool use_acc, const uint8_t* rowlen) {
+                                          const PowTab& pt, double* acc, bool use_acc, const uint8_t* rowlen,
+                                          uint32_t xb = 0) {
   constexpr int cw = CPLX ? 16 : 8;
+  using RP = typename LeanRp<XS>::T;
   const uint32_t dict = blk + kLeanDict;
   const int32_t s0 = int32_t(rec.w & 0xffffu), s1 = int32_t(rec.w >> 16);
   const int32_t l0 = s0 * 32 + int32_t(lane), l1 = s1 * 32 + int32_t(lane);
   const bool pat = VD && (rec.z & kLeanPattern) != 0;
   // lanes past the tile (last slice) use the last valid lane's pattern: gather
   // around that row (their sums are discarded)
-  const char* rp0 = pt.yin + int64_t(r0 + (pat ? min(l0, nrows - 1) : l0)) * cw;
+  RP rp0;
+  if constexpr (XS)
+    rp0 = xb + uint32_t(pat ? min(int32_t(lane), nrows - 1 - s0 * 32) : int32_t(lane)) * uint32_t(cw);
+  else
+    rp0 = pt.yin + int64_t(r0 + (pat ? min(l0, nrows - 1) : l0)) * cw;
   uint32_t cp0, vp0;
   lean_ptrs<W, VD>(blk, rec.x, (rec.z >> 16) & 255u, pat, lane, cp0, vp0, rec.y);
   const bool padded = (rec.z & kLeanPadded) != 0;
   if (rec.z & kLeanPair) {
-    const char* rp1 = pt.yin + int64_t(r0 + (pat ? min(l1, nrows - 1) : l1)) * cw;
+    RP rp1;
+    if constexpr (XS)
+      rp1 = xb + uint32_t(pat ? min(int32_t(lane), nrows - 1 - s1 * 32) : int32_t(lane)) * uint32_t(cw);
+    else
+      rp1 = pt.yin + int64_t(r0 + (pat ? min(l1, nrows - 1) : l1)) * cw;
     uint32_t cp1, vp1;
     if (pat) {
       lean_ptrs<W, VD>(blk, rec.y, rec.z >> 24, true, lane, cp1, vp1, 0u);
@@ -360,20 +398,132 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
       vp1 = vp0 + (VD ? lean_code_bytes(W) : lean_raw_bytes(W));
     }
     LeanSum<CPLX> a, b;
-    lean_pair<W, CPLX, EXACT, VD>(cp0, vp0, cp1, vp1, dict, lane, rp0, rp1, a, b);
+    lean_pair<W, CPLX, EXACT, VD, XS>(cp0, vp0, cp1, vp1, dict, lane, rp0, rp1, a, b);
     if (padded) {
       if (lean_nan(a.r) || (CPLX && lean_nan(a.i)))
-        if (l0 < nrows) a = lean_row_exact<CPLX, EXACT, VD>(cp0, vp0, dict, lane, rp0, W, rowlen[r0 + l0]);
+        if (l0 < nrows) a = lean_row_exact<CPLX, EXACT, VD, XS>(cp0, vp0, dict, lane, rp0, W, rowlen[r0 + l0]);
       if (lean_nan(b.r) || (CPLX && lean_nan(b.i)))
-        if (l1 < nrows) b = lean_row_exact<CPLX, EXACT, VD>(cp1, vp1, dict, lane, rp1, W, rowlen[r0 + l1]);
+        if (l1 < nrows) b = lean_row_exact<CPLX, EXACT, VD, XS>(cp1, vp1, dict, lane, rp1, W, rowlen[r0 + l1]);
     }
     if (l0 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
     if (l1 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l1), b);
   } else {
-    LeanSum<CPLX> a = lean_slice<W, CPLX, EXACT, VD>(cp0, vp0, dict, lane, rp0);
+    LeanSum<CPLX> a = lean_slice<W, CPLX, EXACT, VD, XS>(cp0, vp0, dict, lane, rp0);
     if (padded && (lean_nan(a.r) || (CPLX && lean_nan(a.i))))
-      if (l0 < nrows) a = lean_row_exact<CPLX, EXACT, VD>(cp0, vp0, dict, lane, rp0, W, rowlen[r0 + l0]);
+      if (l0 < nrows) a = lean_row_exact<CPLX, EXACT, VD, XS>(cp0, vp0, dict, lane, rp0, W, rowlen[r0 + l0]);
     if (l0 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
+  }
+}
+
+// ---------------------------------------------------------------- XP units
+// Staged dictionary tilings whose slices repeat few distinct rows (structured
+// grids) use XP blocks: a unit is a run of m <= 4 consecutive slices.  Its
+// data is one ROW RECORD per distinct row of the slice --
+//   [Wc x i32: (x-buffer entry - lane) * entry bytes][Wc x f64: values]
+// -- behind 32 u8 record ids when the rows differ; a UNIFORM unit (every row
+// of every slice the same record, the interior of a grid) holds the one
+// record and no ids, and its m slices reuse the registers: slice i gathers at
+// the same fields + 32 i entries.  A row costs no index arithmetic beyond one
+// add per gather and no dictionary lookups.
+constexpr uint32_t kXpUniform = 1u << 8, kXpPadded = 1u << 9;
+__host__ __device__ constexpr int xp_rec_bytes(int w) { return 12 * lean_wc(w); }
+
+template <int W>
+__device__ __forceinline__ void xp_load(uint32_t ra, int32_t (&c)[W], double (&v)[W]) {
+  constexpr int WC = lean_wc(W);
+  {
+    const uint4 a = lds_v4(ra);
+    const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 0; j < (W < 4 ? W : 4); ++j) c[j] = int32_t(w4[j]);
+  }
+  if constexpr (W > 4) {
+    const uint4 a = lds_v4(ra + 16);
+    const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+    for (int j = 4; j < W; ++j) c[j] = int32_t(w4[j - 4]);
+  }
+#pragma unroll
+  for (int j = 0; j + 1 < W; j += 2) {
+    const double2 d = lds_d2(ra + 4 * WC + 8 * j);
+    v[j] = d.x, v[j + 1] = d.y;
+  }
+  if constexpr (W & 1) v[W - 1] = lds_d(ra + 4 * WC + 8 * (W - 1));
+}
+
+// gather at byte offset c from the lane's row pointer (x staging: shared)
+template <bool CPLX, bool XS>
+__device__ __forceinline__ typename LeanX<CPLX>::T xp_gather(typename LeanRp<XS>::T rp, int32_t c) {
+  if constexpr (XS) {
+    if constexpr (CPLX)
+      return lds_d2(rp + uint32_t(c));
+    else
+      return lds_d(rp + uint32_t(c));
+  } else if constexpr (CPLX) {
+    double2 v;
+    asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(rp + int64_t(c)));
+    return v;
+  } else {
+    double v;
+    asm("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(rp + int64_t(c)));
+    return v;
+  }
+}
+
+// slow path of a padded row whose sum came out NaN: the row's true length
+template <bool CPLX, bool EXACT, bool XS>
+__device__ __noinline__ LeanSum<CPLX> xp_row_exact(uint32_t ra, typename LeanRp<XS>::T rp, int wc, int len) {
+  LeanSum<CPLX> s{0.0, 0.0};
+  for (int j = 0; j < len; ++j) {
+    const int32_t c = int32_t(lds_u32(ra + 4 * j));
+    const double v = lds_d(ra + 4 * wc + 8 * j);
+    const typename LeanX<CPLX>::T x = xp_gather<CPLX, XS>(rp, c);
+    if constexpr (CPLX) {
+      s.r = madd<EXACT>(s.r, v, x.x);
+      s.i = madd<EXACT>(s.i, v, x.y);
+    } else {
+      s.r = madd<EXACT>(s.r, v, x);
+    }
+  }
+  return s;
+}
+
+// rec = {data offset, first slice | m << 16, W | flags, records}.  XS: the
+// fields are x-buffer offsets (gathers from shared memory at xb); otherwise
+// (column - row) byte offsets and the gathers read y_{p-1} in global memory.
+template <int W, bool CPLX, bool EXACT, bool GEN, bool XS = true>
+__device__ __forceinline__ void xp_unit(uint32_t blk, uint4 rec, uint32_t lane, int32_t r0, int32_t nrows,
+                                        const PowTab& pt, double* acc, bool use_acc, const uint8_t* rowlen,
+                                        uint32_t xb) {
+  constexpr uint32_t cw = CPLX ? 16u : 8u;
+  const int32_t m = int32_t(rec.y >> 16);
+  int32_t lr = int32_t(rec.y & 0xffffu) * 32 + int32_t(lane);  // tile-local row
+  typename LeanRp<XS>::T rp;
+  if constexpr (XS)
+    rp = xb + lane * cw;
+  else
+    rp = pt.yin + int64_t(r0 + lr) * int64_t(cw);
+  if constexpr (W == 0) {
+    for (int32_t i = 0; i < m; ++i, lr += 32)
+      if (lr < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + lr), LeanSum<CPLX>{0.0, 0.0});
+  } else {
+    uint32_t ra = blk + rec.x;
+    if (!(rec.z & kXpUniform)) ra += 32u + lds_b8(ra + lane) * uint32_t(xp_rec_bytes(W));
+    int32_t c[W];
+    double v[W];
+    xp_load<W>(ra, c, v);
+    const bool padded = (rec.z & kXpPadded) != 0;
+    for (int32_t i = 0; i < m; ++i) {
+      typename LeanX<CPLX>::T x[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) x[j] = xp_gather<CPLX, XS>(rp, c[j]);
+      LeanSum<CPLX> a = lean_chain<W, CPLX, EXACT>(v, x);
+      if (padded && (lean_nan(a.r) || (CPLX && lean_nan(a.i))))
+        if (lr < nrows) a = xp_row_exact<CPLX, EXACT, XS>(ra, rp, lean_wc(W), rowlen[r0 + lr]);
+      if (lr < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + lr), a);
+      rp += 32u * cw;
+      lr += 32;
+    }
   }
 }
 
@@ -390,7 +540,7 @@ __device__ __forceinline__ uint32_t lean_wait(uint64_t* bar, uint32_t parity, ui
 // ---------------------------------------------------------------- kernel
 // Same launch contract as mpk_ring_kernel (cooperative, one CTA per SM, a
 // 2-piece ring): warp NC is the producer, warp NC + 1 the publisher.
-template <bool CPLX, bool EXACT, bool VD, bool GEN, int NP>
+template <bool CPLX, bool EXACT, bool VD, bool GEN, int NP, bool XP = false>
 __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
     mpk_lean_kernel(MpkParams P, PowerCfgDev C, LeanParams L) {
   constexpr int NC = kLeanConsumers;
@@ -511,6 +661,33 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
       // static striding, rotated by the piece counter
       int32_t u = warp + int32_t(k % uint32_t(NC));
       if (u >= NC) u -= NC;
+      if (XP && lds_u32(blk + 8) == 2u) {
+        // XP block (row records, units of up to 4 slices; the units are
+        // binned per consumer warp at build time, bin starts at blk + 16)
+        const uint32_t b2 = lds_u32(blk + 16u + 2u * uint32_t(u & ~1));
+        const int32_t ub = (u & 1) ? int32_t(b2 >> 16) : int32_t(b2 & 0xffffu);
+        const uint32_t e2 = lds_u32(blk + 16u + 2u * uint32_t((u + 1) & ~1));
+        const int32_t ue = ((u + 1) & 1) ? int32_t(e2 >> 16) : int32_t(e2 & 0xffffu);
+        for (int32_t q = ub; q < ue; ++q) {
+          const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(q) * 16u);
+          switch (rec.z & 15u) {
+#define LMPK_XP_CASE(Wv) \
+  case Wv: xp_unit<Wv, CPLX, EXACT, GEN, false>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen, 0u); break;
+            LMPK_XP_CASE(0)
+            LMPK_XP_CASE(1)
+            LMPK_XP_CASE(2)
+            LMPK_XP_CASE(3)
+            LMPK_XP_CASE(4)
+            LMPK_XP_CASE(5)
+            LMPK_XP_CASE(6)
+            LMPK_XP_CASE(7)
+            LMPK_XP_CASE(8)
+#undef LMPK_XP_CASE
+            default: break;
+          }
+        }
+        u = nu;  // the lean loop below is skipped
+      }
       for (; u < nu; u += NC) {
         const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);
         switch (rec.z & 15u) {
@@ -538,6 +715,340 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
         d_done[slot] = 0;
         mbar_arrive(&done_bar[slot]);
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- staged kernel
+// The lean walk with x staging: a piece is [lean block | x buffer].  The
+// producer bulk-copies, behind the tile's block, the runs of y_{p-1} the tile's
+// rows gather (LeanParams::runs, planned once per tiling by k_lean_xplan) --
+// after the item's dependencies were acquired, with a generic->async proxy
+// fence in between -- and the consumers gather from shared memory: an
+// unaligned 32 x 8 B gather costs 2 shared-memory wavefronts instead of 3 L1
+// tag lookups and never waits for an L1 miss.  Ring depth L.np (2..4, run
+// time): the slot and its phase are stepped, not divided.
+// Dependency wait of the staged kernel: progress[lo..hi] >= target with
+// ACQUIRE loads (LDG.STRONG.GPU + CCTL.IVALL) instead of relaxed loads and a
+// gpu-scope fence (MEMBAR.ALL.GPU: ~1 us on a busy SM, once per item): the
+// data behind the flags is only read by the bulk copies issued afterwards.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool spin_deps_acq(const MpkParams& P, int32_t lo, int32_t hi, uint32_t target,
+                                              unsigned long long* rounds) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long t0 = 0;
+  for (int spins = 0;; ++spins) {
+    uint32_t m = 0xffffffffu;
+    for (int32_t i = lo + lane; i <= hi; i += 32) m = min(m, ld_acquire_u32(P.progress + i));
+    ++*rounds;
+    if (__all_sync(0xffffffffu, m >= target)) return true;
+    if (spins > 2) __nanosleep(64);
+    if ((spins & 63) == 63) {
+      const unsigned long long now = globaltimer();
+      if (t0 == 0) t0 = now;
+      const volatile unsigned long long* ab = P.queue + 1;
+      bool stop = *ab != 0ull;
+      if (!stop && now - t0 > kWatchdogNs) {
+        if (lane == 0) {
+          atomicExch(P.queue + 1, 1ull);
+          *P.err = 1;
+        }
+        stop = true;
+      }
+      if (__any_sync(0xffffffffu, stop)) return false;
+    }
+  }
+}
+
+constexpr int kXleanRingMax = 4;
+template <bool CPLX, bool EXACT, bool VD, bool GEN, bool XP = false>
+__global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
+    mpk_xlean_kernel(MpkParams P, PowerCfgDev C, LeanParams L) {
+  constexpr int NC = kLeanConsumers;
+  constexpr int NPM = kXleanRingMax;
+  constexpr uint32_t cw = CPLX ? 16u : 8u;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int NQ = 8;  // publish queue entries
+  __shared__ uint64_t full_bar[NPM], empty_bar[NPM], done_bar[NQ], pq_free[NQ];
+  __shared__ int32_t d_t[NPM], d_p[NPM], pq_t[NQ], pq_p[NQ];
+  __shared__ uint32_t d_done[NPM];
+  __shared__ uint32_t trace_ctr;
+  __shared__ PowTab s_pow[LMPK_MAX_POWERS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  build_powtab(s_pow, P, C);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NPM; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+      d_done[i] = 0;
+    }
+    for (int i = 0; i < NQ; ++i) {
+      mbar_init(&done_bar[i], 1);
+      mbar_init(&pq_free[i], 1);
+    }
+    trace_ctr = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int NP = L.np;
+  const uint32_t cap = uint32_t(P.smem_cap);
+  const uint32_t ring = smem_u32(smem_raw);
+  if (warp == NC + 1) {
+    // ------------------------------------------------ publisher
+    // The last consumer warp of a piece frees its slot itself and queues
+    // (tile, power) here; the publisher makes every piece queued so far
+    // visible with ONE gpu-scope fence (~1-2 us on a busy SM: per piece it
+    // would cap the walk at one piece per fence) and relaxed flag stores.
+    if (lane == 0) {
+      uint32_t kk = 0;
+      for (bool stop = false; !stop;) {
+        mbar_wait_sleep(&done_bar[kk & (NQ - 1)], (kk / NQ) & 1u);
+        const uint32_t k0 = kk++;
+        while (kk - k0 < uint32_t(L.pub_batch) && mbar_try_wait(&done_bar[kk & (NQ - 1)], (kk / NQ) & 1u)) ++kk;
+        fence_acq_rel_gpu();
+        for (uint32_t q = k0; q < kk; ++q) {
+          const int32_t t = pq_t[q & (NQ - 1)], p = pq_p[q & (NQ - 1)];
+          mbar_arrive(&pq_free[q & (NQ - 1)]);
+          if (t < 0) {
+            stop = true;
+            break;
+          }
+          st_relaxed_u32(P.progress + t, P.epoch_base + uint32_t(p));
+        }
+      }
+    }
+  } else if (warp == NC) {
+    // ------------------------------------------------ producer
+    const int pm = (P.flags >> 8) & 3;
+    const uint64_t pol = pm == 1 ? policy_evict_normal() : (pm == 3 ? policy_evict_last() : policy_evict_first());
+    const uint64_t xpol = policy_evict_normal();
+    unsigned long long rounds = 0;
+    int slot = 0;
+    uint32_t ph = 0;
+    bool wrapped = false, abort = false;
+    if (L.wl) {
+      // ---- static work list: 32 piece records per coalesced load; the runs
+      // of the next piece are fetched while this one waits for its slot
+      const int32_t w0 = __ldg(L.wl_ptr + blockIdx.x), w1 = __ldg(L.wl_ptr + blockIdx.x + 1);
+      for (int32_t base = w0; base < w1 && !abort; base += 32) {
+        int4 ra = make_int4(0, 0, 0, 0), rb = ra;
+        if (base + lane < w1) {
+          ra = __ldg(L.wl + 2 * int64_t(base + lane));
+          rb = __ldg(L.wl + 2 * int64_t(base + lane) + 1);
+        }
+        const int32_t cnt = min(32, w1 - base);
+        int4 rn = make_int4(0, 0, 0, 0);
+        {
+          const int32_t mf = __shfl_sync(0xffffffffu, ra.x, 0), nf = __shfl_sync(0xffffffffu, rb.w, 0) & 255;
+          if (lane < nf) rn = __ldg(L.runs + int64_t(mf) * kLeanMaxRuns + lane);
+        }
+        for (int32_t j = 0; j < cnt; ++j) {
+          const int32_t m = __shfl_sync(0xffffffffu, ra.x, j), pf = __shfl_sync(0xffffffffu, ra.y, j);
+          const int32_t dlo = __shfl_sync(0xffffffffu, ra.z, j), dhi = __shfl_sync(0xffffffffu, ra.w, j);
+          const uint32_t olo = uint32_t(__shfl_sync(0xffffffffu, rb.x, j)), ohi = uint32_t(__shfl_sync(0xffffffffu, rb.y, j));
+          const int32_t bytes = __shfl_sync(0xffffffffu, rb.z, j), xw = __shfl_sync(0xffffffffu, rb.w, j);
+          const int4 rc = rn;  // this piece's runs; fetch the next piece's
+          if (j + 1 < cnt) {
+            const int32_t mn = __shfl_sync(0xffffffffu, ra.x, j + 1), nn = __shfl_sync(0xffffffffu, rb.w, j + 1) & 255;
+            if (lane < nn) rn = __ldg(L.runs + int64_t(mn) * kLeanMaxRuns + lane);
+          }
+          const int32_t p = pf & 255;
+          if (p > P.n_powers) continue;
+          if (pf & 256) {
+            if (lane == 0) trace_ev(P, &trace_ctr, 1, 0, uint32_t(m) << 8 | uint32_t(p));
+            if (p > 1 && !spin_deps_acq(P, dlo, dhi, P.epoch_base + uint32_t(p - 1), &rounds)) {
+              abort = true;
+              break;
+            }
+            // the bulk copies below read y_{p-1} through the async proxy
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (lane == 0) trace_ev(P, &trace_ctr, 4, 0, uint32_t(m) << 8 | uint32_t(p));
+          }
+          if (wrapped && !mbar_wait_bounded(&empty_bar[slot], ph ^ 1u, P)) {
+            abort = true;
+            break;
+          }
+          if (lane == 0) {
+            d_t[slot] = m;
+            d_p[slot] = p;
+            trace_ev(P, &trace_ctr, 2, uint32_t(slot), uint32_t(m) << 8 | uint32_t(p));
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full_bar[slot], uint32_t(bytes) + uint32_t(xw >> 8) * cw);
+            bulk_g2s_a(ring + uint32_t(slot) * cap, L.blocks + (int64_t(ohi) << 32 | int64_t(olo)), uint32_t(bytes),
+                       &full_bar[slot], p == P.n_powers ? policy_evict_first() : pol);
+          }
+          __syncwarp();
+          if (lane < (xw & 255))
+            bulk_g2s_a(ring + uint32_t(slot) * cap + uint32_t(L.xoff) + uint32_t(rc.z) * cw,
+                       s_pow[p - 1].yin + int64_t(rc.x) * int64_t(cw), uint32_t(rc.y) * cw, &full_bar[slot], xpol);
+          __syncwarp();
+          if (++slot == NP) slot = 0, ph ^= 1u, wrapped = true;
+        }
+      }
+      // keep the ticket counter where the queue walk would leave it (the host
+      // advances queue_base by n_items + grid per launch)
+      if (lane == 0) {
+        const int32_t mine = (P.n_items > int32_t(blockIdx.x)) ? (P.n_items - 1 - int32_t(blockIdx.x)) / int32_t(gridDim.x) + 1 : 0;
+        atomicAdd(P.queue, static_cast<unsigned long long>(mine + 1));
+      }
+    } else
+    for (;;) {
+      int32_t i = 0;
+      if (lane == 0) i = int32_t(atomicAdd(P.queue, 1ull) - P.queue_base);
+      i = __shfl_sync(0xffffffffu, i, 0);
+      if (i >= P.n_items || i < 0) break;
+      const int32_t code = __ldg(P.items + i);
+      const int32_t T = code >> 8, p = (code & 255) + 1;
+      if (p > P.n_powers) continue;
+      const int32_t m0 = __ldg(P.st_first + T), m1 = __ldg(P.st_first + T + 1);
+      if (lane == 0) trace_ev(P, &trace_ctr, 1, 0, uint32_t(T) << 8 | uint32_t(p));
+      if (p > 1 && !spin_deps_acq(P, __ldg(P.st_lo + T), __ldg(P.st_hi + T), P.epoch_base + uint32_t(p - 1), &rounds)) {
+        abort = true;
+        break;
+      }
+      // the bulk copies below read y_{p-1} through the async proxy
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (lane == 0) trace_ev(P, &trace_ctr, 4, 0, uint32_t(T) << 8 | uint32_t(p));
+      const char* yin = s_pow[p - 1].yin;
+      for (int32_t m = m0; m < m1; ++m) {
+        if (wrapped && !mbar_wait_bounded(&empty_bar[slot], ph ^ 1u, P)) {
+          abort = true;
+          break;
+        }
+        const int2 xi = __ldg(L.xinfo + m);
+        if (lane == 0) {
+          const int64_t ofs = __ldg(L.ofs + m), bytes = __ldg(L.ofs + m + 1) - ofs;
+          d_t[slot] = m;
+          d_p[slot] = p;
+          trace_ev(P, &trace_ctr, 2, uint32_t(slot), uint32_t(m) << 8 | uint32_t(p));
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full_bar[slot], uint32_t(bytes) + uint32_t(xi.y) * cw);
+          bulk_g2s_a(ring + uint32_t(slot) * cap, L.blocks + ofs, uint32_t(bytes), &full_bar[slot],
+                     p == P.n_powers ? policy_evict_first() : pol);
+        }
+        __syncwarp();
+        if (lane < xi.x) {
+          const int4 rn = __ldg(L.runs + int64_t(m) * kLeanMaxRuns + lane);
+          bulk_g2s_a(ring + uint32_t(slot) * cap + uint32_t(L.xoff) + uint32_t(rn.z) * cw,
+                     yin + int64_t(rn.x) * int64_t(cw), uint32_t(rn.y) * cw, &full_bar[slot], xpol);
+        }
+        __syncwarp();
+        if (++slot == NP) slot = 0, ph ^= 1u, wrapped = true;
+      }
+      if (abort) break;
+    }
+    if (lane == 0) {
+      bool ok = true;
+      if (wrapped) {
+        unsigned long long t0 = globaltimer();
+        while (!mbar_try_wait(&empty_bar[slot], ph ^ 1u)) {
+          if (globaltimer() - t0 > kWatchdogNs || *(volatile unsigned long long*)(P.queue + 1) != 0ull) {
+            ok = false;
+            break;
+          }
+        }
+      }
+      if (ok) {
+        d_t[slot] = -1;
+        mbar_arrive(&full_bar[slot]);
+      }
+    }
+    if (P.prof && lane == 0) atomicAdd(P.prof + 3, rounds);
+  } else {
+    // ------------------------------------------------ consumers
+    const bool use_acc = P.use_acc != 0;
+    int slot = 0;
+    uint32_t ph = 0, kk = 0;
+    int32_t rot = warp;
+    for (;;) {
+      const uint32_t blk = lean_wait(&full_bar[slot], ph, ring + uint32_t(slot) * cap);
+      const int32_t t = d_t[slot];
+      if (t < 0) {
+        if (warp == 0 && lane == 0) {
+          const uint32_t q = kk & (NQ - 1);
+          if (kk >= uint32_t(NQ)) mbar_wait(&pq_free[q], (kk / NQ - 1) & 1u);
+          pq_t[q] = -1;
+          mbar_arrive(&done_bar[q]);
+        }
+        break;
+      }
+      const int32_t p = d_p[slot];
+      const uint4 hdr = lds_v4(blk);  // {units, rows, format, first row}
+      const int32_t nu = int32_t(hdr.x), nrows = int32_t(hdr.y), r0 = int32_t(hdr.w);
+      const uint32_t xb = blk + uint32_t(L.xoff);
+      const PowTab& pt = s_pow[p - 1];
+      if (lane == 0) trace_ev(P, &trace_ctr, 10, uint32_t(slot), uint32_t(t) << 8 | uint32_t(p));
+      // static striding, rotated piece by piece; XP tilings: a piece is an XP
+      // block (header word 2 == 2) or a lean block
+#define LMPK_XLEAN_LOOP(UNIT)                                        \
+  for (int32_t u = rot; u < nu; u += NC) {                           \
+    const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);    \
+    switch (rec.z & 15u) {                                           \
+      case 0: UNIT(0) break;                                         \
+      case 1: UNIT(1) break;                                         \
+      case 2: UNIT(2) break;                                         \
+      case 3: UNIT(3) break;                                         \
+      case 4: UNIT(4) break;                                         \
+      case 5: UNIT(5) break;                                         \
+      case 6: UNIT(6) break;                                         \
+      case 7: UNIT(7) break;                                         \
+      case 8: UNIT(8) break;                                         \
+      default: break;                                                \
+    }                                                                \
+  }
+#define LMPK_UNIT_XP(Wv) xp_unit<Wv, CPLX, EXACT, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen, xb);
+#define LMPK_UNIT_LEAN(Wv) \
+  lean_unit<Wv, CPLX, EXACT, VD, GEN, true>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen, xb);
+      if (XP && hdr.z == 2u) {
+        // XP blocks: the units are binned per consumer warp at build time
+        // (longest-first onto the lightest bin); bin starts at blk + 16
+        const uint32_t b2 = lds_u32(blk + 16u + 2u * uint32_t(rot & ~1));
+        const int32_t ub = (rot & 1) ? int32_t(b2 >> 16) : int32_t(b2 & 0xffffu);
+        const uint32_t e2 = lds_u32(blk + 16u + 2u * uint32_t((rot + 1) & ~1));
+        const int32_t ue = ((rot + 1) & 1) ? int32_t(e2 >> 16) : int32_t(e2 & 0xffffu);
+        for (int32_t u = ub; u < ue; ++u) {
+          const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);
+          switch (rec.z & 15u) {
+            case 0: LMPK_UNIT_XP(0) break;
+            case 1: LMPK_UNIT_XP(1) break;
+            case 2: LMPK_UNIT_XP(2) break;
+            case 3: LMPK_UNIT_XP(3) break;
+            case 4: LMPK_UNIT_XP(4) break;
+            case 5: LMPK_UNIT_XP(5) break;
+            case 6: LMPK_UNIT_XP(6) break;
+            case 7: LMPK_UNIT_XP(7) break;
+            case 8: LMPK_UNIT_XP(8) break;
+            default: break;
+          }
+        }
+      } else {
+        LMPK_XLEAN_LOOP(LMPK_UNIT_LEAN)
+      }
+#undef LMPK_UNIT_XP
+#undef LMPK_UNIT_LEAN
+#undef LMPK_XLEAN_LOOP
+      if (++rot == NC) rot = 0;
+      __syncwarp();
+      if (lane == 0) trace_ev(P, &trace_ctr, 11, uint32_t(slot), uint32_t(t) << 8 | uint32_t(p));
+      uint32_t old = 0;
+      if (lane == 0) old = atom_add_acqrel_cta_smem(&d_done[slot], 1u);
+      if (__shfl_sync(0xffffffffu, old, 0) == uint32_t(NC - 1) && lane == 0) {
+        // last warp of the piece: queue it for the publisher, free the slot
+        trace_ev(P, &trace_ctr, 12, uint32_t(slot), uint32_t(t) << 8 | uint32_t(p));
+        d_done[slot] = 0;
+        const uint32_t q = kk & (NQ - 1);
+        if (kk >= uint32_t(NQ)) mbar_wait(&pq_free[q], (kk / NQ - 1) & 1u);
+        pq_t[q] = t;
+        pq_p[q] = p;
+        mbar_arrive(&done_bar[q]);
+        mbar_arrive(&empty_bar[slot]);
+      }
+      ++kk;
+      if (++slot == NP) slot = 0, ph ^= 1u;
     }
   }
 }

@@ -124,6 +124,19 @@ struct lmpk_tiling {
   int32_t lean_vd = -1;            // -1 none, 0 raw values, 1 dictionary
   int64_t lean_bytes = 0;
   int32_t lean_piece = 0;          // bytes of the largest lean block (the lean ring's piece)
+  // lean x staging (mpk_xlean_kernel): a piece is [lean block | x buffer]
+  int32_t lean_xs = 0;             // 1: column fields are x-buffer entries, gathers come from shared memory
+  int32_t lean_xp = 0;             // 1: XP blocks (row records, units of up to 4 slices; lean_kernel.cuh)
+  int32_t lean_xoff = 0;           // byte offset of the x buffer in a piece (= largest lean block)
+  int32_t lean_np = 0;             // ring depth of the staged kernel
+  int32_t lean_cplx = 0;           // vectors the x buffer was sized for (16-byte entries)
+  int4* d_lean_runs = nullptr;     // [n_tiles * 32] {first entry, entries, buffer entry, 0}
+  int2* d_lean_xinfo = nullptr;    // [n_tiles] {runs, staged entries}
+  int4* d_lean_wl = nullptr;       // staged kernel: per-CTA work lists (2 x int4 per piece, mpk_lean.cu)
+  int32_t* d_lean_wl_ptr = nullptr;  // [grid + 1] first piece record of each CTA's list
+  int32_t lean_wl_grid = 0;        // grid the work lists were cut for
+  std::vector<int64_t> h_lean_ofs;
+  std::vector<int2> h_lean_xinfo;
   uint32_t wrap_gen = 0;           // ctx wrap generation its progress words belong to
 };
 

@@ -281,7 +281,15 @@ int64_t lean_tile_bytes(const std::vector<int32_t>& width, int32_t s0, int32_t s
 int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr, const int32_t* col,
                const double* val, const std::vector<int32_t>& first, const std::vector<int32_t>& width,
                const int32_t* d_wmin, const std::vector<int32_t>& tmode, const std::vector<int32_t>& tdict,
-               const uint64_t* d_dict_tab, const int32_t* d_width, int64_t cap, cudaStream_t st);
+               const uint64_t* d_dict_tab, const int32_t* d_width, int64_t cap, bool want_xs, bool cplx,
+               cudaStream_t st);
+int lean_xplan(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col, const int32_t* d_tile_row,
+               int32_t nt, bool cplx, int4** d_runs, int2** d_xinfo, int32_t* max_entries, cudaStream_t st);
+int64_t lean_xs_budget(const lmpk_ctx* ctx);
+bool lean_xs_wanted();
+bool lean_xs_runnable(const lmpk_tiling* T, const double* y, int64_t ldy, bool cplx);
+int lean_worklist(lmpk_tiling* T, const std::vector<int32_t>& items, const std::vector<int32_t>& st_first,
+                  const std::vector<int32_t>& lo, const std::vector<int32_t>& hi, int grid, cudaStream_t st);
 void lean_free(lmpk_tiling* T);
 int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool gen,
                 int grid, cudaStream_t st);
@@ -573,7 +581,7 @@ struct XCounter {
 template <class Cost>
 static void partition_range(const std::vector<int32_t>& width, int32_t s0, int32_t s1, int64_t cap, int64_t e_cap,
                             Cost cost, std::vector<int32_t>& first, std::vector<int64_t>& Es,
-                            XCounter* xc = nullptr) {
+                            XCounter* xc = nullptr, int32_t ns_cap = INT32_MAX) {
   int32_t s = s0;
   while (s < s1) {
     int32_t ns = 0;
@@ -583,7 +591,7 @@ static void partition_range(const std::vector<int32_t>& width, int32_t s0, int32
       const int64_t e2 = E + int64_t(width[s + ns]) * 32;
       const size_t u = xc ? xc->add(s + ns) : 0;
       const int64_t need = cost(s, ns + 1, e2) + (xc ? xc->bytes() : 0);
-      if (ns > 0 && (need > cap || e2 > e_cap)) {
+      if (ns > 0 && (need > cap || e2 > e_cap || ns >= ns_cap)) {
         if (xc) xc->undo(u);
         break;
       }
@@ -606,7 +614,10 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
                         const int32_t* col, const double* val, const std::vector<int32_t>& width,
                         const int32_t* d_wmin, int64_t cap, const std::vector<int32_t>* h_rp,
                         const std::vector<int32_t>* h_col, bool xstage, const std::vector<uint8_t>* fit16,
-                        int64_t e_cap, cudaStream_t st) {
+                        int64_t e_cap, cudaStream_t st, int32_t xs_slices = 0, bool cplx = false) {
+  // xs_slices > 0: the lean walk stages x (lean_build): tiles hold at most
+  // that many slices, so a tile's block and x buffer share one ring piece
+  const int32_t ns_cap = xs_slices > 0 ? xs_slices : INT32_MAX;
   const int32_t S = static_cast<int32_t>(width.size());
   std::vector<int32_t> first;
   std::vector<int64_t> Es;
@@ -651,9 +662,9 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
       while (e < S && (*fit16)[e] == (*fit16)[s]) ++e;
       const size_t before = f1.size();
       if ((*fit16)[s])
-        partition_range(width, s, e, cap, e_cap, dict_cost, f1, E1, xc);
+        partition_range(width, s, e, cap, e_cap, dict_cost, f1, E1, xc, ns_cap);
       else
-        partition_range(width, s, e, cap, INT64_MAX, plain_cost, f1, E1, xc);
+        partition_range(width, s, e, cap, INT64_MAX, plain_cost, f1, E1, xc, ns_cap);
       c1.resize(f1.size(), (*fit16)[s]);
       (void)before;
       s = e;
@@ -703,7 +714,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
         tdict.push_back(li);
       } else {
         const size_t b = first.size();
-        partition_range(width, s0, s1, cap, e_cap, raw_cost, first, Es, xc);
+        partition_range(width, s0, s1, cap, e_cap, raw_cost, first, Es, xc, ns_cap);
         for (size_t i = b; i < first.size(); ++i) {
           const int32_t a0 = first[i], a1 = i + 1 < first.size() ? first[i + 1] : s1;
           // a single slice too large for a slot stays plain (read from global)
@@ -840,10 +851,10 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
                                                              T->d_dep_hi);
   launch_count_add(ctx, 1);
   LMPK_CHECK_CUDA(cudaGetLastError());
-  if (n_comp == nt && !xc) {
+  if ((n_comp == nt || (xs_slices > 0 && n_comp > 0)) && !xc) {
     std::vector<int32_t> tfirst(first.begin(), first.begin() + nt);
     LMPK_TRY(lean_build(ctx, T, n, row_ptr, col, val, tfirst, width, d_wmin, tmode, tdict, d_dict_tab, d_width, cap,
-                        st));
+                        xs_slices > 0, cplx, st));
   }
   T->h_dep_lo.resize(nt);
   T->h_dep_hi.resize(nt);
@@ -938,6 +949,7 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_st_lo, lo.data(), ns * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_st_hi, hi.data(), ns * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  LMPK_TRY(lean_worklist(T, items, first, lo, hi, T->info.grid, st));
   (void)ctx;
   if (info) *info = T->info;
   *out = T;
@@ -1064,6 +1076,55 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   // the SM's unified L1/shared memory to the gathers)
   int64_t slot_cap = INT64_MAX;
   if (const char* e = getenv("LMPK_SLOT_KB")) slot_cap = std::max(4, atoi(e)) * int64_t(1024);
+  // Lean x staging (ring tilings of matrices with rows <= 8 entries, the
+  // default): tiles are capped at R rows so that a tile's lean block and the
+  // runs of y_{p-1} its rows gather share one ring piece (lean_build).  R is
+  // the largest candidate whose x buffers (k_lean_xplan on a fixed-R grid)
+  // leave room for the blocks at ring depth 2; the block estimate takes the
+  // dictionary format when the first rows hold <= kDictMax distinct values.
+  int32_t xs_slices = 0;
+  int64_t xs_bcap = 0;
+  const bool cplx_t = (prm.mode_flags & LMPK_FLAG_COMPLEX) != 0;
+  if (ring && compress && !xstage && max_row >= 1 && max_row <= 8 && n > 0 && lean_xs_wanted()) {
+    bool dictish = false;
+    {
+      const int32_t ns = std::min<int32_t>(h_nnz, 32768);
+      std::vector<double> hv(ns);
+      if (ns > 0) LMPK_CHECK_CUDA(cudaMemcpyAsync(hv.data(), val, size_t(ns) * 8, cudaMemcpyDeviceToHost, st));
+      LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+      std::vector<uint64_t> bits(ns);
+      if (ns > 0) memcpy(bits.data(), hv.data(), size_t(ns) * 8);
+      std::sort(bits.begin(), bits.end());
+      dictish = std::unique(bits.begin(), bits.end()) - bits.begin() <= kDictMax;
+    }
+    std::vector<int32_t> rows_c{1664, 832, 416};
+    if (const char* e = getenv("LMPK_XLEAN_ROWS")) rows_c = {std::max(32, atoi(e) & ~31)};
+    const int64_t slice_b = 16 + lean_col_bytes(max_row) + (dictish ? lean_code_bytes(max_row) : lean_raw_bytes(max_row));
+    for (int32_t R : rows_c) {
+      const int32_t ntf = (n + R - 1) / R;
+      std::vector<int32_t> trow(ntf + 1);
+      for (int32_t t = 0; t <= ntf; ++t) trow[t] = std::min<int64_t>(int64_t(t) * R, n);
+      int32_t* d_trow = nullptr;
+      LMPK_TRY(dmalloc(&d_trow, ntf + 1));
+      LMPK_CHECK_CUDA(cudaMemcpyAsync(d_trow, trow.data(), size_t(ntf + 1) * 4, cudaMemcpyHostToDevice, st));
+      int4* d_runs = nullptr;
+      int2* d_xinfo = nullptr;
+      int32_t mx = -1;
+      const int rc = lean_xplan(ctx, n, row_ptr, col, d_trow, ntf, cplx_t, &d_runs, &d_xinfo, &mx, st);
+      cudaFree(d_trow);
+      cudaFree(d_runs);
+      cudaFree(d_xinfo);
+      if (rc != LMPK_OK) return rc;
+      if (mx < 0) continue;
+      // 12% headroom: the real tiles are cut by bytes too and need not sit on the R grid
+      const int64_t xb = ((int64_t(mx) * (cplx_t ? 16 : 8) * 112 / 100) + 127) & ~int64_t(127);
+      const int64_t bcap = (lean_xs_budget(ctx) / 2 - xb) & ~int64_t(127);
+      if (bcap < kLeanRec + int64_t(R / 32) * slice_b + 256) continue;
+      xs_slices = R / 32;
+      xs_bcap = bcap;
+      break;
+    }
+  }
   for (const Cand& cd : cands) {
     const int64_t slot = std::min<int64_t>(unstaged ? per_cta / 2 : per_cta / cd.slots, slot_cap) & ~int64_t(127);
     int64_t cap = slot;  // with x staging the slot holds [block | x buffer] (build_tiling)
@@ -1071,6 +1132,7 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     if (prm.tile_nnz_hint > 0 && !compress && !ring)
       cap = std::min<int64_t>(cap, int64_t(prm.tile_nnz_hint) * 12 + 2048);
     const int64_t e_cap = (compress && !ring && prm.tile_nnz_hint > 0) ? int64_t(prm.tile_nnz_hint) : INT64_MAX;
+    if (xs_slices > 0) cap = std::min(cap, xs_bcap);
     cap &= ~int64_t(127);
     if (cap < 2048) continue;
     const int64_t xoff = 0;
@@ -1085,7 +1147,8 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     cand->ctx = ctx;
     cand->n = n;
     const int rc = build_tiling(ctx, cand, n, row_ptr, col, val, width, d_wmin, cap, xstage ? &h_rp : nullptr,
-                                xstage ? &h_col : nullptr, xstage, compress ? &fit16 : nullptr, e_cap, st);
+                                xstage ? &h_col : nullptr, xstage, compress ? &fit16 : nullptr, e_cap, st,
+                                xs_slices, cplx_t);
     if (rc != LMPK_OK) {
       lmpk_tiling_destroy(cand);
       return rc;
@@ -1457,7 +1520,8 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
       else if (T->info.compressed_tiles == T->info.n_tiles && T->info.dict_tiles == 0)
         uniform = 2;
     }
-    if (T->d_lean && T->staged_tiles == 0 && T->slots == 2 && !getenv("LMPK_NO_LEAN_RUN")) {
+    if (T->d_lean && T->staged_tiles == 0 && T->slots == 2 && !getenv("LMPK_NO_LEAN_RUN") &&
+        lean_xs_runnable(T, y, ldy, cplx)) {
       bool plain = !use_acc;
       for (int i = 0; i < P; ++i) plain = plain && C.kernel[i] == LMPK_KERNEL_SPMV;
       return launch_lean(ctx, T, Pm, C, cplx, exact, !plain, grid, st);

@@ -3,10 +3,11 @@
 #include "lean_kernel.cuh"
 
 namespace lmpk {
-const void* mpk_lean_fn_c_e(bool vd, int np) {
-#define LMPK_LEAN_FN(V) (np == 4 ? reinterpret_cast<const void*>(mpk_lean_kernel<true, true, V, true, 4>) \
-                                 : reinterpret_cast<const void*>(mpk_lean_kernel<true, true, V, true, 2>))
-  return vd ? LMPK_LEAN_FN(true) : LMPK_LEAN_FN(false);
+const void* mpk_lean_fn_c_e(bool vd, int np, bool xp) {
+#define LMPK_LEAN_FN(V, X) (np == 4 ? reinterpret_cast<const void*>(mpk_lean_kernel<true, true, V, true, 4, X>) \
+                                    : reinterpret_cast<const void*>(mpk_lean_kernel<true, true, V, true, 2, X>))
+  if (vd && xp) return LMPK_LEAN_FN(true, true);
+  return vd ? LMPK_LEAN_FN(true, false) : LMPK_LEAN_FN(false, false);
 #undef LMPK_LEAN_FN
 }
 }  // namespace lmpk

@@ -1,0 +1,11 @@
+// mpk_xlean_cf.cu -- instantiations of the staged lean walk (complex128 vectors, fused row sums).
+#include "lean_kernel.cuh"
+
+namespace lmpk {
+const void* mpk_xlean_fn_c_f(bool vd, bool xp) {
+#define LMPK_XLEAN_FN(V, X) reinterpret_cast<const void*>(mpk_xlean_kernel<true, false, V, true, X>)
+  if (vd && xp) return LMPK_XLEAN_FN(true, true);
+  return vd ? LMPK_XLEAN_FN(true, false) : LMPK_XLEAN_FN(false, false);
+#undef LMPK_XLEAN_FN
+}
+}  // namespace lmpk
