@@ -32,25 +32,26 @@
 
 namespace lmpk {
 
-constexpr int kBfsThreads = 256;
+constexpr int kBfsThreads = 512;
 
+// Grid barrier of the cooperative BFS kernel: one arrival counter that only
+// grows (zeroed before the launch); barrier number e completes when it reaches
+// e * nblocks.  One atomic per CTA and a spin on the same word -- no reset, no
+// generation word, no sleep: ~598 of these are cfg2's whole level loop.
 struct GridBar {
   unsigned int count;
-  unsigned int gen;
+  unsigned int pad;
 };
 
-__device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned int nblocks) {
+__device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned int nblocks, unsigned int& epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = &gb->gen;
-    const unsigned int g = *vgen;
+    ++epoch;
     __threadfence();
-    if (atomicAdd(&gb->count, 1u) == nblocks - 1) {
-      gb->count = 0;
-      __threadfence();
-      atomicAdd(&gb->gen, 1u);
-    } else {
-      while (*vgen == g) __nanosleep(32);
+    atomicAdd(&gb->count, 1u);
+    const unsigned int target = epoch * nblocks;
+    volatile unsigned int* vc = &gb->count;
+    while (*vc < target) {
     }
     __threadfence();
   }
@@ -198,28 +199,29 @@ __device__ void bfs_expand(const RP* row_ptr, const int32_t* col, const BfsState
   }
 }
 
+// Level loop: ONE grid barrier per level.  The frontier sizes rotate through
+// three counters (sizes[4 + lev % 3]): level lev reads its own, pushes into the
+// next one and resets the third, which nobody touches until the level after
+// next.  sizes[0] is the seeded frontier, sizes[2] the last level reached.
 template <typename RP>
 __global__ void __launch_bounds__(kBfsThreads) k_bfs(const RP* row_ptr, const int32_t* col, BfsState S) {
   int32_t lev = 0;
   int32_t* qin = S.qa;
   int32_t* qout = S.qb;
-  int cur = 0;
+  uint32_t* cnt = S.sizes + 4;
+  unsigned int epoch = 0;
   while (true) {
-    const uint32_t n_in = *((volatile uint32_t*)&S.sizes[cur]);
+    const uint32_t n_in = *((volatile uint32_t*)(lev == 0 ? S.sizes : cnt + lev % 3));
     if (n_in == 0) break;
-    bfs_expand(row_ptr, col, S, qin, n_in, qout, &S.sizes[cur ^ 1], lev);
-    grid_barrier(S.bar, gridDim.x);
-    // reset the consumed queue size for the next round (one thread), then
-    // a second barrier so nobody reads the stale size
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      S.sizes[cur] = 0;
-      if (*((volatile uint32_t*)&S.sizes[cur ^ 1]) > 0) S.sizes[2] = uint32_t(lev + 1);
+      if (lev > 0) S.sizes[2] = uint32_t(lev);
+      cnt[(lev + 2) % 3] = 0;
     }
-    grid_barrier(S.bar, gridDim.x);
+    bfs_expand(row_ptr, col, S, qin, n_in, qout, cnt + (lev + 1) % 3, lev);
+    grid_barrier(S.bar, gridDim.x, epoch);
     int32_t* t = qin;
     qin = qout;
     qout = t;
-    cur ^= 1;
     ++lev;
   }
 }
@@ -323,8 +325,11 @@ template <typename RP>
 static int launch_bfs(lmpk_ctx* ctx, const RP* row_ptr, const int32_t* col, BfsState S, cudaStream_t st) {
   int occ = 0;
   LMPK_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bfs<RP>, kBfsThreads, 0));
-  occ = std::max(1, std::min(occ, 4));
+  occ = std::max(1, std::min(occ, 2));
   const int grid = occ * ctx->sm_count;
+  // rotating frontier counters and the barrier's arrival counter start at zero
+  LMPK_CHECK_CUDA(cudaMemsetAsync(S.sizes + 4, 0, 16, st));
+  LMPK_CHECK_CUDA(cudaMemsetAsync(S.bar, 0, sizeof(GridBar), st));
   void* args[] = {(void*)&row_ptr, (void*)&col, (void*)&S};
   LMPK_CHECK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_bfs<RP>), dim3(grid),
                                               dim3(kBfsThreads), args, 0, st));

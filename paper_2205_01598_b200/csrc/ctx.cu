@@ -137,7 +137,7 @@ extern "C" int lmpk_ctx_destroy(lmpk_ctx* c) {
   if (!c) return LMPK_OK;
   cudaDeviceSynchronize();
   Scratch* pools[] = {&c->s_small, &c->s_a, &c->s_b, &c->s_c,
-                      &c->s_d,     &c->s_e, &c->s_f, &c->s_g, &c->s_heavy};
+                      &c->s_d,     &c->s_e, &c->s_f, &c->s_g, &c->s_heavy, &c->s_prod};
   for (Scratch* s : pools) s->release();
   if (c->queue_ctr) cudaFree(c->queue_ctr);
   if (c->heavy_ev) cudaEventDestroy(c->heavy_ev);

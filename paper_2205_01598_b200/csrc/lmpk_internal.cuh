@@ -74,7 +74,8 @@ struct lmpk_ctx {
   uint32_t wrap_gen = 0;   // bumped when the epoch counter wraps
   // scratch pools
   lmpk::Scratch s_small, s_a, s_b, s_c, s_d, s_e, s_f, s_g;
-  lmpk::Scratch s_heavy;  // CRS kernel: list of heavy rows (count + indices)
+  lmpk::Scratch s_heavy;  // CRS kernel: list of heavy rows (count, entries, (row, product offset) pairs)
+  lmpk::Scratch s_prod;   // CRS kernel: products of the heavy rows' entries (compact)
   cudaEvent_t heavy_ev = nullptr;  // recorded after the last kernel reading s_heavy
   uint64_t* queue_ctr = nullptr;  // monotone work-queue counter (device)
   uint64_t queue_base = 0;        // host mirror of the counter value

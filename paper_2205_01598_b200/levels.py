@@ -65,6 +65,4 @@ def bfs_levels(a: CsrMatrix, root: int = 0):
     before level i (levels.py:106-114).
     """
     levels, perm, inv = bfs_levels_device(a, root)
-    p = Permutation._trusted(perm.cpu().numpy(), inv.cpu().numpy())
-    object.__setattr__(p, "_dev", (perm, inv))
-    return levels, p
+    return levels, Permutation._from_device(perm, inv)

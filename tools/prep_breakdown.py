@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2205_01598_b200 as lm
 from paper_2205_01598_b200 import kernels as K
 import cProfile, pstats
-a = lm.gen_stencil_3d(int(os.environ.get("N", "200")), 2)
+a = lm.gen_stencil_3d(int(os.environ.get("N", "200")), 2, device=bool(int(os.environ.get("DEV", "1"))))
 lm.warmup(); torch.cuda.synchronize()
 def run():
     t0 = time.perf_counter(); pre = lm.prepare(a, "lb_lg_p2p", 8, 126e6); torch.cuda.synchronize(); t1 = time.perf_counter()
