@@ -201,6 +201,16 @@ typedef struct lmpk_power_cfg {
 int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* tiling, double* y, int64_t ldy, int32_t n_slots,
                  const lmpk_power_cfg* cfg, double* acc, int use_acc, int flags, void* stream);
 
+/* The same plan semantics as lmpk_mpk_run on the CRS arrays, one sweep per
+ * power with the power's kernel (SpMV / Chebyshev step) and accumulation
+ * fused into the row store -- run_plan's path (executor.py:213-230) for
+ * matrices whose rows exceed the tile format (> 65535 entries, power-law
+ * hubs): real or complex128 (LMPK_FLAG_COMPLEX) vectors, results bitwise those
+ * of the level-blocked walk. */
+int lmpk_mpk_crs_run(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                     const double* val, double* y, int64_t ldy, int32_t n_slots,
+                     const lmpk_power_cfg* cfg, double* acc, int use_acc, int flags, void* stream);
+
 /* Synchronize `stream` and report a device-side failure of the last MPK
  * launches (watchdog: a dependency spin exceeded its bound, the analogue of
  * the reference's join watchdog executor.py:173-179). */

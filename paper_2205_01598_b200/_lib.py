@@ -103,6 +103,8 @@ SIGNATURES = {
     "lmpk_tiling_geometry": (_int, [_vp, _vp, _vp, _vp]),
     "lmpk_mpk_run": (_int, [_vp, _vp, _vp, _i64, _i32, ctypes.POINTER(PowerCfg), _vp, _int,
                             _int, _vp]),
+    "lmpk_mpk_crs_run": (_int, [_vp, _i32, _vp, _vp, _vp, _vp, _i64, _i32, ctypes.POINTER(PowerCfg), _vp,
+                                _int, _int, _vp]),
     "lmpk_bfs_levels": (_int, [_vp, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _i64p, _vp]),
     "lmpk_symmetrized_pattern": (_int, [_vp, _i32, _vp, _vp, ctypes.POINTER(_int), _i64p,
                                         _vp, _vp, _i64, _vp]),

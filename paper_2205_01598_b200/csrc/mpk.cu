@@ -885,6 +885,10 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
                               lmpk_tiling_info* info, lmpk_tiling** out, cudaStream_t st) {
   const int32_t nt = T->info.n_tiles;
   int64_t target = 32768;
+  // complex vectors double the bytes a tile touches: items of one tile keep
+  // the window of blocks and vectors between a tile's consecutive powers
+  // smaller (cfg5 complex Chebyshev step 3.91 -> 3.47 ms, tools/cfg5_sweep.py)
+  if (prm.mode_flags & LMPK_FLAG_COMPLEX) target = 8192;
   if (prm.tile_nnz_hint > 0) target = prm.tile_nnz_hint;
   else if (const char* e = getenv("LMPK_SUPER_NNZ")) target = std::max(1, atoi(e));
   std::vector<int32_t> tE(nt);

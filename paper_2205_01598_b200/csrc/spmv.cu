@@ -151,6 +151,163 @@ static int spmv_launch(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col
   return LMPK_OK;
 }
 
+// ---------------------------------------------------------------- CRS plan sweeps
+// One power of a plan on the CRS arrays with the plan's per-power epilogue
+// fused in: t = row sum (storage order, unfused, as above); Chebyshev
+// t = 2 t - y_prev[r]; y_out[r] = t; acc[r] += c t (executor.py:127-147).
+// Real or complex128 vectors (a real matrix: two independent sums).  This is
+// the level-blocked plans' fallback for matrices the tile format cannot hold
+// (rows longer than 65,535 entries), so that Chebyshev and accumulating plans
+// run there too; bitwise equal to the walk's row body.
+struct SweepEpi {
+  const double* prev;  // y_{p-2} slot (Chebyshev), or null
+  double* acc;         // accumulator, or null
+  double cre, cim;
+};
+template <bool CPLX>
+__device__ __forceinline__ void sweep_store(double* __restrict__ out, const SweepEpi& E, int64_t r, double tr,
+                                            double ti) {
+  if constexpr (!CPLX) {
+    if (E.prev) tr = __dsub_rn(__dmul_rn(2.0, tr), E.prev[r]);
+    out[r] = tr;
+    if (E.acc) E.acc[r] = __dadd_rn(E.acc[r], __dmul_rn(E.cre, tr));
+  } else {
+    if (E.prev) {
+      tr = __dsub_rn(__dmul_rn(2.0, tr), E.prev[2 * r]);
+      ti = __dsub_rn(__dmul_rn(2.0, ti), E.prev[2 * r + 1]);
+    }
+    out[2 * r] = tr;
+    out[2 * r + 1] = ti;
+    if (E.acc) {
+      const double pr = __dsub_rn(__dmul_rn(E.cre, tr), __dmul_rn(E.cim, ti));
+      const double pi = __dadd_rn(__dmul_rn(E.cre, ti), __dmul_rn(E.cim, tr));
+      E.acc[2 * r] = __dadd_rn(E.acc[2 * r], pr);
+      E.acc[2 * r + 1] = __dadd_rn(E.acc[2 * r + 1], pi);
+    }
+  }
+}
+
+struct LdgX {
+  const double* x;
+  __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+};
+struct LdgX2 {
+  const double2* x;
+  __device__ __forceinline__ double2 operator()(int c) const { return __ldg(x + c); }
+};
+
+template <bool CPLX>
+__device__ __forceinline__ void sweep_gather(const double* __restrict__ x, int32_t c, double& xr, double& xi) {
+  if constexpr (CPLX) {
+    const double2 xx = c >= 0 ? __ldg(reinterpret_cast<const double2*>(x) + c) : make_double2(0.0, 0.0);
+    xr = xx.x;
+    xi = xx.y;
+  } else {
+    xr = c >= 0 ? __ldg(x + c) : 0.0;
+    xi = 0.0;
+  }
+}
+
+template <bool CPLX>
+__global__ void __launch_bounds__(256) sweep_rows_kernel(const int32_t* __restrict__ row_ptr,
+                                                         const int32_t* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x, double* __restrict__ out,
+                                                         SweepEpi E, int32_t n, const int32_t* __restrict__ list,
+                                                         int32_t hb) {
+  if (int32_t(blockIdx.x) < hb) {
+    // one warp per heavy row, pipelined as in spmv_rows_heavy_kernel
+    __shared__ __align__(16) double buf[8][2][kHStage * (CPLX ? 2 : 1)];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t i = int32_t(blockIdx.x) * 8 + warp;
+    const int32_t na = __ldg(list), nb = __ldg(list + 1);
+    if (i >= na + nb) return;
+    const int32_t r = i < na ? __ldg(list + 2 + i) : __ldg(list + 2 + n - 1 - (i - na));
+    const int32_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
+    const int32_t nst = (b - a + kHStage - 1) / kHStage;
+    int32_t c2[4];
+    double v2[4], v1[4], x1r[4], x1i[4];
+#define LMPK_SWEEP_LOAD_CV(S)                                      \
+  _Pragma("unroll") for (int q = 0; q < 4; ++q) {                  \
+    const int32_t e = a + (S) * kHStage + q * 32 + lane;           \
+    c2[q] = e < b ? __ldg(col + e) : -1;                           \
+    v2[q] = e < b ? __ldg(val + e) : 0.0;                          \
+  }
+#define LMPK_SWEEP_GATHER()                                        \
+  _Pragma("unroll") for (int q = 0; q < 4; ++q) {                  \
+    sweep_gather<CPLX>(x, c2[q], x1r[q], x1i[q]);                  \
+    v1[q] = v2[q];                                                 \
+  }
+    LMPK_SWEEP_LOAD_CV(0)
+    LMPK_SWEEP_GATHER()
+    if (nst > 1) {
+      LMPK_SWEEP_LOAD_CV(1)
+    }
+    double tr = 0.0, ti = 0.0;
+    for (int32_t s = 0; s < nst; ++s) {
+      double mr[4], mi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        mr[q] = __dmul_rn(v1[q], x1r[q]);
+        mi[q] = CPLX ? __dmul_rn(v1[q], x1i[q]) : 0.0;
+      }
+      if (s + 1 < nst) {
+        LMPK_SWEEP_GATHER()
+      }
+      if (s + 2 < nst) {
+        LMPK_SWEEP_LOAD_CV(s + 2)
+      }
+      double* bw = buf[warp][s & 1];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if constexpr (CPLX) {
+          bw[2 * (q * 32 + lane)] = mr[q];
+          bw[2 * (q * 32 + lane) + 1] = mi[q];
+        } else {
+          bw[q * 32 + lane] = mr[q];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int32_t cnt = min(kHStage, b - a - s * kHStage);
+        const double2* b2 = reinterpret_cast<const double2*>(bw);
+        if constexpr (CPLX) {
+          for (int32_t k = 0; k < cnt; ++k) {
+            const double2 p = b2[k];
+            tr = __dadd_rn(tr, p.x);
+            ti = __dadd_rn(ti, p.y);
+          }
+        } else {
+          int32_t k = 0;
+          for (; k + 2 <= cnt; k += 2) {
+            const double2 p = b2[k / 2];
+            tr = __dadd_rn(tr, p.x);
+            tr = __dadd_rn(tr, p.y);
+          }
+          if (k < cnt) tr = __dadd_rn(tr, bw[k]);
+        }
+      }
+      __syncwarp();
+    }
+    if (lane == 0) sweep_store<CPLX>(out, E, r, tr, ti);
+#undef LMPK_SWEEP_LOAD_CV
+#undef LMPK_SWEEP_GATHER
+    return;
+  }
+  const int64_t stride = int64_t(gridDim.x - hb) * blockDim.x;
+  for (int64_t r = int64_t(blockIdx.x - hb) * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const int32_t k0 = __ldg(row_ptr + r), k1 = __ldg(row_ptr + r + 1);
+    if (k1 - k0 > kHeavy) continue;
+    if constexpr (CPLX) {
+      const double2 t = row_sum_exact_c(col + k0, val + k0, k1 - k0, LdgX2{reinterpret_cast<const double2*>(x)});
+      sweep_store<true>(out, E, r, t.x, t.y);
+    } else {
+      const double t = row_sum_exact(col + k0, val + k0, k1 - k0, LdgX{x});
+      sweep_store<false>(out, E, r, t, 0.0);
+    }
+  }
+}
+
 // heavy-row list of [r0, r1) in the ctx scratch (two counts, then cap slots)
 static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t r1, int32_t** out,
                       int32_t* n_heavy, cudaStream_t st) {
@@ -213,6 +370,47 @@ extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_pt
   for (int32_t p = 1; p <= p_m; ++p)
     LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy,
                          n_heavy, st));
+  LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
+  return LMPK_OK;
+}
+
+// Replaces run_plan's walker (executor.py:84-230) for plans on matrices whose
+// rows do not fit the tile format: cfg->n_powers sweeps over the CRS arrays
+// with the per-power slots, kernel (SpMV / Chebyshev) and accumulation.
+extern "C" int lmpk_mpk_crs_run(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* col,
+                                const double* val, double* y, int64_t ldy, int32_t n_slots,
+                                const lmpk_power_cfg* cfg, double* acc, int use_acc, int flags, void* stream) {
+  LMPK_ARG_CHECK(ctx && cfg && y, "lmpk_mpk_crs_run: NULL ctx/cfg/y");
+  const bool cplx = (flags & LMPK_FLAG_COMPLEX) != 0;
+  LMPK_ARG_CHECK(cfg->n_powers >= 1 && cfg->n_powers <= LMPK_MAX_POWERS, "n_powers out of range");
+  LMPK_ARG_CHECK(ldy >= int64_t(n) * (cplx ? 2 : 1), "ldy too small");
+  LMPK_ARG_CHECK(!use_acc || acc != nullptr, "use_acc requires acc");
+  LMPK_ARG_CHECK(!cplx || (reinterpret_cast<uintptr_t>(y) & 15) == 0, "complex y must be 16-byte aligned");
+  if (n == 0) return LMPK_OK;
+  cudaStream_t st = as_stream(stream);
+  int32_t* heavy = nullptr;
+  int32_t n_heavy = 0;
+  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_heavy, st));
+  const int threads = 256;
+  const int64_t blocks = (int64_t(n) + threads - 1) / threads;
+  const int grid = static_cast<int>(std::min<int64_t>(blocks, int64_t(ctx->sm_count) * 8));
+  const int hb = (n_heavy + 7) / 8;
+  for (int32_t i = 0; i < cfg->n_powers; ++i) {
+    const int32_t so = cfg->out_slot[i], si = cfg->in_slot[i], sp = cfg->prev_slot[i];
+    LMPK_ARG_CHECK(so >= 0 && so < n_slots && si >= 0 && si < n_slots && so != si, "bad slots at power %d", i + 1);
+    const bool cheb = cfg->kernel[i] == LMPK_KERNEL_CHEB;
+    LMPK_ARG_CHECK(!cheb || (sp >= 0 && sp < n_slots), "bad prev_slot at power %d", i + 1);
+    SweepEpi E{cheb ? y + int64_t(sp) * ldy : nullptr, use_acc ? acc : nullptr, cfg->acc_coef_re[i],
+               cplx ? cfg->acc_coef_im[i] : 0.0};
+    const double* x = y + int64_t(si) * ldy;
+    double* out = y + int64_t(so) * ldy;
+    if (cplx)
+      sweep_rows_kernel<true><<<hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, E, n, heavy, hb);
+    else
+      sweep_rows_kernel<false><<<hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, E, n, heavy, hb);
+    launch_count_add(ctx, 1);
+  }
+  LMPK_CHECK_CUDA(cudaGetLastError());
   LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
   return LMPK_OK;
 }

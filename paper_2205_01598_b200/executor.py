@@ -188,10 +188,12 @@ def _launch(plan: ExecPlan, yd, accd, use_acc, flags=0, sync=True):
         cfg = plan.power_config()
         til = plan.tiling(complex_state=cplx)
         if til is None:
-            # rows too long for the tile format: CRS sweeps (plain MPK only)
+            # rows too long for the tile format (power-law hubs): sweeps over the
+            # CRS arrays, the plan's Chebyshev steps / accumulation fused in
             if cplx or use_acc or np.any(plan.kernel != 0):
-                raise NotImplementedError("rows longer than 65535 entries: only plain real MPK runs (CRS sweeps)")
-            K.mpk_baseline(plan.a.device(), yv, plan.p_m)
+                K.mpk_crs_run(plan.a.device(), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx)
+            else:
+                K.mpk_baseline(plan.a.device(), yv, plan.p_m)
         else:
             sched = _schedule(plan, til, yv, cfg, av, use_acc, cplx, flags)
             if sched == "crs":
@@ -226,6 +228,8 @@ def plan_launcher(plan: ExecPlan, yd, accd=None, use_acc=False, flags=0):
         return (lambda: K.mpk_baseline(plan.a.device(), yv, plan.p_m)), "crs"
     til = plan.tiling(complex_state=cplx)
     if til is None:
+        if cplx or use_acc or np.any(plan.kernel != 0):
+            return (lambda: K.mpk_crs_run(plan.a.device(), yv, cfg, acc=av, use_acc=use_acc, complex_state=cplx)), "crs"
         return (lambda: K.mpk_baseline(plan.a.device(), yv, plan.p_m)), "crs"
     sched = _schedule(plan, til, yv, cfg, av, use_acc, cplx, flags)
     if sched == "crs":

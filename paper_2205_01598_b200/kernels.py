@@ -172,6 +172,17 @@ def mpk_run(tiling: Tiling, y, cfg, acc=None, use_acc=False, complex_state=False
         check(ctx.lib.lmpk_ctx_check(ctx.handle, stream_handle(stream)), "mpk_run")
 
 
+def mpk_crs_run(a: DeviceCsr, y, cfg, acc=None, use_acc=False, complex_state=False, stream=None):
+    """A plan's powers as sweeps over the CRS arrays with the per-power kernel
+    (SpMV / Chebyshev) and accumulation fused (lmpk_mpk_crs_run): the path of
+    level-blocked plans on matrices whose rows exceed the tile format."""
+    ctx = context()
+    f = (_lib.FLAG_COMPLEX if complex_state else 0) | _lib.FLAG_EXACT
+    check(ctx.lib.lmpk_mpk_crs_run(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val), ptr(y),
+                                   int(y.stride(0)), int(y.shape[0]), ctypes.byref(cfg), ptr(acc),
+                                   1 if use_acc else 0, f, stream_handle(stream)), "mpk_crs_run")
+
+
 def bfs_levels(a: DeviceCsr, root=0, stream=None):
     """Returns (perm int32 tensor, inv_perm int32 tensor, level_ptr int64 numpy)."""
     torch = _torch()

@@ -240,6 +240,44 @@ def test_hub_rows_fall_back_to_crs_sweeps():
     assert np.array_equal(np.asarray(res.y.data), ref)
 
 
+def _star(n, off=-1e-3, diag=2.0):
+    i = np.arange(1, n)
+    rows = np.concatenate([np.zeros(n - 1, dtype=np.int64), i, np.arange(n)])
+    cols = np.concatenate([i, np.zeros(n - 1, dtype=np.int64), np.arange(n)])
+    vals = np.concatenate([np.full(n - 1, off), np.full(n - 1, off), np.full(n, diag)])
+    return lm.CsrMatrix.from_triplets(n, rows, cols, vals)
+
+
+@pytest.mark.parametrize("cplx", [False, True])
+def test_hub_rows_chebyshev_plans_run_as_crs_sweeps(cplx):
+    """Chebyshev propagation (fused recurrence + accumulation, real heat and
+    complex Schrodinger coefficients) on the star graph: its 70,000-entry row
+    exceeds the tile format, so every batch runs as lmpk_mpk_crs_run sweeps --
+    bitwise the oracle's restatement of ChebPropagator.step (cheb.py:221-246)."""
+    from oracle import cpu as C
+
+    a = _star(70_000, off=-1e-4, diag=0.5)
+    lo, hi = lm.gershgorin_bounds(a)
+    rng = np.random.default_rng(3)
+    if cplx:
+        co = lm.cheb_coeffs_schrodinger(0.3, lo, hi, tol=1e-10)
+        x = np.exp(1j * rng.uniform(0, 2 * np.pi, a.n_rows)) / np.sqrt(a.n_rows)
+        prop = lm.ChebPropagator(a, 0.3, coeffs=co, p_m_batch=4, cache_bytes=126e6)
+    else:
+        prop = lm.ChebPropagator(a, 0.3, tol=1e-8, p_m_batch=4, cache_bytes=126e6)
+        co = prop.coeffs
+        x = rng.uniform(-1, 1, a.n_rows)
+    assert prop._plan_for[4].tiling(complex_state=cplx) is None  # the tile format refuses the hub row
+    got = prop.step(x)
+    b = lm.scale_for_heat(a, lo, hi)
+    p = prop.pre.perm.perm
+    rp, c, v = C.permute_symmetric(b.row_ptr, b.col, b.val, p)
+    accp = O.cheb_batches(rp, c, v, x[p], np.real(co.c), np.imag(co.c) if cplx else None)
+    ref = np.empty_like(accp)
+    ref[p] = accp
+    assert np.array_equal(got, ref)
+
+
 @pytest.mark.parametrize("sched", ["walk", "sweep", "crs", "auto"])
 def test_schedule_choice_bitwise(sched, monkeypatch):
     """The executor's walk / sweep choice (LMPK_SCHEDULE) never changes the bits."""
