@@ -765,10 +765,13 @@ __device__ __forceinline__ bool spin_deps_acq(const MpkParams& P, int32_t lo, in
 }
 
 constexpr int kXleanRingMax = 4;
-template <bool CPLX, bool EXACT, bool VD, bool GEN, bool XP = false>
-__global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
+// NCV consumer warps and MINB CTAs per SM: (26, 1) or (12, 2) -- two CTAs per SM
+// are two independent rings, so one CTA's hand-off gaps are the other's work.
+constexpr int kXleanConsumers2 = 12;
+template <bool CPLX, bool EXACT, bool VD, bool GEN, bool XP = false, int NCV = kLeanConsumers, int MINB = 1>
+__global__ void __launch_bounds__(32 * (NCV + 2), MINB)
     mpk_xlean_kernel(MpkParams P, PowerCfgDev C, LeanParams L) {
-  constexpr int NC = kLeanConsumers;
+  constexpr int NC = NCV;
   constexpr int NPM = kXleanRingMax;
   constexpr uint32_t cw = CPLX ? 16u : 8u;
   extern __shared__ __align__(128) unsigned char smem_raw[];

@@ -130,6 +130,7 @@ struct lmpk_tiling {
   int32_t lean_xp = 0;             // 1: XP blocks (row records, units of up to 4 slices; lean_kernel.cuh)
   int32_t lean_xoff = 0;           // byte offset of the x buffer in a piece (= largest lean block)
   int32_t lean_np = 0;             // ring depth of the staged kernel
+  int32_t lean_ctas = 1;           // CTAs per SM the staged kernel runs with (2: 12 consumer warps each)
   int32_t lean_cplx = 0;           // vectors the x buffer was sized for (16-byte entries)
   int4* d_lean_runs = nullptr;     // [n_tiles * 32] {first entry, entries, buffer entry, 0}
   int2* d_lean_xinfo = nullptr;    // [n_tiles] {runs, staged entries}

@@ -953,7 +953,7 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_st_lo, lo.data(), ns * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_st_hi, hi.data(), ns * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-  LMPK_TRY(lean_worklist(T, items, first, lo, hi, T->info.grid, st));
+  LMPK_TRY(lean_worklist(T, items, first, lo, hi, T->info.grid * std::max(1, T->lean_ctas), st));
   (void)ctx;
   if (info) *info = T->info;
   *out = T;

@@ -8,10 +8,10 @@ const void* mpk_lean_fn_r_e(bool vd, bool gen, int np, bool xp);
 const void* mpk_lean_fn_r_f(bool vd, bool gen, int np, bool xp);
 const void* mpk_lean_fn_c_e(bool vd, int np, bool xp);
 const void* mpk_lean_fn_c_f(bool vd, int np, bool xp);
-const void* mpk_xlean_fn_r_e(bool vd, bool gen, bool xp);
-const void* mpk_xlean_fn_r_f(bool vd, bool gen, bool xp);
-const void* mpk_xlean_fn_c_e(bool vd, bool xp);
-const void* mpk_xlean_fn_c_f(bool vd, bool xp);
+const void* mpk_xlean_fn_r_e(bool vd, bool gen, bool xp, int ctas);
+const void* mpk_xlean_fn_r_f(bool vd, bool gen, bool xp, int ctas);
+const void* mpk_xlean_fn_c_e(bool vd, bool xp, int ctas);
+const void* mpk_xlean_fn_c_f(bool vd, bool xp, int ctas);
 
 // Sorted-slice descriptor for the fill kernel: global slice, tile, the
 // slice's column / value byte offsets inside the tile's lean block (pattern
@@ -510,7 +510,16 @@ int lean_xplan(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int32_t* 
 
 // Shared memory the staged kernel may use for its ring (static part and the
 // driver's reserve left out).
-int64_t lean_xs_budget(const lmpk_ctx* ctx) { return int64_t(ctx->max_smem_block) - 6144; }
+// CTAs per SM of the staged kernel: 1 x 26 consumer warps, or (LMPK_XLEAN_CTAS=2)
+// 2 x 12 -- two independent rings per SM
+int lean_xs_ctas() {
+  const char* e = getenv("LMPK_XLEAN_CTAS");
+  return e != nullptr && atoi(e) == 2 ? 2 : 1;
+}
+int64_t lean_xs_budget(const lmpk_ctx* ctx) {
+  if (lean_xs_ctas() == 2) return (int64_t(ctx->max_smem_sm) - 2 * (1024 + 6144)) / 2;
+  return int64_t(ctx->max_smem_block) - 6144;
+}
 // x staging is opt-in (LMPK_XLEAN=1): on the BASELINE shapes the unstaged walk
 // over XP blocks measured faster (the shallow ring of [block | x]
 // pieces leaves the consumers idle ~40% of the time)
@@ -586,6 +595,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   LMPK_TRY(lmalloc(&d_desc, S));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_tdict, tdict.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_nd, nd.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
+  const int ctas = xs ? lean_xs_ctas() : 1;
+  const int nc = ctas == 2 ? kXleanConsumers2 : kLeanConsumers;  // consumer warps per CTA
   // ---- XP blocks (staged dictionary tilings): units = runs of <= 4 slices.
   // A tile takes the XP format when its block stays under xp_limit (tiles of
   // many distinct rows -- grid corners -- keep the compact lean format).
@@ -664,7 +675,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
         // bins: longest unit first onto the lightest consumer warp
         {
           const size_t cntu = xp_recs.size() - u0;
-          std::vector<int32_t> idx(cntu), binof(cntu), load(kLeanConsumers, 0);
+          std::vector<int32_t> idx(cntu), binof(cntu), load(nc, 0);
           std::iota(idx.begin(), idx.end(), 0);
           auto cost = [&](int32_t i) {
             const uint4& r = xp_recs[u0 + i];
@@ -674,7 +685,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
           std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return cost(a) > cost(b); });
           for (int32_t i : idx) {
             int best = 0;
-            for (int b = 1; b < kLeanConsumers; ++b)
+            for (int b = 1; b < nc; ++b)
               if (load[b] < load[best]) best = b;
             binof[i] = best;
             load[best] += cost(i);
@@ -682,7 +693,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
           std::vector<uint4> r2;
           std::vector<XpUnitDesc> d2;
           std::vector<uint16_t> starts(kLeanConsumers + 2, 0);
-          for (int b = 0; b < kLeanConsumers; ++b) {
+          for (int b = 0; b < nc; ++b) {
             starts[b] = uint16_t(r2.size());
             for (size_t i = 0; i < cntu; ++i)
               if (binof[i] == b) {
@@ -690,7 +701,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
                 d2.push_back(xp_desc[u0 + i]);
               }
           }
-          starts[kLeanConsumers] = starts[kLeanConsumers + 1] = uint16_t(r2.size());
+          for (int b = nc; b < kLeanConsumers + 2; ++b) starts[b] = uint16_t(r2.size());
           std::copy(r2.begin(), r2.end(), xp_recs.begin() + u0);
           std::copy(d2.begin(), d2.end(), xp_desc.begin() + u0);
           xp_bins.insert(xp_bins.end(), starts.begin(), starts.end());
@@ -734,7 +745,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   // consumer warp a unit (shared-memory gathers need no second slice in flight)
   int pair_min = 0;
   if (xs) {
-    pair_min = 2 * kLeanConsumers;
+    pair_min = 2 * nc;
     if (const char* e = getenv("LMPK_XLEAN_PAIR")) pair_min = atoi(e) ? 0 : INT32_MAX;
   }
   for (int32_t t = 0; t < nt; ++t) {
@@ -904,6 +915,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
     int np_ring = int(std::min<int64_t>(kXleanRingMax, lean_xs_budget(ctx) / T->lean_piece));
     if (const char* e = getenv("LMPK_XLEAN_NP")) np_ring = std::max(2, std::min(np_ring, atoi(e)));
     T->lean_np = np_ring;
+    T->lean_ctas = ctas;
     T->d_lean_runs = d_runs;
     T->d_lean_xinfo = d_xinfo;
     T->h_lean_xinfo.resize(nt);
@@ -989,6 +1001,8 @@ bool lean_xs_runnable(const lmpk_tiling* T, const double* y, int64_t ldy, bool c
 // MpkParams as launch_ring; smem = the ring's pieces).
 int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev& C, bool cplx, bool exact, bool gen,
                 int grid, cudaStream_t st) {
+  const int ctas = T->lean_xs ? std::max(1, T->lean_ctas) : 1;
+  grid *= ctas;
   const bool wl = T->lean_xs && T->lean_wl_grid == grid;
   LeanParams L{T->d_lean,    T->d_lean_ofs, T->d_rowlen, T->d_lean_runs,
                T->d_lean_xinfo, T->lean_xoff, T->lean_np, wl ? T->d_lean_wl : nullptr,
@@ -1007,8 +1021,8 @@ int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev&
   if (T->lean_xs) {
     np = T->lean_np;
     const bool xp = T->lean_xp != 0;
-    fn = cplx ? (exact ? mpk_xlean_fn_c_e(vd, xp) : mpk_xlean_fn_c_f(vd, xp))
-              : (exact ? mpk_xlean_fn_r_e(vd, gen, xp) : mpk_xlean_fn_r_f(vd, gen, xp));
+    fn = cplx ? (exact ? mpk_xlean_fn_c_e(vd, xp, ctas) : mpk_xlean_fn_c_f(vd, xp, ctas))
+              : (exact ? mpk_xlean_fn_r_e(vd, gen, xp, ctas) : mpk_xlean_fn_r_f(vd, gen, xp, ctas));
   } else {
     const bool xp = T->lean_xp != 0;
     fn = cplx ? (exact ? mpk_lean_fn_c_e(vd, np, xp) : mpk_lean_fn_c_f(vd, np, xp))
@@ -1033,12 +1047,13 @@ int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev&
     cudaFuncAttributes fa;
     LMPK_CHECK_CUDA(cudaFuncGetAttributes(&fa, fn));
     const int per_sm = std::max(1, ctx->max_smem_sm);
-    int pct = std::min(100, int((int64_t(smem + int(fa.sharedSizeBytes) + 1024) * 100 + per_sm - 1) / per_sm));
+    int pct = std::min(100, int((int64_t(smem + int(fa.sharedSizeBytes) + 1024) * ctas * 100 + per_sm - 1) / per_sm));
     if (const char* e = getenv("LMPK_LEAN_CARVE")) pct = std::max(0, std::min(100, atoi(e)));
     LMPK_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
   }
   Pm.smem_cap = piece;
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(32 * (kLeanConsumers + 2)), args, smem, st);
+  const int nthreads = 32 * ((ctas == 2 ? kXleanConsumers2 : kLeanConsumers) + 2);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(nthreads), args, smem, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("mpk lean launch failed: %s (grid %d, smem %d)", cudaGetErrorString(e), grid, smem);

@@ -2,8 +2,10 @@
 #include "lean_kernel.cuh"
 
 namespace lmpk {
-const void* mpk_xlean_fn_c_f(bool vd, bool xp) {
-#define LMPK_XLEAN_FN(V, X) reinterpret_cast<const void*>(mpk_xlean_kernel<true, false, V, true, X>)
+const void* mpk_xlean_fn_c_f(bool vd, bool xp, int ctas) {
+#define LMPK_XLEAN_FN(V, X)                                                                                  \
+  (ctas == 2 ? reinterpret_cast<const void*>(mpk_xlean_kernel<true, false, V, true, X, kXleanConsumers2, 2>) \
+             : reinterpret_cast<const void*>(mpk_xlean_kernel<true, false, V, true, X>))
   if (vd && xp) return LMPK_XLEAN_FN(true, true);
   return vd ? LMPK_XLEAN_FN(true, false) : LMPK_XLEAN_FN(false, false);
 #undef LMPK_XLEAN_FN
