@@ -4,6 +4,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <chrono>
 #include <vector>
 
 #include "lmpk.h"
@@ -146,6 +147,25 @@ namespace lmpk {
 
 int ctx_check_device_error(lmpk_ctx* ctx, const char* what);
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// LMPK_TILING_PROF=1: host wall-clock marks of lmpk_tiling_create's phases
+struct PhaseTimer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit PhaseTimer(cudaStream_t s) : on(getenv("LMPK_TILING_PROF") != nullptr), st(s) {
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tiling] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
+
 
 // ------------------------------------------------------------------ device helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

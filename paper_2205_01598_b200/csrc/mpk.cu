@@ -619,6 +619,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   // that many slices, so a tile's block and x buffer share one ring piece
   const int32_t ns_cap = xs_slices > 0 ? xs_slices : INT32_MAX;
   const int32_t S = static_cast<int32_t>(width.size());
+  PhaseTimer pt(st);
   std::vector<int32_t> first;
   std::vector<int64_t> Es;
   std::vector<int32_t> tmode;   // per tile: 0 plain, else kModeC16 [| kModeDict | nd << 8]
@@ -670,6 +671,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
       s = e;
     }
     const int32_t n1 = static_cast<int32_t>(f1.size());
+    pt.mark("partition pass 1");
     // dictionaries of the compressed pass-1 tiles (on the device)
     std::vector<int32_t> row1(n1 + 1), list;
     for (int32_t t = 0; t < n1; ++t) {
@@ -696,6 +698,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
       cudaFree(d_list);
       cudaFree(d_nd);
     }
+    pt.mark("tile dictionaries");
     // pass 2: final tiles
     for (int32_t t = 0, li = 0; t < n1; ++t) {
       const int32_t s0 = f1[t], s1 = t + 1 < n1 ? f1[t + 1] : S;
@@ -733,6 +736,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     tdict.assign(first.size(), -1);
   }
   const int32_t nt = static_cast<int32_t>(first.size());
+  pt.mark("partition pass 2");
   // compressed tiles with slices wider than 8 take the long-row kernel body
   for (int32_t t = 0; t < nt; ++t) {
     if (!tmode[t]) continue;
@@ -851,11 +855,13 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
                                                              T->d_dep_hi);
   launch_count_add(ctx, 1);
   LMPK_CHECK_CUDA(cudaGetLastError());
+  pt.mark("alloc + fill blocks + deps");
   if ((n_comp == nt || (xs_slices > 0 && n_comp > 0)) && !xc) {
     std::vector<int32_t> tfirst(first.begin(), first.begin() + nt);
     LMPK_TRY(lean_build(ctx, T, n, row_ptr, col, val, tfirst, width, d_wmin, tmode, tdict, d_dict_tab, d_width, cap,
                         xs_slices > 0, cplx, st));
   }
+  pt.mark("lean build");
   T->h_dep_lo.resize(nt);
   T->h_dep_hi.resize(nt);
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->h_dep_lo.data(), T->d_dep_lo, nt * 4, cudaMemcpyDeviceToHost, st));
@@ -870,6 +876,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   cudaFree(d_dict_tab);
   T->info.n_tiles = nt;
   T->info.block_bytes = ofs;
+  pt.mark("geometry D2H + frees");
   return LMPK_OK;
 }
 
@@ -1019,6 +1026,8 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     }
   }
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  PhaseTimer ptc(st);
+  ptc.mark("slice widths (sync only)");
   int32_t max_row = 0;
   for (int32_t w : width) max_row = std::max(max_row, w);
   LMPK_ARG_CHECK(max_row <= 65535, "rows longer than 65535 entries are not supported by the tiled kernel");
@@ -1208,7 +1217,12 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   T->info.slots = slots;
   T->xoff = xoff_used;
   T->info.x_staged_tiles = T->staged_tiles;
-  if (ring) return finish_ring_tiling(ctx, T, p_m, prm, info, out, st);
+  ptc.mark("candidates / build_tiling");
+  if (ring) {
+    const int rc = finish_ring_tiling(ctx, T, p_m, prm, info, out, st);
+    ptc.mark("finish_ring_tiling");
+    return rc;
+  }
   // skewed diagonal key (t + g*M, g), M = q*D + slack
   const int32_t G = (p_m + q_used - 1) / q_used;
   // default slack ~3 * (items in flight) / G: the dependency of an item must

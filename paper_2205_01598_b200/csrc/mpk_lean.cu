@@ -547,6 +547,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   if (nt == 0 || S == 0 || getenv("LMPK_NO_LEAN")) return LMPK_OK;
   for (int32_t s = 0; s < S; ++s)
     if (width[s] > 8) return LMPK_OK;
+  PhaseTimer pt(st);
   int vd = -1;
   bool any_plain = false;
   for (int32_t t = 0; t < nt; ++t) {
@@ -732,6 +733,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
     LMPK_CHECK_CUDA(cudaMemcpyAsync(np.data(), d_np, size_t(S) * 4, cudaMemcpyDeviceToHost, st));
   }
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+  pt.mark("  lean: plan + pattern pass");
   std::vector<int64_t> ofs(nt + 1, 0);
   std::vector<int32_t> rec_ptr(nt + 1, 0);
   std::vector<uint4> recs;
@@ -756,13 +758,15 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
       ofs[t + 1] = ofs[t] + xp_bytes[t];
       continue;
     }
-    // width classes 0..8, full slices first inside a class
-    order.clear();
-    for (int w = 0; w <= 8; ++w)
-      for (int pad = 0; pad < 2; ++pad)
-        for (int32_t s = s0; s < s1; ++s)
-          if (width[s] == w && ((wmin[s] < w) ? 1 : 0) == pad) order.push_back(s);
+    // width classes 0..8, full slices first inside a class (counting sort)
     const int32_t ns = s1 - s0;
+    {
+      int32_t cnt[19] = {0};
+      for (int32_t s = s0; s < s1; ++s) ++cnt[2 * width[s] + (wmin[s] < width[s] ? 1 : 0) + 1];
+      for (int q = 0; q < 18; ++q) cnt[q + 1] += cnt[q];
+      order.resize(ns);
+      for (int32_t s = s0; s < s1; ++s) order[cnt[2 * width[s] + (wmin[s] < width[s] ? 1 : 0)]++] = s;
+    }
     const bool pairing = ns >= pair_min;
     int32_t nu = 0;
     for (int32_t i = 0; i < ns;) {
@@ -825,6 +829,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
     ofs[t + 1] = ofs[t] + bytes;
   }
   rec_ptr[nt] = static_cast<int32_t>(recs.size());
+  pt.mark("  lean: host units");
   const int64_t total = ofs[nt];
   int64_t* d_ofs = nullptr;
   unsigned char* d_lean = nullptr;
@@ -895,6 +900,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   cudaFree(d_tdict);
   cudaFree(d_nd);
   cudaFree(d_np);
+  pt.mark("  lean: alloc + fill + frees");
   T->d_lean = d_lean;
   T->d_lean_ofs = d_ofs;
   T->d_rowlen = d_rowlen;
