@@ -1452,6 +1452,7 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
     Pm.xmode = aligned ? 1 : 2;
   }
   Pm.flags = flags;
+  if (const char* e = getenv("LMPK_ACQ")) Pm.flags |= atoi(e) == 0 ? kFlagNoAcqFence : (atoi(e) == 1 ? kFlagAcqLoads : 0);
   if (const char* e = getenv("LMPK_YPOL")) Pm.ypol = atoi(e);
   Pm.err = ctx->err.dev;
   Pm.prof = ctx->prof;

@@ -1235,6 +1235,11 @@ __device__ __forceinline__ bool mbar_wait_bounded(uint64_t* bar, uint32_t parity
   return ok != 0;
 }
 
+// Experiment switches of the dependency wait (LMPK_ACQ, mpk.cu): acquire
+// loads instead of relaxed loads + fence; no fence at all (measurement only:
+// not a valid acquire pattern).
+constexpr int kFlagNoAcqFence = 0x100000, kFlagAcqLoads = 0x200000;
+
 // Spin until progress[lo..hi] >= target (one warp, all loads in flight per
 // round); then one acquire fence (also invalidates L1 for the gathers).
 // Returns false if the launch is aborting (abort flag or watchdog).
@@ -1244,10 +1249,18 @@ __device__ __forceinline__ bool spin_deps(const MpkParams& P, int32_t lo, int32_
   unsigned long long t0 = 0;
   for (int spins = 0;; ++spins) {
     uint32_t m = 0xffffffffu;
-    for (int32_t i = lo + lane; i <= hi; i += 32) m = min(m, ld_relaxed_u32(P.progress + i));
+    if (P.flags & kFlagAcqLoads) {
+      for (int32_t i = lo + lane; i <= hi; i += 32) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.progress + i) : "memory");
+        m = min(m, v);
+      }
+    } else {
+      for (int32_t i = lo + lane; i <= hi; i += 32) m = min(m, ld_relaxed_u32(P.progress + i));
+    }
     ++*rounds;
     if (__all_sync(0xffffffffu, m >= target)) {
-      fence_acq_rel_gpu();
+      if (!(P.flags & (kFlagAcqLoads | kFlagNoAcqFence))) fence_acq_rel_gpu();
       return true;
     }
     if (spins > 2) __nanosleep(64);
