@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -s 0 -c 400 --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 for cfg in ${PROF_CONFIGS:-cfg2 cfg5 cfg1 cfg3 cfg4}; do
   case $cfg in
-    cfg4) K='regex:spmv_rows_kernel' ;;
+    cfg4) K='regex:spmv_rows' ;;
     *) K='regex:mpk_(lean|ring|group)_kernel|spmv_rows_kernel' ;;
   esac
   timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k "$K" -c 1 -f \

@@ -8,7 +8,7 @@ import paper_2205_01598_b200 as lm
 from paper_2205_01598_b200 import kernels as K
 
 REPS = int(os.environ.get("REPS", "30"))
-KNOBS = ("LMPK_XLEAN_CTAS", "LMPK_XLEAN", "LMPK_XP", "LMPK_XLEAN_PUB", "LMPK_NO_WORKLIST", "LMPK_LEAN_NP", "LMPK_NO_XP", "LMPK_XP_LIMIT", "LMPK_XP_RUN", "LMPK_NO_XLEAN", "LMPK_XLEAN_ROWS", "LMPK_XLEAN_NP", "LMPK_XLEAN_PAIR", "LMPK_SUPER_NNZ", "LMPK_LEAN_CARVE",
+KNOBS = ("LMPK_ACQ", "LMPK_XLEAN_CTAS", "LMPK_XLEAN", "LMPK_XP", "LMPK_XLEAN_PUB", "LMPK_NO_WORKLIST", "LMPK_LEAN_NP", "LMPK_NO_XP", "LMPK_XP_LIMIT", "LMPK_XP_RUN", "LMPK_NO_XLEAN", "LMPK_XLEAN_ROWS", "LMPK_XLEAN_NP", "LMPK_XLEAN_PAIR", "LMPK_SUPER_NNZ", "LMPK_LEAN_CARVE",
          "LMPK_PASS_POWERS", "LMPK_NO_PATTERN")
 
 
