@@ -155,6 +155,9 @@ typedef struct lmpk_tiling_info {
                          /* in shared memory (a piece = lean block + x buffer)  */
   int32_t lean_ring;     /* staged lean walk: pieces in the shared-memory ring   */
   int32_t lean_piece;    /* staged lean walk: bytes of one piece                 */
+  int32_t dp_tiles;      /* tiles in the diagonal-private dictionary format (DP  */
+                         /* tiling: one global dictionary of off-diagonal values, */
+                         /* a private diagonal value per row, 32-bit offsets)    */
 } lmpk_tiling_info;
 
 /* Tuning knobs of lmpk_tiling_create (0 = library default). */

@@ -57,6 +57,7 @@ class TilingInfo(ctypes.Structure):
         ("compressed_tiles", _i32), ("dict_tiles", _i32), ("super_tiles", _i32),
         ("lean_bytes", _i64), ("lean_pattern_tiles", _i32),
         ("lean_xstaged", _i32), ("lean_ring", _i32), ("lean_piece", _i32),
+        ("dp_tiles", _i32),
     ]
 
     def as_dict(self):

@@ -341,6 +341,59 @@ __device__ __forceinline__ void lean_store(const PowTab& pt, double* acc, bool u
   }
 }
 
+// The epilogue's own operands (y_{p-2} of the Chebyshev step, acc) are
+// L1-prefetched BEFORE the gathers are issued, so their L2 / HBM latency
+// overlaps the gathers' instead of following the row sum; lean_store_pf then
+// loads them with plain L1-allocating loads.  (Loading them into registers up
+// front does not work: under the 72-register cap ptxas sinks the loads below
+// the row sum, and the Chebyshev subtraction took 35% of all stall samples.)
+// Both vectors are written only by this row's items at other powers, which
+// the item dependencies order, and the item's dependency acquire invalidated
+// the L1 -- the argument that makes the gathers coherent.
+template <bool CPLX, bool GEN>
+__device__ __forceinline__ void lean_prefetch_epi(const PowTab& pt, const double* acc, bool use_acc, int64_t r,
+                                                  bool valid) {
+  if constexpr (GEN) {
+    if (valid) {
+      if (pt.cheb) asm volatile("prefetch.global.L1 [%0];" ::"l"(pt.ypv + (CPLX ? 2 : 1) * r));
+      if (use_acc) asm volatile("prefetch.global.L1 [%0];" ::"l"(acc + (CPLX ? 2 : 1) * r));
+    }
+  }
+}
+template <bool CPLX, bool EXACT, bool GEN>
+__device__ __forceinline__ void lean_store_pf(const PowTab& pt, double* acc, bool use_acc, int64_t r,
+                                              LeanSum<CPLX> s) {
+  if constexpr (!CPLX) {
+    double t = s.r;
+    if constexpr (GEN) {
+      if (pt.cheb) t = __dsub_rn(__dmul_rn(2.0, t), ldg_f64(reinterpret_cast<const char*>(pt.ypv + r)));
+    }
+    stg_f64(pt.yout + r, t);
+    if constexpr (GEN) {
+      if (use_acc) stg_f64(acc + r, madd<EXACT>(ldg_f64(reinterpret_cast<const char*>(acc + r)), pt.cre, t));
+    }
+  } else {
+    double2 t = make_double2(s.r, s.i);
+    const int64_t r2 = 2 * r;
+    if constexpr (GEN) {
+      if (pt.cheb) {
+        const double2 pv = ldg_f64x2(reinterpret_cast<const char*>(pt.ypv + r2));
+        t.x = __dsub_rn(__dmul_rn(2.0, t.x), pv.x);
+        t.y = __dsub_rn(__dmul_rn(2.0, t.y), pv.y);
+      }
+    }
+    stg_f64x2(pt.yout + r2, t);
+    if constexpr (GEN) {
+      if (use_acc) {
+        const double2 a = ldg_f64x2(reinterpret_cast<const char*>(acc + r2));
+        const double pr = __dsub_rn(__dmul_rn(pt.cre, t.x), __dmul_rn(pt.cim, t.y));
+        const double pim = __dadd_rn(__dmul_rn(pt.cre, t.y), __dmul_rn(pt.cim, t.x));
+        stg_f64x2(acc + r2, make_double2(__dadd_rn(a.x, pr), __dadd_rn(a.y, pim)));
+      }
+    }
+  }
+}
+
 // Lane's column-offset / code addresses of one slice.  Plain lean slices
 // hold every lane's entries (lane-contiguous); PATTERN slices (dictionary
 // tiles) hold the slice's distinct rows once -- [32 u8 row pattern ids]
@@ -350,7 +403,7 @@ __device__ __forceinline__ void lean_ptrs(uint32_t blk, uint32_t off, uint32_t n
                                           uint32_t& cp, uint32_t& vp, uint32_t vo) {
   if (VD && pat) {
     const uint32_t sl = blk + off;
-    const uint32_t id = lds_b8(sl + lane);
+    const uint32_t id = np > 1u ? lds_b8(sl + lane) : 0u;  // one pattern (grid interior): no id
     cp = sl + 32 + id * (2 * lean_wc(W));
     vp = sl + 32 + np * (2 * lean_wc(W)) + id * lean_wc(W);
   } else {
@@ -364,6 +417,15 @@ __device__ __forceinline__ void lean_ptrs(uint32_t blk, uint32_t off, uint32_t n
 // {slice a off, slice b off, W | flags | Pa << 16 | Pb << 24, slice ids}.
 // XS (x staging): the column fields hold (x-buffer entry - lane) and the
 // gathers read the piece's x buffer at shared address xb.
+// the staged kernel keeps the L2 loads of lean_store (its gathers come from shared memory)
+template <bool CPLX, bool EXACT, bool GEN, bool XS>
+__device__ __forceinline__ void lean_store_u(const PowTab& pt, double* acc, bool use_acc, int64_t r, LeanSum<CPLX> s) {
+  if constexpr (XS)
+    lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, r, s);
+  else
+    lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, r, s);
+}
+
 template <int W, bool CPLX, bool EXACT, bool VD, bool GEN, bool XS = false>
 __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane, int32_t r0, int32_t nrows,
                                           const PowTab& pt, double* acc, bool use_acc, const uint8_t* rowlen,
@@ -384,7 +446,9 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
   uint32_t cp0, vp0;
   lean_ptrs<W, VD>(blk, rec.x, (rec.z >> 16) & 255u, pat, lane, cp0, vp0, rec.y);
   const bool padded = (rec.z & kLeanPadded) != 0;
+  if constexpr (!XS) lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l0), l0 < nrows);
   if (rec.z & kLeanPair) {
+    if constexpr (!XS) lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l1), l1 < nrows);
     RP rp1;
     if constexpr (XS)
       rp1 = xb + uint32_t(pat ? min(int32_t(lane), nrows - 1 - s1 * 32) : int32_t(lane)) * uint32_t(cw);
@@ -405,13 +469,181 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
       if (lean_nan(b.r) || (CPLX && lean_nan(b.i)))
         if (l1 < nrows) b = lean_row_exact<CPLX, EXACT, VD, XS>(cp1, vp1, dict, lane, rp1, W, rowlen[r0 + l1]);
     }
-    if (l0 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
-    if (l1 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l1), b);
+    if (l0 < nrows) lean_store_u<CPLX, EXACT, GEN, XS>(pt, acc, use_acc, int64_t(r0 + l0), a);
+    if (l1 < nrows) lean_store_u<CPLX, EXACT, GEN, XS>(pt, acc, use_acc, int64_t(r0 + l1), b);
   } else {
     LeanSum<CPLX> a = lean_slice<W, CPLX, EXACT, VD, XS>(cp0, vp0, dict, lane, rp0);
     if (padded && (lean_nan(a.r) || (CPLX && lean_nan(a.i))))
       if (l0 < nrows) a = lean_row_exact<CPLX, EXACT, VD, XS>(cp0, vp0, dict, lane, rp0, W, rowlen[r0 + l0]);
-    if (l0 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
+    if (l0 < nrows) lean_store_u<CPLX, EXACT, GEN, XS>(pt, acc, use_acc, int64_t(r0 + l0), a);
+  }
+}
+
+// ---------------------------------------------------------------- DP units
+// DIAGONAL-PRIVATE dictionary blocks (lean_vd == 2; built by dp_build in
+// mpk_dp.cuh): matrices whose off-diagonal values come from one small global
+// dictionary while the diagonal differs row by row -- a stencil plus a
+// potential (the Anderson / Schroedinger operators of the paper's Chebyshev
+// application).  Every slice is a pattern slice with 32-bit column offsets:
+//   [32 u8 row pattern ids][P x Wc i32 (col - row)][P x Wc u8 codes]
+//   [pad to 8][32 f64 private values (lane's diagonal entry)]
+// A code is 8 x the dictionary index; kDpPriv marks the row's diagonal
+// entry, whose value is the lane's private one.  The row sum itself is
+// lean_chain in storage order, so EXACT mode stays bitwise the reference
+// (executor.py:127-130, csr.py:195-201); padding entries carry the code of
+// +0.0 and repeat the row's last column as in the lean blocks above.
+constexpr uint32_t kDpPriv = 248u;
+__host__ __device__ constexpr int dp_priv_off(int w, int np) { return (32 + 5 * lean_wc(w) * np + 7) & ~7; }
+__host__ __device__ constexpr int dp_slice_bytes(int w, int np) {
+  return w <= 0 ? 0 : ((dp_priv_off(w, np) + 256 + 15) & ~15);
+}
+
+// Lane's addresses in a DP slice: op = its pattern's offsets, kp = its
+// pattern's codes, pd = (address of its private value) - dict - kDpPriv.
+template <int W>
+__device__ __forceinline__ void dp_ptrs(uint32_t sl, uint32_t np, uint32_t lane, uint32_t dict, uint32_t& op,
+                                        uint32_t& kp, uint32_t& pd) {
+  constexpr uint32_t WC = lean_wc(W);
+  const uint32_t id = np > 1u ? lds_b8(sl + lane) : 0u;
+  op = sl + 32u + id * (4u * WC);
+  kp = sl + 32u + np * (4u * WC) + id * WC;
+  pd = sl + ((32u + 5u * WC * np + 7u) & ~7u) + lane * 8u - dict - kDpPriv;
+}
+template <int W>
+__device__ __forceinline__ void dp_cols(uint32_t op, int32_t (&c)[W]) {
+  const uint4 a = lds_v4(op);
+  const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int j = 0; j < (W < 4 ? W : 4); ++j) c[j] = int32_t(w4[j]);
+  if constexpr (W > 4) {
+    const uint4 b = lds_v4(op + 16);
+    const uint32_t v4[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int j = 4; j < W; ++j) c[j] = int32_t(v4[j - 4]);
+  }
+}
+template <int W>
+__device__ __forceinline__ void dp_vals(uint32_t kp, uint32_t dict, uint32_t pd, double (&v)[W]) {
+  uint32_t k0, k1 = 0u;
+  if constexpr (lean_wc(W) == 8) {
+    const uint2 k = lds_v2(kp);
+    k0 = k.x, k1 = k.y;
+  } else {
+    k0 = lds_u32(kp);
+  }
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    const uint32_t code = __byte_perm(j < 4 ? k0 : k1, 0u, 0x4440u + uint32_t(j & 3));
+    v[j] = lds_d(dict + code + (code == kDpPriv ? pd : 0u));
+  }
+}
+template <bool CPLX, bool EXACT>
+__device__ __noinline__ LeanSum<CPLX> dp_row_exact(uint32_t op, uint32_t kp, uint32_t dict, uint32_t pd,
+                                                   const char* rp, int len) {
+  LeanSum<CPLX> s{0.0, 0.0};
+  for (int j = 0; j < len; ++j) {
+    const int32_t c = int32_t(lds_u32(op + 4 * j));
+    const uint32_t code = lds_b8(kp + j);
+    const double v = lds_d(dict + code + (code == kDpPriv ? pd : 0u));
+    const typename LeanX<CPLX>::T x = lean_gather<CPLX, false>(rp, c);
+    if constexpr (CPLX) {
+      s.r = madd<EXACT>(s.r, v, x.x);
+      s.i = madd<EXACT>(s.i, v, x.y);
+    } else {
+      s.r = madd<EXACT>(s.r, v, x);
+    }
+  }
+  return s;
+}
+
+// One slice of a DP unit (tile-local slice sidx at byte offset sl_off of the
+// block, np distinct rows): prefetch of the epilogue operands, gathers, row
+// sum, epilogue.
+template <int W, bool CPLX, bool EXACT, bool GEN>
+__device__ __forceinline__ void dp_single(uint32_t blk, uint32_t sl_off, uint32_t np, int32_t sidx, bool padded,
+                                          uint32_t lane, int32_t r0, int32_t nrows, const PowTab& pt, double* acc,
+                                          bool use_acc, const uint8_t* rowlen) {
+  constexpr int cw = CPLX ? 16 : 8;
+  const uint32_t dict = blk + kLeanDict;
+  const int32_t l0 = sidx * 32 + int32_t(lane);
+  // lanes past the tile use the last valid lane's pattern: gather around that row
+  const char* rp0 = pt.yin + int64_t(r0 + min(l0, nrows - 1)) * cw;
+  uint32_t op0, kp0, pd0;
+  dp_ptrs<W>(blk + sl_off, np, lane, dict, op0, kp0, pd0);
+  lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l0), l0 < nrows);
+  int32_t c0[W];
+  dp_cols<W>(op0, c0);
+  typename LeanX<CPLX>::T x0[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) x0[j] = lean_gather<CPLX, false>(rp0, c0[j]);
+  double v[W];
+  dp_vals<W>(kp0, dict, pd0, v);
+  LeanSum<CPLX> a = lean_chain<W, CPLX, EXACT>(v, x0);
+  if (padded && (lean_nan(a.r) || (CPLX && lean_nan(a.i))))
+    if (l0 < nrows) a = dp_row_exact<CPLX, EXACT>(op0, kp0, dict, pd0, rp0, rowlen[r0 + l0]);
+  if (l0 < nrows) lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
+}
+
+// One DP unit of width W: rec = {slice a off, slice b off,
+// W | flags | Pa << 16 | Pb << 24, slice ids} as for lean pattern units.
+// Real vectors keep both slices of a pair in flight (2W gathers); complex
+// vectors take a pair's slices one after the other (2W double2 gathers exceed
+// the register budget; dp_build gives complex tilings single-slice units).
+template <int W, bool CPLX, bool EXACT, bool GEN>
+__device__ __forceinline__ void dp_unit(uint32_t blk, uint4 rec, uint32_t lane, int32_t r0, int32_t nrows,
+                                        const PowTab& pt, double* acc, bool use_acc, const uint8_t* rowlen) {
+  constexpr int cw = CPLX ? 16 : 8;
+  const uint32_t dict = blk + kLeanDict;
+  const int32_t s0 = int32_t(rec.w & 0xffffu), s1 = int32_t(rec.w >> 16);
+  const int32_t l0 = s0 * 32 + int32_t(lane), l1 = s1 * 32 + int32_t(lane);
+  const bool pair = (rec.z & kLeanPair) != 0;
+  const bool padded = (rec.z & kLeanPadded) != 0;
+  if constexpr (W == 0) {
+    if (l0 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), LeanSum<CPLX>{0.0, 0.0});
+    if (pair && l1 < nrows) lean_store<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l1), LeanSum<CPLX>{0.0, 0.0});
+  } else if constexpr (CPLX) {
+#pragma unroll 1
+    for (int h = 0; h < (pair ? 2 : 1); ++h)
+      dp_single<W, CPLX, EXACT, GEN>(blk, h ? rec.y : rec.x, h ? (rec.z >> 24) : ((rec.z >> 16) & 255u), h ? s1 : s0,
+                                     padded, lane, r0, nrows, pt, acc, use_acc, rowlen);
+  } else if (!pair) {
+    dp_single<W, CPLX, EXACT, GEN>(blk, rec.x, (rec.z >> 16) & 255u, s0, padded, lane, r0, nrows, pt, acc, use_acc,
+                                   rowlen);
+  } else {
+    const char* rp0 = pt.yin + int64_t(r0 + min(l0, nrows - 1)) * cw;
+    const char* rp1 = pt.yin + int64_t(r0 + min(l1, nrows - 1)) * cw;
+    uint32_t op0, kp0, pd0, op1, kp1, pd1;
+    dp_ptrs<W>(blk + rec.x, (rec.z >> 16) & 255u, lane, dict, op0, kp0, pd0);
+    dp_ptrs<W>(blk + rec.y, rec.z >> 24, lane, dict, op1, kp1, pd1);
+    lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l0), l0 < nrows);
+    lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l1), l1 < nrows);
+    int32_t c0[W], c1[W];
+    dp_cols<W>(op0, c0);
+    dp_cols<W>(op1, c1);
+    typename LeanX<CPLX>::T x0[W], x1[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) x0[j] = lean_gather<CPLX, false>(rp0, c0[j]);
+#pragma unroll
+    for (int j = 0; j < W; ++j) x1[j] = lean_gather<CPLX, false>(rp1, c1[j]);
+    LeanSum<CPLX> a, b;
+    {
+      double v[W];
+      dp_vals<W>(kp0, dict, pd0, v);
+      a = lean_chain<W, CPLX, EXACT>(v, x0);
+    }
+    {
+      double v[W];
+      dp_vals<W>(kp1, dict, pd1, v);
+      b = lean_chain<W, CPLX, EXACT>(v, x1);
+    }
+    if (padded) {
+      if (lean_nan(a.r))
+        if (l0 < nrows) a = dp_row_exact<CPLX, EXACT>(op0, kp0, dict, pd0, rp0, rowlen[r0 + l0]);
+      if (lean_nan(b.r))
+        if (l1 < nrows) b = dp_row_exact<CPLX, EXACT>(op1, kp1, dict, pd1, rp1, rowlen[r0 + l1]);
+    }
+    if (l0 < nrows) lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
+    if (l1 < nrows) lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l1), b);
   }
 }
 
@@ -540,7 +772,7 @@ __device__ __forceinline__ uint32_t lean_wait(uint64_t* bar, uint32_t parity, ui
 // ---------------------------------------------------------------- kernel
 // Same launch contract as mpk_ring_kernel (cooperative, one CTA per SM, a
 // 2-piece ring): warp NC is the producer, warp NC + 1 the publisher.
-template <bool CPLX, bool EXACT, bool VD, bool GEN, int NP, bool XP = false>
+template <bool CPLX, bool EXACT, bool VD, bool GEN, int NP, bool XP = false, bool DP = false>
 __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
     mpk_lean_kernel(MpkParams P, PowerCfgDev C, LeanParams L) {
   constexpr int NC = kLeanConsumers;
@@ -691,8 +923,13 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
       for (; u < nu; u += NC) {
         const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);
         switch (rec.z & 15u) {
-#define LMPK_LEAN_CASE(Wv) \
-  case Wv: lean_unit<Wv, CPLX, EXACT, VD, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen); break;
+#define LMPK_LEAN_CASE(Wv)                                                                     \
+  case Wv:                                                                                     \
+    if constexpr (DP)                                                                          \
+      dp_unit<Wv, CPLX, EXACT, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen);  \
+    else                                                                                       \
+      lean_unit<Wv, CPLX, EXACT, VD, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen); \
+    break;
           LMPK_LEAN_CASE(0)
           LMPK_LEAN_CASE(1)
           LMPK_LEAN_CASE(2)

@@ -880,6 +880,8 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   return LMPK_OK;
 }
 
+#include "mpk_dp.cuh"
+
 // Ring walk: super-tiles (runs of consecutive tiles of ~tile_nnz_hint
 // nonzeros, default 32K: cfg2's ~34K-nonzero tiles become one super-tile
 // each, 0.447 vs 0.470 ms for the former 64K default that paired them; cfg5
@@ -931,7 +933,8 @@ static int finish_ring_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t p_m, const 
   // take 4x the spacing: nothing is lost to the longer reuse distance and the
   // dependency waits all but vanish (cfg2 0.381 -> 0.371 ms, tools/xlean_sweep.py SLACK)
   const int32_t mult = (T->d_lean && T->lean_bytes < (int64_t(48) << 20)) ? 20 : 5;
-  const int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (mult * T->info.grid) / G);
+  int32_t slack = prm.queue_slack > 0 ? prm.queue_slack : std::max(1, (mult * T->info.grid) / G);
+  if (const char* e = getenv("LMPK_RING_SLACK")) slack = std::max(1, atoi(e));  // experiments (tools/cfg5_sweep.py)
   T->info.queue_slack = G > 1 ? slack : 0;
   T->info.max_fwd_reach = D;
   T->info.super_tiles = ns;
@@ -1140,6 +1143,46 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
       xs_slices = R / 32;
       xs_bcap = bcap;
       break;
+    }
+  }
+  // DP tiling (mpk_dp.cuh): rows of <= 8 entries whose values defeat the
+  // per-tile dictionaries but whose off-diagonal values come from one small
+  // global dictionary (stencil + potential: cfg5's Anderson operator)
+  if (default_plan && ring && compress && !xstage && !unstaged && xs_slices == 0 && n > 0 && prm.slots == 0 &&
+      prm.tile_nnz_hint == 0 && max_row >= 1 && max_row <= 8) {
+    bool dictish = false;
+    {
+      const int32_t ns = std::min<int32_t>(h_nnz, 32768);
+      std::vector<uint64_t> bits(ns);
+      if (ns > 0) LMPK_CHECK_CUDA(cudaMemcpyAsync(bits.data(), val, size_t(ns) * 8, cudaMemcpyDeviceToHost, st));
+      LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+      std::sort(bits.begin(), bits.end());
+      dictish = std::unique(bits.begin(), bits.end()) - bits.begin() <= kDictMax;
+    }
+    if (dp_wanted(max_row, dictish)) {
+      lmpk_tiling* D = nullptr;
+      LMPK_TRY(dp_build(ctx, n, row_ptr, col, val, width, d_w, d_wmin, cplx_t, st, &D));
+      if (D) {
+        D->info.p_m = p_m;
+        D->info.mode = 3;
+        D->info.block = 32 * (kLeanConsumers + 2);
+        D->ring = true;
+        D->piece = D->lean_piece;
+        D->slots = 2;
+        D->info.smem_bytes = 2 * D->lean_piece;
+        D->info.tile_nnz_cap = 0;
+        D->info.chain_reach = chain_reach(D->h_dep_hi, p_m - 1, nullptr);
+        D->info.max_row_nnz = max_row;
+        D->info.nnz = h_nnz;
+        D->info.grid = ctx->sm_count;
+        D->info.powers_per_item = 1;
+        D->info.slots = 2;
+        ptc.mark("dp_build");
+        const int rc = finish_ring_tiling(ctx, D, p_m, prm, info, out, st);
+        if (rc != LMPK_OK) lmpk_tiling_destroy(D);
+        ptc.mark("finish_ring_tiling");
+        return rc;
+      }
     }
   }
   for (const Cand& cd : cands) {
@@ -1469,6 +1512,39 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
     Pm.smem_cap = T->piece;
     Pm.blk_cap = T->piece;
   }
+  if (sweep && T->lean_vd == 2) {
+    // DP tilings hold lean blocks only: a sweep is one lean launch per power
+    // over the power-1 items (no dependencies), each with an epoch of its own
+    for (int i = 0; i < P; ++i) {
+      PowerCfgDev Ci;
+      memset(&Ci, 0, sizeof(Ci));
+      Ci.out_slot[0] = C.out_slot[i];
+      Ci.in_slot[0] = C.in_slot[i];
+      Ci.prev_slot[0] = C.prev_slot[i];
+      Ci.kernel[0] = C.kernel[i];
+      Ci.coef_re[0] = C.coef_re[i];
+      Ci.coef_im[0] = C.coef_im[i];
+      ctx->epoch += 1;
+      if (ctx->epoch >= (1u << 24)) {
+        ctx->epoch = 1;
+        ctx->wrap_gen += 1;
+      }
+      if (Tm->wrap_gen != ctx->wrap_gen) {
+        LMPK_CHECK_CUDA(cudaMemsetAsync(Tm->d_progress, 0, size_t(T->info.n_tiles) * 4, st));
+        Tm->wrap_gen = ctx->wrap_gen;
+      }
+      Pm.epoch_base = ctx->epoch * kEpochStride;
+      Pm.queue_base = ctx->queue_base;
+      Pm.n_powers = 1;
+      Pm.mode = 1;
+      Pm.items = T->d_items;
+      Pm.q = 1;
+      Pm.n_items = T->n_items;
+      Pm.n_tiles = T->info.n_tiles;
+      LMPK_TRY(launch_lean(ctx, T, Pm, Ci, cplx, exact, use_acc || Ci.kernel[0] != LMPK_KERNEL_SPMV, grid, st));
+    }
+    return LMPK_OK;
+  }
   if (sweep) {
     // n_powers back-to-back, dependency-free passes (one launch per power)
     for (int i = 0; i < P; ++i) {
@@ -1543,8 +1619,8 @@ extern "C" int lmpk_mpk_run(lmpk_ctx* ctx, const lmpk_tiling* T, double* y, int6
       else if (T->info.compressed_tiles == T->info.n_tiles && T->info.dict_tiles == 0)
         uniform = 2;
     }
-    if (T->d_lean && T->staged_tiles == 0 && T->slots == 2 && !getenv("LMPK_NO_LEAN_RUN") &&
-        lean_xs_runnable(T, y, ldy, cplx)) {
+    if (T->d_lean && T->staged_tiles == 0 && T->slots == 2 &&
+        (T->lean_vd == 2 || (!getenv("LMPK_NO_LEAN_RUN") && lean_xs_runnable(T, y, ldy, cplx)))) {
       bool plain = !use_acc;
       for (int i = 0; i < P; ++i) plain = plain && C.kernel[i] == LMPK_KERNEL_SPMV;
       return launch_lean(ctx, T, Pm, C, cplx, exact, !plain, grid, st);

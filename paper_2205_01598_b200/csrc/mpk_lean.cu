@@ -8,6 +8,10 @@ const void* mpk_lean_fn_r_e(bool vd, bool gen, int np, bool xp);
 const void* mpk_lean_fn_r_f(bool vd, bool gen, int np, bool xp);
 const void* mpk_lean_fn_c_e(bool vd, int np, bool xp);
 const void* mpk_lean_fn_c_f(bool vd, int np, bool xp);
+const void* mpk_dp_fn_r_e(bool gen, int np);
+const void* mpk_dp_fn_r_f(bool gen, int np);
+const void* mpk_dp_fn_c_e(int np);
+const void* mpk_dp_fn_c_f(int np);
 const void* mpk_xlean_fn_r_e(bool vd, bool gen, bool xp, int ctas);
 const void* mpk_xlean_fn_r_f(bool vd, bool gen, bool xp, int ctas);
 const void* mpk_xlean_fn_c_e(bool vd, bool xp, int ctas);
@@ -1024,7 +1028,9 @@ int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev&
   int np = (4 * int64_t(piece) + 8192 <= ctx->max_smem_block) ? 4 : 2;
   if (const char* e = getenv("LMPK_LEAN_NP")) np = atoi(e) == 4 && 4 * int64_t(piece) + 8192 <= ctx->max_smem_block ? 4 : 2;
   const void* fn;
-  if (T->lean_xs) {
+  if (T->lean_vd == 2) {  // DP blocks (diagonal-private dictionary)
+    fn = cplx ? (exact ? mpk_dp_fn_c_e(np) : mpk_dp_fn_c_f(np)) : (exact ? mpk_dp_fn_r_e(gen, np) : mpk_dp_fn_r_f(gen, np));
+  } else if (T->lean_xs) {
     np = T->lean_np;
     const bool xp = T->lean_xp != 0;
     fn = cplx ? (exact ? mpk_xlean_fn_c_e(vd, xp, ctas) : mpk_xlean_fn_c_f(vd, xp, ctas))

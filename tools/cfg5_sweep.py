@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2205_01598_b200 as lm
 from paper_2205_01598_b200.cheb import ChebCoeffs, cheb_coeffs_schrodinger, gershgorin_bounds
 KNOBS = ("LMPK_PASS_POWERS", "LMPK_SUPER_NNZ", "LMPK_SLOT_KB", "LMPK_XLEAN", "LMPK_XLEAN_ROWS", "LMPK_SCHEDULE",
-         "LMPK_NO_LEAN", "LMPK_XLEAN_NP", "LMPK_NO_WORKLIST")
+         "LMPK_NO_LEAN", "LMPK_XLEAN_NP", "LMPK_NO_WORKLIST", "LMPK_NO_DP", "LMPK_DP_TILE_KB", "LMPK_DP_PAIR",
+         "LMPK_RING_SLACK", "LMPK_LEAN_NP", "LMPK_LEAN_CARVE")
 n = int(os.environ.get("N", "128"))
 a = lm.gen_anderson_3d(n, seed=2)
 lo, hi = gershgorin_bounds(a)
@@ -37,7 +38,7 @@ for var in os.environ.get("VARIANTS", "LMPK_SCHEDULE=walk|LMPK_SCHEDULE=sweep").
         print(json.dumps({"var": var, "ms": round(min(ts), 3), "gflops": round(flops / (min(ts) * 1e-3) / 1e9),
                           "bitwise": bool(torch.equal(y, ref)), "tiles": i.get("n_tiles"), "super": i.get("super_tiles"),
                           "block_MB": round(i.get("block_bytes", 0) / 1e6, 1), "lean_MB": round(i.get("lean_bytes", 0) / 1e6, 1),
-                          "xs": i.get("lean_xstaged"), "np": i.get("lean_ring"), "piece": i.get("lean_piece"),
+                          "dp": i.get("dp_tiles"), "slack": i.get("queue_slack"), "D": i.get("max_fwd_reach"), "xs": i.get("lean_xstaged"), "np": i.get("lean_ring"), "piece": i.get("lean_piece"),
                           "sched": prop._plan_for[8].schedule_choice(True, False)}), flush=True)
         del prop
     except Exception as e:
