@@ -551,6 +551,26 @@ def run_ours(args, cfgd):
         line["config"].update({"tiles": til.info["n_tiles"], "lean_bytes": til.info["lean_bytes"],
                                "block_bytes": til.info["block_bytes"], "super_tiles": til.info["super_tiles"]})
     # ---------------- k x SpMV comparators and parity of the timed result
+    if cfgd["kind"] == "cheb":
+        # the same step as degree x SpMV: (a) sweeps over the CRS arrays of the
+        # natural-order operator with the recurrence fused into the row store
+        # (lmpk_mpk_crs_run: the "k back-to-back SpMVs" of the paper), (b)
+        # per-power sweeps over the tiles of the natural-order operator
+        y_walk = prop.step(xd)
+        base = lm.ChebPropagator(a, coeffs.dt, coeffs=coeffs, p_m_batch=k, variant="baseline")
+        base.check_errors = False
+        t_tiled = _event_time(lambda: base.step(xd))
+        base.force_crs = True
+        y_crs = base.step(xd)
+        t_crs = _event_time(lambda: base.step(xd))
+        rel = float((y_crs - y_walk).abs().max() / y_walk.abs().max())
+        line["kspmv_baseline"] = {
+            "crs_ms": t_crs * 1e3, "tiled_sweep_ms": t_tiled * 1e3,
+            "crs_roofline_frac": coeffs.n_moments * (12 * nnz + 4 * (n + 1) + 16 * n * 5) / t_crs / 1e9 / peak,
+            "speedup_vs_crs": t_crs / t_kernel, "speedup_vs_best": min(t_crs, t_tiled) / t_kernel,
+            "rel_diff_vs_walk": rel,
+            "note": "natural order; per power 12 nnz + 4(N+1) + 16N*5 bytes (in, prev, out, acc read+write)"}
+        del base
     if cfgd["kind"] == "mpk":
         yb = torch.zeros_like(y)
         yb[0] = y[0]
