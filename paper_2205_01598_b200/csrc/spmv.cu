@@ -47,6 +47,127 @@ __global__ void k_heavy_rows(const int32_t* __restrict__ row_ptr, int32_t r0, in
   }
 }
 
+// A HUGE row (> kHuge entries) takes a whole CTA: warps 1..7 load col/val,
+// gather x and write the products (each the same rounded double as the
+// sequential kernel's) into a shared-memory ring of stages of 896 entries;
+// lane 0 of warp 0 only adds them, in storage order from +0.0, next group's
+// products already in registers -- the dependent DADD chain never waits for
+// anything else, so the row costs its entries x the DADD latency (cfg4's
+// 97,280-entry hub: ~0.45 ms, the floor of a bit-exact sum; one warp doing
+// both jobs in turns took 0.8 ms and set the time of the whole sweep).
+constexpr int kHugeWarps = 7;
+constexpr int kHugeStage = kHugeWarps * 128;
+template <bool CPLX>
+struct HugeRing {
+  static constexpr int kStages = CPLX ? 2 : 4;
+  static constexpr int kDoubles = kStages * kHugeStage * (CPLX ? 2 : 1);
+};
+template <bool CPLX>
+__device__ __forceinline__ void huge_row_sum(const int32_t* __restrict__ col, const double* __restrict__ val,
+                                             const double* __restrict__ x, int32_t a, int32_t b, double* ring,
+                                             uint64_t* full, uint64_t* empty, double& tr, double& ti) {
+  constexpr int NS = HugeRing<CPLX>::kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 32 * kHugeWarps);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int32_t nst = (b - a + kHugeStage - 1) / kHugeStage;
+  tr = 0.0, ti = 0.0;
+  if (warp > 0) {
+    const int32_t wofs = (warp - 1) * 128 + lane;
+    for (int32_t s = 0; s < nst; ++s) {
+      int32_t c[4];
+      double v[4], mr[4], mi[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int32_t e = a + s * kHugeStage + wofs + q * 32;
+        c[q] = e < b ? __ldg(col + e) : -1;
+        v[q] = e < b ? __ldg(val + e) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if constexpr (CPLX) {
+          const double2 xx = c[q] >= 0 ? __ldg(reinterpret_cast<const double2*>(x) + c[q]) : make_double2(0.0, 0.0);
+          mr[q] = __dmul_rn(v[q], xx.x);
+          mi[q] = __dmul_rn(v[q], xx.y);
+        } else {
+          mr[q] = __dmul_rn(v[q], c[q] >= 0 ? __ldg(x + c[q]) : 0.0);
+          mi[q] = 0.0;
+        }
+      }
+      const int slot = s % NS;
+      if (s >= NS) mbar_wait(&empty[slot], uint32_t(s / NS - 1) & 1u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if constexpr (CPLX)
+          reinterpret_cast<double2*>(ring)[slot * kHugeStage + wofs + q * 32] = make_double2(mr[q], mi[q]);
+        else
+          ring[slot * kHugeStage + wofs + q * 32] = mr[q];
+      }
+      mbar_arrive(&full[slot]);
+    }
+  } else if (lane == 0) {
+    for (int32_t s = 0; s < nst; ++s) {
+      const int slot = s % NS;
+      mbar_wait(&full[slot], uint32_t(s / NS) & 1u);
+      const int32_t cnt = min(kHugeStage, b - a - s * kHugeStage);
+      // Blocks of 32 products (complex: 16), written out as four groups over
+      // two register buffers: each group's shared-memory loads are issued one
+      // group ahead of its adds, the first group of the next block (index
+      // clamped to the stage) during the last group.  The block loop is not
+      // unrolled by the compiler and has no conditional loads: an earlier
+      // form with a conditional prefetch inside an unrollable loop was
+      // miscompiled (one group of an unrolled remainder was dropped).
+      constexpr int kPer = CPLX ? 16 : 32;  // entries per block = 16 double2 loads
+      const double2* b2 = CPLX ? reinterpret_cast<const double2*>(ring) + slot * kHugeStage
+                               : reinterpret_cast<const double2*>(ring + slot * kHugeStage);
+      auto ld4 = [&](double2(&P)[4], int32_t i) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) P[j] = b2[i + j];
+      };
+      auto add4 = [&](const double2(&P)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if constexpr (CPLX) {
+            tr = __dadd_rn(tr, P[j].x);
+            ti = __dadd_rn(ti, P[j].y);
+          } else {
+            tr = __dadd_rn(tr, P[j].x);
+            tr = __dadd_rn(tr, P[j].y);
+          }
+        }
+      };
+      const int32_t nblk = cnt / kPer;
+      double2 A[4], B[4];
+      ld4(A, 0);
+#pragma unroll 1
+      for (int32_t blk = 0; blk < nblk; ++blk) {
+        const int32_t i0 = 16 * blk;
+        const int32_t inext = 16 * min(blk + 1, kHugeStage / kPer - 1);
+        ld4(B, i0 + 4);
+        add4(A);
+        ld4(A, i0 + 8);
+        add4(B);
+        ld4(B, i0 + 12);
+        add4(A);
+        ld4(A, inext);
+        add4(B);
+      }
+      if constexpr (CPLX) {
+        for (int32_t k = kPer * nblk; k < cnt; ++k) tr = __dadd_rn(tr, b2[k].x), ti = __dadd_rn(ti, b2[k].y);
+      } else {
+        for (int32_t k = kPer * nblk; k < cnt; ++k) tr = __dadd_rn(tr, ring[slot * kHugeStage + k]);
+      }
+      mbar_arrive(&empty[slot]);
+    }
+  }
+}
+
 // One sweep over [r0, r1).  CTAs [0, hb): one WARP per heavy row, software
 // pipelined in stages of 128 entries -- the lanes load col/val (coalesced) two
 // stages ahead and gather x one stage ahead, form the stage's products (each
@@ -61,12 +182,25 @@ __global__ void __launch_bounds__(256) spmv_rows_heavy_kernel(const int32_t* __r
                                                               const double* __restrict__ val,
                                                               const double* __restrict__ x,
                                                               double* __restrict__ out, int32_t r0, int32_t r1,
-                                                              const int32_t* __restrict__ list, int32_t hb) {
-  if (int32_t(blockIdx.x) < hb) {
-    __shared__ __align__(16) double buf[8][2][kHStage];
+                                                              const int32_t* __restrict__ list, int32_t ha,
+                                                              int32_t hb) {
+  // CTAs [0, ha): one huge row each; [ha, ha + hb): 8 heavy rows each; the rest: light rows
+  __shared__ __align__(16) double smem_d[HugeRing<false>::kDoubles];
+  __shared__ uint64_t bars[2 * HugeRing<false>::kStages];
+  static_assert(HugeRing<false>::kDoubles >= 8 * 2 * kHStage, "heavy-row buffers share the ring's memory");
+  if (int32_t(blockIdx.x) < ha) {
+    const int32_t r = __ldg(list + 2 + int32_t(blockIdx.x));
+    double tr, ti;
+    huge_row_sum<false>(col, val, x, __ldg(row_ptr + r), __ldg(row_ptr + r + 1), smem_d, bars,
+                        bars + HugeRing<false>::kStages, tr, ti);
+    if (threadIdx.x == 0) out[r] = tr;
+    return;
+  }
+  if (int32_t(blockIdx.x) < ha + hb) {
+    double(*buf)[2][kHStage] = reinterpret_cast<double(*)[2][kHStage]>(smem_d);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int32_t i = int32_t(blockIdx.x) * 8 + warp;
     const int32_t na = __ldg(list), nb = __ldg(list + 1);
+    const int32_t i = na + (int32_t(blockIdx.x) - ha) * 8 + warp;
     if (i >= na + nb) return;
     const int32_t r = i < na ? __ldg(list + 2 + i) : __ldg(list + 2 + (r1 - r0) - 1 - (i - na));
     const int32_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
@@ -124,8 +258,8 @@ __global__ void __launch_bounds__(256) spmv_rows_heavy_kernel(const int32_t* __r
     if (lane == 0) out[r] = t;
     return;
   }
-  const int64_t stride = int64_t(gridDim.x - hb) * blockDim.x;
-  for (int64_t r = r0 + int64_t(blockIdx.x - hb) * blockDim.x + threadIdx.x; r < r1; r += stride) {
+  const int64_t stride = int64_t(gridDim.x - ha - hb) * blockDim.x;
+  for (int64_t r = r0 + int64_t(blockIdx.x - ha - hb) * blockDim.x + threadIdx.x; r < r1; r += stride) {
     const int32_t k0 = __ldg(row_ptr + r), k1 = __ldg(row_ptr + r + 1);
     if (k1 - k0 <= kHeavy)
       out[r] = row_sum_exact(col + k0, val + k0, k1 - k0, [x](int c) { return __ldg(x + c); });
@@ -134,7 +268,7 @@ __global__ void __launch_bounds__(256) spmv_rows_heavy_kernel(const int32_t* __r
 
 static int spmv_launch(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col, const double* val,
                        const double* x, double* out, int32_t r0, int32_t r1, const int32_t* heavy,
-                       int32_t n_heavy, cudaStream_t st) {
+                       int32_t n_huge, int32_t n_heavy, cudaStream_t st) {
   if (r1 <= r0) return LMPK_OK;
   const int threads = 256;
   const int64_t blocks = (int64_t(r1) - r0 + threads - 1) / threads;
@@ -143,8 +277,9 @@ static int spmv_launch(lmpk_ctx* ctx, const int32_t* row_ptr, const int32_t* col
   if (n_heavy == 0) {  // no hub rows
     spmv_rows_kernel<<<grid, threads, 0, st>>>(row_ptr, col, val, x, out, r0, r1);
   } else {
-    const int hb = (n_heavy + 7) / 8;
-    spmv_rows_heavy_kernel<<<hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, r0, r1, heavy, hb);
+    const int hb = (n_heavy - n_huge + 7) / 8;
+    spmv_rows_heavy_kernel<<<n_huge + hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, r0, r1, heavy, n_huge,
+                                                                   hb);
   }
   launch_count_add(ctx, 1);
   LMPK_CHECK_CUDA(cudaGetLastError());
@@ -214,13 +349,26 @@ __global__ void __launch_bounds__(256) sweep_rows_kernel(const int32_t* __restri
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ x, double* __restrict__ out,
                                                          SweepEpi E, int32_t n, const int32_t* __restrict__ list,
-                                                         int32_t hb) {
-  if (int32_t(blockIdx.x) < hb) {
+                                                         int32_t ha, int32_t hb) {
+  constexpr int kHW = kHStage * (CPLX ? 2 : 1);
+  constexpr int kSm = HugeRing<CPLX>::kDoubles > 8 * 2 * kHW ? HugeRing<CPLX>::kDoubles : 8 * 2 * kHW;
+  __shared__ __align__(16) double smem_d[kSm];
+  __shared__ uint64_t bars[2 * HugeRing<CPLX>::kStages];
+  if (int32_t(blockIdx.x) < ha) {
+    // one CTA per huge row (huge_row_sum above)
+    const int32_t r = __ldg(list + 2 + int32_t(blockIdx.x));
+    double tr, ti;
+    huge_row_sum<CPLX>(col, val, x, __ldg(row_ptr + r), __ldg(row_ptr + r + 1), smem_d, bars,
+                       bars + HugeRing<CPLX>::kStages, tr, ti);
+    if (threadIdx.x == 0) sweep_store<CPLX>(out, E, r, tr, ti);
+    return;
+  }
+  if (int32_t(blockIdx.x) < ha + hb) {
     // one warp per heavy row, pipelined as in spmv_rows_heavy_kernel
-    __shared__ __align__(16) double buf[8][2][kHStage * (CPLX ? 2 : 1)];
+    double(*buf)[2][kHW] = reinterpret_cast<double(*)[2][kHW]>(smem_d);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int32_t i = int32_t(blockIdx.x) * 8 + warp;
     const int32_t na = __ldg(list), nb = __ldg(list + 1);
+    const int32_t i = na + (int32_t(blockIdx.x) - ha) * 8 + warp;
     if (i >= na + nb) return;
     const int32_t r = i < na ? __ldg(list + 2 + i) : __ldg(list + 2 + n - 1 - (i - na));
     const int32_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
@@ -294,8 +442,8 @@ __global__ void __launch_bounds__(256) sweep_rows_kernel(const int32_t* __restri
 #undef LMPK_SWEEP_GATHER
     return;
   }
-  const int64_t stride = int64_t(gridDim.x - hb) * blockDim.x;
-  for (int64_t r = int64_t(blockIdx.x - hb) * blockDim.x + threadIdx.x; r < n; r += stride) {
+  const int64_t stride = int64_t(gridDim.x - ha - hb) * blockDim.x;
+  for (int64_t r = int64_t(blockIdx.x - ha - hb) * blockDim.x + threadIdx.x; r < n; r += stride) {
     const int32_t k0 = __ldg(row_ptr + r), k1 = __ldg(row_ptr + r + 1);
     if (k1 - k0 > kHeavy) continue;
     if constexpr (CPLX) {
@@ -310,7 +458,7 @@ __global__ void __launch_bounds__(256) sweep_rows_kernel(const int32_t* __restri
 
 // heavy-row list of [r0, r1) in the ctx scratch (two counts, then cap slots)
 static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t r1, int32_t** out,
-                      int32_t* n_heavy, cudaStream_t st) {
+                      int32_t* n_huge, int32_t* n_heavy, cudaStream_t st) {
   // the list is shared ctx scratch: a call on another stream may still be
   // reading it -- order this call (and any reallocation) after that reader
   if (!ctx->heavy_ev) LMPK_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->heavy_ev, cudaEventDisableTiming));
@@ -328,6 +476,7 @@ static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t
   int32_t head[2] = {0, 0};
   LMPK_CHECK_CUDA(cudaMemcpyAsync(head, list, 8, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));  // once per call: decides the heavy-row launch
+  *n_huge = head[0];
   *n_heavy = head[0] + head[1];
   *out = list;
   return LMPK_OK;
@@ -348,9 +497,9 @@ extern "C" int lmpk_spmv_rows(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, 
   if (r1 == r0) return LMPK_OK;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
-  int32_t n_heavy = 0;
-  LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, &n_heavy, st));
-  LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, n_heavy, st));
+  int32_t n_heavy = 0, n_huge = 0;
+  LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, &n_huge, &n_heavy, st));
+  LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, n_huge, n_heavy, st));
   LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
   return LMPK_OK;
 }
@@ -365,11 +514,11 @@ extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_pt
   (void)flags;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
-  int32_t n_heavy = 0;
-  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_heavy, st));
+  int32_t n_heavy = 0, n_huge = 0;
+  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_huge, &n_heavy, st));
   for (int32_t p = 1; p <= p_m; ++p)
     LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy,
-                         n_heavy, st));
+                         n_huge, n_heavy, st));
   LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
   return LMPK_OK;
 }
@@ -389,12 +538,12 @@ extern "C" int lmpk_mpk_crs_run(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr
   if (n == 0) return LMPK_OK;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
-  int32_t n_heavy = 0;
-  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_heavy, st));
+  int32_t n_heavy = 0, n_huge = 0;
+  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_huge, &n_heavy, st));
   const int threads = 256;
   const int64_t blocks = (int64_t(n) + threads - 1) / threads;
   const int grid = static_cast<int>(std::min<int64_t>(blocks, int64_t(ctx->sm_count) * 8));
-  const int hb = (n_heavy + 7) / 8;
+  const int ha = n_huge, hb = (n_heavy - n_huge + 7) / 8;
   for (int32_t i = 0; i < cfg->n_powers; ++i) {
     const int32_t so = cfg->out_slot[i], si = cfg->in_slot[i], sp = cfg->prev_slot[i];
     LMPK_ARG_CHECK(so >= 0 && so < n_slots && si >= 0 && si < n_slots && so != si, "bad slots at power %d", i + 1);
@@ -405,9 +554,9 @@ extern "C" int lmpk_mpk_crs_run(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr
     const double* x = y + int64_t(si) * ldy;
     double* out = y + int64_t(so) * ldy;
     if (cplx)
-      sweep_rows_kernel<true><<<hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, E, n, heavy, hb);
+      sweep_rows_kernel<true><<<ha + hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, E, n, heavy, ha, hb);
     else
-      sweep_rows_kernel<false><<<hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, E, n, heavy, hb);
+      sweep_rows_kernel<false><<<ha + hb + grid, threads, 0, st>>>(row_ptr, col, val, x, out, E, n, heavy, ha, hb);
     launch_count_add(ctx, 1);
   }
   LMPK_CHECK_CUDA(cudaGetLastError());
