@@ -1029,6 +1029,9 @@ int launch_lean(lmpk_ctx* ctx, const lmpk_tiling* T, MpkParams& Pm, PowerCfgDev&
   if (const char* e = getenv("LMPK_LEAN_NP")) np = atoi(e) == 4 && 4 * int64_t(piece) + 8192 <= ctx->max_smem_block ? 4 : 2;
   const void* fn;
   if (T->lean_vd == 2) {  // DP blocks (diagonal-private dictionary)
+    // pieces beyond 32 KB run a ring of 2: four would leave the gathers no L1
+    // (cfg5, 48 KB pieces: 2.40 vs 2.59 ms per step)
+    if (piece > 32 * 1024 && getenv("LMPK_LEAN_NP") == nullptr) np = 2;
     fn = cplx ? (exact ? mpk_dp_fn_c_e(np) : mpk_dp_fn_c_f(np)) : (exact ? mpk_dp_fn_r_e(gen, np) : mpk_dp_fn_r_f(gen, np));
   } else if (T->lean_xs) {
     np = T->lean_np;

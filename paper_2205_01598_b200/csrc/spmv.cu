@@ -47,6 +47,28 @@ __global__ void k_heavy_rows(const int32_t* __restrict__ row_ptr, int32_t r0, in
   }
 }
 
+// Longest huge rows first (their CTAs are scheduled in list order and the
+// longest row's add chain is the critical path of the sweep): rank sort of the
+// na huge rows by (length descending, row ascending) by one CTA, through the
+// free slots between the two ends of the list.
+__global__ void __launch_bounds__(1024) k_sort_huge(const int32_t* __restrict__ row_ptr, int32_t* list, int32_t na) {
+  int32_t* rows = list + 2;
+  int32_t* tmp = rows + na;
+  for (int32_t i = threadIdx.x; i < na; i += blockDim.x) {
+    const int32_t r = rows[i];
+    const int32_t len = __ldg(row_ptr + r + 1) - __ldg(row_ptr + r);
+    int32_t rank = 0;
+    for (int32_t j = 0; j < na; ++j) {
+      const int32_t q = rows[j];
+      const int32_t lq = __ldg(row_ptr + q + 1) - __ldg(row_ptr + q);
+      rank += (lq > len) || (lq == len && q < r);
+    }
+    tmp[rank] = r;
+  }
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < na; i += blockDim.x) rows[i] = tmp[i];
+}
+
 // A HUGE row (> kHuge entries) takes a whole CTA: warps 1..7 load col/val,
 // gather x and write the products (each the same rounded double as the
 // sequential kernel's) into a shared-memory ring of stages of 896 entries;
@@ -478,6 +500,11 @@ static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));  // once per call: decides the heavy-row launch
   *n_huge = head[0];
   *n_heavy = head[0] + head[1];
+  if (head[0] > 1 && int64_t(r1 - r0) - head[0] - head[1] >= head[0]) {
+    k_sort_huge<<<1, 1024, 0, st>>>(row_ptr, list, head[0]);
+    LMPK_CHECK_CUDA(cudaGetLastError());
+    launch_count_add(ctx, 1);
+  }
   *out = list;
   return LMPK_OK;
 }
