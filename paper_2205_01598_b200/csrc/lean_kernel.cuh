@@ -44,6 +44,7 @@ constexpr int kLeanHdr = 16;          // [nu, nrows, flags, 0]
 constexpr int kLeanDict = 16;         // dictionary byte offset in the block
 constexpr int kLeanRec = 16 + 256;    // first unit record
 constexpr uint32_t kLeanPair = 1u << 8, kLeanPadded = 1u << 9, kLeanPattern = 1u << 10;
+constexpr uint32_t kLeanSameVal = 1u << 11;  // pattern pair whose slices share one row of dictionary values
 
 __host__ __device__ constexpr int lean_wc(int w) { return w <= 0 ? 0 : (w <= 4 ? 4 : 8); }
 // bytes of one slice's column offsets / dictionary codes / raw values
@@ -236,7 +237,7 @@ __device__ __forceinline__ LeanSum<CPLX> lean_slice(uint32_t cp, uint32_t vp, ui
 }
 
 // Two slices of the same width: every gather of both in flight at once.
-template <int W, bool CPLX, bool EXACT, bool VD, bool XS = false>
+template <int W, bool CPLX, bool EXACT, bool VD, bool XS = false, bool SV = false>
 __device__ __forceinline__ void lean_pair(uint32_t cp0, uint32_t vp0, uint32_t cp1, uint32_t vp1, uint32_t dict,
                                           uint32_t lane, typename LeanRp<XS>::T rp0, typename LeanRp<XS>::T rp1,
                                           LeanSum<CPLX>& s0, LeanSum<CPLX>& s1) {
@@ -251,21 +252,28 @@ __device__ __forceinline__ void lean_pair(uint32_t cp0, uint32_t vp0, uint32_t c
     for (int j = 0; j < W; ++j) x0[j] = lean_gather<CPLX, XS>(rp0, c0[j]);
 #pragma unroll
     for (int j = 0; j < W; ++j) x1[j] = lean_gather<CPLX, XS>(rp1, c1[j]);
-    {
+    if constexpr (SV) {  // kLeanSameVal: one row of dictionary values for both slices
       double v[W];
-      if constexpr (VD)
-        lean_dvals<W>(vp0, dict, v);
-      else
-        lean_raw<W>(vp0, lane, v);
+      lean_dvals<W>(vp0, dict, v);
       s0 = lean_chain<W, CPLX, EXACT>(v, x0);
-    }
-    {
-      double v[W];
-      if constexpr (VD)
-        lean_dvals<W>(vp1, dict, v);
-      else
-        lean_raw<W>(vp1, lane, v);
       s1 = lean_chain<W, CPLX, EXACT>(v, x1);
+    } else {
+      {
+        double v[W];
+        if constexpr (VD)
+          lean_dvals<W>(vp0, dict, v);
+        else
+          lean_raw<W>(vp0, lane, v);
+        s0 = lean_chain<W, CPLX, EXACT>(v, x0);
+      }
+      {
+        double v[W];
+        if constexpr (VD)
+          lean_dvals<W>(vp1, dict, v);
+        else
+          lean_raw<W>(vp1, lane, v);
+        s1 = lean_chain<W, CPLX, EXACT>(v, x1);
+      }
     }
   }
 }
@@ -462,7 +470,10 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
       vp1 = vp0 + (VD ? lean_code_bytes(W) : lean_raw_bytes(W));
     }
     LeanSum<CPLX> a, b;
-    lean_pair<W, CPLX, EXACT, VD, XS>(cp0, vp0, cp1, vp1, dict, lane, rp0, rp1, a, b);
+    if (VD && !CPLX && (rec.z & kLeanSameVal))
+      lean_pair<W, CPLX, EXACT, VD, XS, VD && !CPLX>(cp0, vp0, cp1, vp1, dict, lane, rp0, rp1, a, b);
+    else
+      lean_pair<W, CPLX, EXACT, VD, XS>(cp0, vp0, cp1, vp1, dict, lane, rp0, rp1, a, b);
     if (padded) {
       if (lean_nan(a.r) || (CPLX && lean_nan(a.i)))
         if (l0 < nrows) a = lean_row_exact<CPLX, EXACT, VD, XS>(cp0, vp0, dict, lane, rp0, W, rowlen[r0 + l0]);

@@ -369,14 +369,18 @@ __global__ void k_xp_head(int32_t nt, const int32_t* tile_row, const int64_t* le
 }
 
 // pass 1 (dictionary tilings): pattern count of every slice
+// (natural slice order: slice i of tile slice_tile[i]); sig_out[i] = the
+// slice's dictionary indices (5 bits per entry) when it holds one pattern
 __global__ void k_lean_patterns(const int32_t* row_ptr, const int32_t* col, const double* val, int32_t n_desc,
-                                const LeanSliceDesc* desc, const int32_t* width, const int32_t* tile_row,
+                                const int32_t* slice_tile, const int32_t* width, const int32_t* tile_row,
                                 const int32_t* tile_dict, const int32_t* tile_nd, const uint64_t* dict_tab,
-                                int32_t* np_out, const int4* runs, const int2* xinfo) {
+                                int32_t* np_out, uint64_t* sig_out, const int4* runs, const int2* xinfo) {
   const int32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= n_desc) return;
-  const LeanSliceDesc d = desc[i];
+  LeanSliceDesc d{};
+  d.s = i;
+  d.t = slice_tile[i];
   const int w = width[d.s];
   int32_t off[8];
   uint32_t code[8];
@@ -385,7 +389,12 @@ __global__ void k_lean_patterns(const int32_t* row_ptr, const int32_t* col, cons
                                dict_tab + int64_t(tile_dict[d.t]) * kDictMax, tile_nd[d.t], true, off, code, v,
                                runs ? runs + int64_t(d.t) * kLeanMaxRuns : nullptr, runs ? xinfo[d.t].x : 0);
   const int2 pp = lean_pattern_ids(off, code, len, lane);
-  if (lane == 0) np_out[i] = pp.y;
+  if (lane == 0) {
+    np_out[i] = pp.y;
+    uint64_t sig = 0;
+    for (int j = 0; j < 8; ++j) sig |= uint64_t(code[j] >> 3) << (5 * j);
+    sig_out[i] = sig;
+  }
 }
 
 // one warp per sorted slice: plain lean slices -- lane-contiguous offsets
@@ -725,16 +734,24 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   }
   // pass 1: pattern counts per slice (natural slice order)
   std::vector<int32_t> np(S, 32);
+  std::vector<uint64_t> sig(S, 0);  // dictionary indices of one-pattern slices (same-value pairs)
+  const bool no_sameval = getenv("LMPK_NO_SAMEVAL") != nullptr;  // A/B switch (tools/lean_ab.py)
   if (try_pat) {
-    std::vector<LeanSliceDesc> nat(S);
-    for (int32_t s = 0; s < S; ++s) nat[s] = LeanSliceDesc{s, slice_tile[s], 0, 0, 0, 0, 0, 0};
+    int32_t* d_st = nullptr;
+    uint64_t* d_sig = nullptr;
     LMPK_TRY(lmalloc(&d_np, S));
-    LMPK_CHECK_CUDA(cudaMemcpyAsync(d_desc, nat.data(), size_t(S) * sizeof(LeanSliceDesc), cudaMemcpyHostToDevice, st));
-    k_lean_patterns<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_desc, d_width,
-                                                                  T->d_tile_row, d_tdict, d_nd, d_dict_tab, d_np,
+    LMPK_TRY(lmalloc(&d_st, S));
+    LMPK_TRY(lmalloc(&d_sig, S));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(d_st, slice_tile.data(), size_t(S) * 4, cudaMemcpyHostToDevice, st));
+    k_lean_patterns<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_st, d_width,
+                                                                  T->d_tile_row, d_tdict, d_nd, d_dict_tab, d_np, d_sig,
                                                                   d_runs, d_xinfo);
     launch_count_add(ctx, 1);
     LMPK_CHECK_CUDA(cudaMemcpyAsync(np.data(), d_np, size_t(S) * 4, cudaMemcpyDeviceToHost, st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(sig.data(), d_sig, size_t(S) * 8, cudaMemcpyDeviceToHost, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_st);
+    cudaFree(d_sig);
   }
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   pt.mark("  lean: plan + pattern pass");
@@ -824,8 +841,11 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
       r.x = uint32_t(c_of[i]);
       r.y = pat ? uint32_t(pair ? c_of[i + 1] : 0) : uint32_t(v_of[i]);
       r.z = uint32_t(w) | (pair ? kLeanPair : 0u) | (padded ? kLeanPadded : 0u);
-      if (pat && w > 0)
+      if (pat && w > 0) {
         r.z |= kLeanPattern | (uint32_t(np[sa]) << 16) | (uint32_t(pair ? np[sb] : 0) << 24);
+        // both slices one pattern with the same dictionary indices: the values are read once
+        if (pair && np[sa] == 1 && np[sb] == 1 && sig[sa] == sig[sb] && !no_sameval) r.z |= kLeanSameVal;
+      }
       r.w = uint32_t(sa - s0) | (uint32_t(sb - s0) << 16);
       recs.push_back(r);
       i += pair ? 2 : 1;
