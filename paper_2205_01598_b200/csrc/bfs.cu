@@ -35,21 +35,27 @@ namespace lmpk {
 constexpr int kBfsThreads = 512;
 
 // Grid barrier of the cooperative BFS kernel: one arrival counter that only
-// grows (zeroed before the launch); barrier number e completes when it reaches
-// e * nblocks.  One atomic per CTA and a spin on the same word -- no reset, no
-// generation word, no sleep: ~598 of these are cfg2's whole level loop.
+// grows (zeroed before the launch); a barrier completes when it reaches the
+// running sum of the arrivals expected so far.  One atomic per arriving CTA
+// and a spin on the same word -- no reset, no generation word, no sleep: ~598
+// of these are cfg2's whole level loop.
 struct GridBar {
   unsigned int count;
   unsigned int pad;
 };
 
-__device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned int nblocks, unsigned int& epoch) {
+// Only the `active` CTAs of a level arrive (the others did no work and just
+// wait): `target` accumulates the active counts, which every CTA derives from
+// the same frontier size.  A narrow frontier (cfg2: ~30K vertices = 59 CTAs of
+// 512 vertices) then costs 59 serialised atomics on the word instead of 296.
+__device__ __forceinline__ void grid_barrier(GridBar* gb, unsigned int active, bool arrive, unsigned int& target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    ++epoch;
-    __threadfence();
-    atomicAdd(&gb->count, 1u);
-    const unsigned int target = epoch * nblocks;
+    target += active;
+    if (arrive) {
+      __threadfence();
+      atomicAdd(&gb->count, 1u);
+    }
     volatile unsigned int* vc = &gb->count;
     while (*vc < target) {
     }
@@ -150,10 +156,10 @@ struct BfsState {
 template <typename RP>
 __device__ void bfs_expand(const RP* row_ptr, const int32_t* col, const BfsState& S,
                            const int32_t* q_in, uint32_t n_in, int32_t* q_out, uint32_t* out_size,
-                           int32_t lev) {
+                           int32_t lev, uint32_t n_ctas) {
   const int lane = threadIdx.x & 31;
   const int64_t warp_global = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t n_warps = (int64_t(n_ctas) * blockDim.x) >> 5;
   for (int64_t base = warp_global * 32; base < n_in; base += n_warps * 32) {
     const int64_t qi = base + lane;
     int64_t start = 0, deg = 0;
@@ -171,29 +177,49 @@ __device__ void bfs_expand(const RP* row_ptr, const int32_t* col, const BfsState
     }
     const int64_t total = __shfl_sync(0xffffffffu, inc, 31);
     const int64_t excl = inc - deg;
-    for (int64_t e0 = 0; e0 < total; e0 += 32) {
-      const int64_t e = e0 + lane;
-      const bool act = e < total;
-      const int64_t ee = act ? e : total - 1;
-      // owner = largest lane whose exclusive degree prefix is <= ee
-      int owner = 0;
+    // four edges per lane and round: the four column loads, then the four
+    // dist reads, then the CAS of the unvisited ones are each issued together,
+    // so a round costs one chain of dependent L2 round trips instead of four
+    // (cfg2's ~30K-vertex frontiers are ~3 rounds of 32 edges per lane)
+    for (int64_t e0 = 0; e0 < total; e0 += 128) {
+      int32_t v[4];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int cand = owner + step;
-        const int64_t ex_c = __shfl_sync(0xffffffffu, excl, cand & 31);
-        if (cand < 32 && ex_c <= ee) owner = cand;
+      for (int j = 0; j < 4; ++j) {
+        const int64_t e = e0 + 32 * j + lane;
+        const bool act = e < total;
+        const int64_t ee = act ? e : total - 1;
+        // owner = largest lane whose exclusive degree prefix is <= ee
+        int owner = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int cand = owner + step;
+          const int64_t ex_c = __shfl_sync(0xffffffffu, excl, cand & 31);
+          if (cand < 32 && ex_c <= ee) owner = cand;
+        }
+        const int64_t st_o = __shfl_sync(0xffffffffu, start, owner);
+        const int64_t ex_o = __shfl_sync(0xffffffffu, excl, owner);
+        v[j] = act ? col[st_o + (ee - ex_o)] : -1;
       }
-      const int64_t st_o = __shfl_sync(0xffffffffu, start, owner);
-      const int64_t ex_o = __shfl_sync(0xffffffffu, excl, owner);
-      const int32_t v = act ? col[st_o + (ee - ex_o)] : -1;
-      bool push = false;
-      if (v >= 0 && S.dist[v] == -1) push = (atomicCAS(S.dist + v, -1, lev + 1) == -1);
-      const uint32_t m = __ballot_sync(0xffffffffu, push);
-      if (m) {
+      bool push[4];
+bool fresh[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fresh[j] = v[j] >= 0 && S.dist[v[j]] == -1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) push[j] = fresh[j] && atomicCAS(S.dist + v[j], -1, lev + 1) == -1;
+      uint32_t m[4], cntj[4], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        m[j] = __ballot_sync(0xffffffffu, push[j]);
+        cntj[j] = tot;
+        tot += uint32_t(__popc(m[j]));
+      }
+      if (tot) {
         uint32_t off = 0;
-        if (lane == 0) off = atomicAdd(out_size, uint32_t(__popc(m)));
+        if (lane == 0) off = atomicAdd(out_size, tot);
         off = __shfl_sync(0xffffffffu, off, 0);
-        if (push) q_out[off + __popc(m & ((1u << lane) - 1u))] = v;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (push[j]) q_out[off + cntj[j] + __popc(m[j] & ((1u << lane) - 1u))] = v[j];
       }
     }
   }
@@ -209,7 +235,7 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs(const RP* row_ptr, const in
   int32_t* qin = S.qa;
   int32_t* qout = S.qb;
   uint32_t* cnt = S.sizes + 4;
-  unsigned int epoch = 0;
+  unsigned int target = 0;
   while (true) {
     const uint32_t n_in = *((volatile uint32_t*)(lev == 0 ? S.sizes : cnt + lev % 3));
     if (n_in == 0) break;
@@ -217,8 +243,11 @@ __global__ void __launch_bounds__(kBfsThreads) k_bfs(const RP* row_ptr, const in
       if (lev > 0) S.sizes[2] = uint32_t(lev);
       cnt[(lev + 2) % 3] = 0;
     }
-    bfs_expand(row_ptr, col, S, qin, n_in, qout, cnt + (lev + 1) % 3, lev);
-    grid_barrier(S.bar, gridDim.x, epoch);
+    // one CTA per 512 frontier vertices (32 per warp), at most the grid
+    const uint32_t active = min(gridDim.x, max(1u, (n_in + kBfsThreads - 1) / kBfsThreads));
+    const bool mine = blockIdx.x < active;
+    if (mine) bfs_expand(row_ptr, col, S, qin, n_in, qout, cnt + (lev + 1) % 3, lev, active);
+    grid_barrier(S.bar, active, mine, target);
     int32_t* t = qin;
     qin = qout;
     qout = t;
