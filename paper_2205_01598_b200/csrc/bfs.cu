@@ -33,6 +33,7 @@
 namespace lmpk {
 
 constexpr int kBfsThreads = 512;
+constexpr int kBfsBatch = 8;  // edges per lane and round of the frontier expansion
 
 // Grid barrier of the cooperative BFS kernel: one arrival counter that only
 // grows (zeroed before the launch); a barrier completes when it reaches the
@@ -177,14 +178,14 @@ __device__ void bfs_expand(const RP* row_ptr, const int32_t* col, const BfsState
     }
     const int64_t total = __shfl_sync(0xffffffffu, inc, 31);
     const int64_t excl = inc - deg;
-    // four edges per lane and round: the four column loads, then the four
+    // kBfsBatch edges per lane and round: the column loads, then the
     // dist reads, then the CAS of the unvisited ones are each issued together,
-    // so a round costs one chain of dependent L2 round trips instead of four
-    // (cfg2's ~30K-vertex frontiers are ~3 rounds of 32 edges per lane)
-    for (int64_t e0 = 0; e0 < total; e0 += 128) {
-      int32_t v[4];
+    // so a round costs one chain of dependent L2 round trips instead of kBfsBatch
+    // (cfg2: 32 frontier vertices x 7 edges = one round per warp)
+    for (int64_t e0 = 0; e0 < total; e0 += 32 * kBfsBatch) {
+      int32_t v[kBfsBatch];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kBfsBatch; ++j) {
         const int64_t e = e0 + 32 * j + lane;
         const bool act = e < total;
         const int64_t ee = act ? e : total - 1;
@@ -200,15 +201,15 @@ __device__ void bfs_expand(const RP* row_ptr, const int32_t* col, const BfsState
         const int64_t ex_o = __shfl_sync(0xffffffffu, excl, owner);
         v[j] = act ? col[st_o + (ee - ex_o)] : -1;
       }
-      bool push[4];
-bool fresh[4];
+      bool push[kBfsBatch];
+bool fresh[kBfsBatch];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) fresh[j] = v[j] >= 0 && S.dist[v[j]] == -1;
+      for (int j = 0; j < kBfsBatch; ++j) fresh[j] = v[j] >= 0 && S.dist[v[j]] == -1;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) push[j] = fresh[j] && atomicCAS(S.dist + v[j], -1, lev + 1) == -1;
-      uint32_t m[4], cntj[4], tot = 0;
+      for (int j = 0; j < kBfsBatch; ++j) push[j] = fresh[j] && atomicCAS(S.dist + v[j], -1, lev + 1) == -1;
+      uint32_t m[kBfsBatch], cntj[kBfsBatch], tot = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kBfsBatch; ++j) {
         m[j] = __ballot_sync(0xffffffffu, push[j]);
         cntj[j] = tot;
         tot += uint32_t(__popc(m[j]));
@@ -218,7 +219,7 @@ bool fresh[4];
         if (lane == 0) off = atomicAdd(out_size, tot);
         off = __shfl_sync(0xffffffffu, off, 0);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < kBfsBatch; ++j)
           if (push[j]) q_out[off + cntj[j] + __popc(m[j] & ((1u << lane) - 1u))] = v[j];
       }
     }

@@ -297,10 +297,12 @@ static int dp_build(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int3
   LMPK_CHECK_CUDA(cudaMemcpyAsync(wmin.data(), d_wmin, size_t(S) * 4, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   pt.mark("  dp: pattern pass");
-  // ---- tiles: consecutive slices up to the piece cap.  48 KB pieces (cfg5:
-  // ~3.7K rows, 570 tiles, a ring of 2) measured best on cfg5 (2.40 ms per
-  // step; 32 KB and a ring of 4: 2.44, 64 KB: 2.65; tools/cfg5_sweep.py)
-  int64_t cap = 48 * 1024;
+  // ---- tiles: consecutive slices up to the piece cap.  Complex tilings: 48 KB
+  // pieces (cfg5: ~3.7K rows, 570 tiles, a ring of 2) measured best (2.40 ms
+  // per Chebyshev step; 32 KB and a ring of 4: 2.44, 64 KB: 2.65;
+  // tools/cfg5_sweep.py).  Real tilings: 32 KB and a ring of 4 (cfg5's matrix,
+  // real MPK k = 8: 0.142 ms against 0.153 at 48 KB; tools/lean_ab.py)
+  int64_t cap = (cplx ? 48 : 32) * 1024;
   if (const char* e = getenv("LMPK_DP_TILE_KB")) cap = std::max(4, std::min(100, atoi(e))) * int64_t(1024);
   std::vector<int32_t> first;
   {
