@@ -51,12 +51,19 @@ __global__ void k_heavy_rows(const int32_t* __restrict__ row_ptr, int32_t r0, in
 // longest row's add chain is the critical path of the sweep): rank sort of the
 // na huge rows by (length descending, row ascending) by one CTA, through the
 // free slots between the two ends of the list.
-__global__ void __launch_bounds__(1024) k_sort_huge(const int32_t* __restrict__ row_ptr, int32_t* list, int32_t na) {
+// n_cta receives the number of rows longer than kCtaRow: only those take the
+// CTA path (its one adding thread per CTA is the fastest chain, but an SM
+// holds three such CTAs against 24 warp-per-row chains); the other huge rows
+// stay at the front of the list, so their warps start first.
+constexpr int kCtaRow = 16384;
+__global__ void __launch_bounds__(1024) k_sort_huge(const int32_t* __restrict__ row_ptr, int32_t* list, int32_t na,
+                                                    int32_t* n_cta) {
   int32_t* rows = list + 2;
   int32_t* tmp = rows + na;
   for (int32_t i = threadIdx.x; i < na; i += blockDim.x) {
     const int32_t r = rows[i];
     const int32_t len = __ldg(row_ptr + r + 1) - __ldg(row_ptr + r);
+    if (len > kCtaRow) atomicAdd(n_cta, 1);
     int32_t rank = 0;
     for (int32_t j = 0; j < na; ++j) {
       const int32_t q = rows[j];
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(256) spmv_rows_heavy_kernel(const int32_t* __r
     double(*buf)[2][kHStage] = reinterpret_cast<double(*)[2][kHStage]>(smem_d);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t na = __ldg(list), nb = __ldg(list + 1);
-    const int32_t i = na + (int32_t(blockIdx.x) - ha) * 8 + warp;
+    const int32_t i = ha + (int32_t(blockIdx.x) - ha) * 8 + warp;  // ha <= na: the longest rows took CTAs
     if (i >= na + nb) return;
     const int32_t r = i < na ? __ldg(list + 2 + i) : __ldg(list + 2 + (r1 - r0) - 1 - (i - na));
     const int32_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(256) sweep_rows_kernel(const int32_t* __restri
     double(*buf)[2][kHW] = reinterpret_cast<double(*)[2][kHW]>(smem_d);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t na = __ldg(list), nb = __ldg(list + 1);
-    const int32_t i = na + (int32_t(blockIdx.x) - ha) * 8 + warp;
+    const int32_t i = ha + (int32_t(blockIdx.x) - ha) * 8 + warp;  // ha <= na: the longest rows took CTAs
     if (i >= na + nb) return;
     const int32_t r = i < na ? __ldg(list + 2 + i) : __ldg(list + 2 + n - 1 - (i - na));
     const int32_t a = __ldg(row_ptr + r), b = __ldg(row_ptr + r + 1);
@@ -484,7 +491,7 @@ static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t
   // the list is shared ctx scratch: a call on another stream may still be
   // reading it -- order this call (and any reallocation) after that reader
   if (!ctx->heavy_ev) LMPK_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->heavy_ev, cudaEventDisableTiming));
-  const size_t list_bytes = (size_t(r1 - r0) + 2) * 4;
+  const size_t list_bytes = (size_t(r1 - r0) + 3) * 4;  // two counts, cap slots, the CTA-path count
   if (ctx->s_heavy.bytes < list_bytes) LMPK_CHECK_CUDA(cudaEventSynchronize(ctx->heavy_ev));
   LMPK_CHECK_CUDA(cudaStreamWaitEvent(st, ctx->heavy_ev, 0));
   LMPK_TRY(ctx->s_heavy.ensure(list_bytes));
@@ -498,12 +505,18 @@ static int heavy_list(lmpk_ctx* ctx, const int32_t* row_ptr, int32_t r0, int32_t
   int32_t head[2] = {0, 0};
   LMPK_CHECK_CUDA(cudaMemcpyAsync(head, list, 8, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));  // once per call: decides the heavy-row launch
-  *n_huge = head[0];
+  *n_huge = head[0];  // rows on the CTA path: every huge row unless the sort below narrows it
   *n_heavy = head[0] + head[1];
-  if (head[0] > 1 && int64_t(r1 - r0) - head[0] - head[1] >= head[0]) {
-    k_sort_huge<<<1, 1024, 0, st>>>(row_ptr, list, head[0]);
+  if (head[0] > 0 && int64_t(r1 - r0) - head[0] - head[1] >= head[0]) {
+    int32_t* d_cta = list + 2 + (r1 - r0);  // one slot behind the cap
+    LMPK_CHECK_CUDA(cudaMemsetAsync(d_cta, 0, 4, st));
+    k_sort_huge<<<1, 1024, 0, st>>>(row_ptr, list, head[0], d_cta);
     LMPK_CHECK_CUDA(cudaGetLastError());
     launch_count_add(ctx, 1);
+    int32_t h_cta = 0;
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(&h_cta, d_cta, 4, cudaMemcpyDeviceToHost, st));
+    LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
+    *n_huge = h_cta;
   }
   *out = list;
   return LMPK_OK;
