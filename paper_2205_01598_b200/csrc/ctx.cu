@@ -115,6 +115,16 @@ extern "C" int lmpk_ctx_create(lmpk_ctx** out, int device) {
     }
   }
   if (e == cudaSuccess) e = cudaMalloc(&c->queue_ctr, 64);
+  if (e == cudaSuccess) {
+    // planning temporaries come from the device's default stream-ordered pool
+    // (tmp_alloc): keep freed blocks cached instead of returning them at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   if (e == cudaSuccess && getenv("LMPK_PROFILE") != nullptr) {
     // 16 phase counters + (LMPK_TRACE) an event trace of CTAs 0 and 1
     const size_t words = 16 + (getenv("LMPK_TRACE") ? size_t(kTraceCtas) * kTraceEvents * 2 : 0);

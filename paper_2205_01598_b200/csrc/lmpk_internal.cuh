@@ -512,6 +512,26 @@ __device__ __forceinline__ double2 row_sum_exact_c(const int32_t* c, const doubl
   return make_double2(tr, ti);
 }
 
+// ------------------------------------------------------------------ planning temporaries
+// Stream-ordered scratch of the tiling / planning code (cudaMallocAsync on
+// the call's stream; the ctx raises the default pool's release threshold so
+// the blocks are reused): a cudaFree synchronises the device, and a tiling
+// used to pay ~25 of them.
+template <typename T>
+static inline int tmp_alloc(T** p, size_t count, cudaStream_t st) {
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), (count > 0 ? count : 1) * sizeof(T), st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    ::lmpk::set_error("cudaMallocAsync(%zu) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+    *p = nullptr;
+    return LMPK_ERR_NOMEM;
+  }
+  return LMPK_OK;
+}
+static inline void tmp_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
 // ------------------------------------------------------------------ host helpers
 int launch_count_add(lmpk_ctx* ctx, int n);
 static inline int div_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

@@ -683,10 +683,10 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
     std::vector<int32_t> nd(nl, -1);
     if (nl > 0) {
       int32_t *d_row1 = nullptr, *d_list = nullptr, *d_nd = nullptr;
-      LMPK_TRY(dmalloc(&d_row1, n1 + 1));
-      LMPK_TRY(dmalloc(&d_list, nl));
-      LMPK_TRY(dmalloc(&d_nd, nl));
-      LMPK_TRY(dmalloc(&d_dict_tab, size_t(nl) * kDictMax));
+      LMPK_TRY(tmp_alloc(&d_row1, n1 + 1, st));
+      LMPK_TRY(tmp_alloc(&d_list, nl, st));
+      LMPK_TRY(tmp_alloc(&d_nd, nl, st));
+      LMPK_TRY(tmp_alloc(&d_dict_tab, size_t(nl) * kDictMax, st));
       LMPK_CHECK_CUDA(cudaMemcpyAsync(d_row1, row1.data(), size_t(n1 + 1) * 4, cudaMemcpyHostToDevice, st));
       LMPK_CHECK_CUDA(cudaMemcpyAsync(d_list, list.data(), size_t(nl) * 4, cudaMemcpyHostToDevice, st));
       k_tile_dict<<<nl, 256, 0, st>>>(row_ptr, val, d_row1, d_list, nl, d_dict_tab, d_nd);
@@ -694,9 +694,9 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
       LMPK_CHECK_CUDA(cudaGetLastError());
       LMPK_CHECK_CUDA(cudaMemcpyAsync(nd.data(), d_nd, size_t(nl) * 4, cudaMemcpyDeviceToHost, st));
       LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-      cudaFree(d_row1);
-      cudaFree(d_list);
-      cudaFree(d_nd);
+      tmp_free(d_row1, st);
+      tmp_free(d_list, st);
+      tmp_free(d_nd, st);
     }
     pt.mark("tile dictionaries");
     // pass 2: final tiles
@@ -793,7 +793,7 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   T->info.dict_tiles = n_dict;
   if (n_comp > 0) {
     LMPK_TRY(dmalloc(&T->d_tile_mode, nt));
-    LMPK_TRY(dmalloc(&d_tile_dict, nt));
+    LMPK_TRY(tmp_alloc(&d_tile_dict, nt, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_mode, tmode.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_tile_dict, tdict.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
   }
@@ -808,9 +808,9 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   LMPK_TRY(dmalloc(&T->d_progress, nt));
   LMPK_TRY(dmalloc(&T->d_blocks, size_t(std::max<int64_t>(ofs, 128))));
   int32_t *d_slice_tile = nullptr, *d_slice_off = nullptr, *d_width = nullptr;
-  LMPK_TRY(dmalloc(&d_slice_tile, std::max(S, 1)));
-  LMPK_TRY(dmalloc(&d_slice_off, std::max(S, 1)));
-  LMPK_TRY(dmalloc(&d_width, std::max(S, 1)));
+  LMPK_TRY(tmp_alloc(&d_slice_tile, std::max(S, 1), st));
+  LMPK_TRY(tmp_alloc(&d_slice_off, std::max(S, 1), st));
+  LMPK_TRY(tmp_alloc(&d_width, std::max(S, 1), st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_row, tile_row.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_ofs, tile_ofs.data(), (nt + 1) * 8, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->d_tile_E, tile_E.data(), nt * 4, cudaMemcpyHostToDevice, st));
@@ -832,8 +832,8 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   int32_t* d_seg_ptr = nullptr;
   int4* d_segs = nullptr;
   if (!segs.empty()) {
-    LMPK_TRY(dmalloc(&d_seg_ptr, nt + 1));
-    LMPK_TRY(dmalloc(&d_segs, segs.size()));
+    LMPK_TRY(tmp_alloc(&d_seg_ptr, nt + 1, st));
+    LMPK_TRY(tmp_alloc(&d_segs, segs.size(), st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_seg_ptr, seg_ptr.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * 16, cudaMemcpyHostToDevice, st));
   }
@@ -867,13 +867,13 @@ static int build_tiling(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t*
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->h_dep_lo.data(), T->d_dep_lo, nt * 4, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(T->h_dep_hi.data(), T->d_dep_hi, nt * 4, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d_slice_tile);
-  cudaFree(d_slice_off);
-  cudaFree(d_width);
-  cudaFree(d_seg_ptr);
-  cudaFree(d_segs);
-  cudaFree(d_tile_dict);
-  cudaFree(d_dict_tab);
+  tmp_free(d_slice_tile, st);
+  tmp_free(d_slice_off, st);
+  tmp_free(d_width, st);
+  tmp_free(d_seg_ptr, st);
+  tmp_free(d_segs, st);
+  tmp_free(d_tile_dict, st);
+  tmp_free(d_dict_tab, st);
   T->info.n_tiles = nt;
   T->info.block_bytes = ofs;
   pt.mark("geometry D2H + frees");
@@ -1003,18 +1003,19 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
   int32_t* d_w = nullptr;
   int32_t* d_wmin = nullptr;
   uint8_t* d_fit = nullptr;
-  LMPK_TRY(dmalloc(&d_w, std::max(S, 1)));
-  LMPK_TRY(dmalloc(&d_wmin, std::max(S, 1)));
-  LMPK_TRY(dmalloc(&d_fit, std::max(S, 1)));
+  LMPK_TRY(tmp_alloc(&d_w, std::max(S, 1), st));
+  LMPK_TRY(tmp_alloc(&d_wmin, std::max(S, 1), st));
+  LMPK_TRY(tmp_alloc(&d_fit, std::max(S, 1), st));
   struct Guard {
     int32_t *a, *b;
     uint8_t* c;
+    cudaStream_t s;
     ~Guard() {
-      cudaFree(a);
-      cudaFree(b);
-      cudaFree(c);
+      tmp_free(a, s);
+      tmp_free(b, s);
+      tmp_free(c, s);
     }
-  } guard{d_w, d_wmin, d_fit};
+  } guard{d_w, d_wmin, d_fit, st};
   // compressed blocks (int16 column offsets + value dictionary): opt-in via
   // LMPK_FLAG_COMPRESS or LMPK_COMPRESS=1; not with unstaged blocks or x staging
   bool compress = (prm.mode_flags & LMPK_FLAG_COMPRESS) != 0 ||

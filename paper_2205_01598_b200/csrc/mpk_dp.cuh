@@ -248,9 +248,9 @@ static int dp_build(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int3
   const int32_t nc = div_up(n, kDpRowsPerCta);
   uint64_t* d_part = nullptr;
   int32_t *d_nd = nullptr, *d_flag = nullptr;
-  LMPK_TRY(dmalloc(&d_part, size_t(nc) * kDictMax));
-  LMPK_TRY(dmalloc(&d_nd, nc));
-  LMPK_TRY(dmalloc(&d_flag, 1));
+  LMPK_TRY(tmp_alloc(&d_part, size_t(nc) * kDictMax, st));
+  LMPK_TRY(tmp_alloc(&d_nd, nc, st));
+  LMPK_TRY(tmp_alloc(&d_flag, 1, st));
   LMPK_CHECK_CUDA(cudaMemsetAsync(d_flag, 0, 4, st));
   k_dp_dict<<<nc, 256, 0, st>>>(row_ptr, col, val, n, d_part, d_nd, d_flag);
   launch_count_add(ctx, 1);
@@ -262,9 +262,9 @@ static int dp_build(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int3
   LMPK_CHECK_CUDA(cudaMemcpyAsync(pnd.data(), d_nd, size_t(nc) * 4, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(&flag, d_flag, 4, cudaMemcpyDeviceToHost, st));
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d_part);
-  cudaFree(d_nd);
-  cudaFree(d_flag);
+  tmp_free(d_part, st);
+  tmp_free(d_nd, st);
+  tmp_free(d_flag, st);
   if (flag) return LMPK_OK;
   std::vector<uint64_t> dict{0ull};  // +0.0, the padding value, is entry 0 (smallest bit pattern)
   for (int32_t c = 0; c < nc; ++c) {
@@ -278,14 +278,16 @@ static int dp_build(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int3
   pt.mark("  dp: dictionary");
   uint64_t* d_dict = nullptr;
   int32_t* d_np = nullptr;
-  LMPK_TRY(dmalloc(&d_dict, 32));
-  LMPK_TRY(dmalloc(&d_np, S));
+  LMPK_TRY(tmp_alloc(&d_dict, 32, st));
+  LMPK_TRY(tmp_alloc(&d_np, S, st));
   struct Guard {
     std::vector<void*> p;
+    cudaStream_t s;
     ~Guard() {
-      for (void* q : p) cudaFree(q);
+      for (void* q : p) tmp_free(q, s);
     }
   } guard;
+  guard.s = st;
   guard.p = {d_dict, d_np};
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_dict, dict.data(), size_t(nd) * 8, cudaMemcpyHostToDevice, st));
   // ---- pass 1: distinct rows per slice
@@ -398,11 +400,11 @@ static int dp_build(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, const int3
       return rc_;                       \
     }                                   \
   } while (0)
-  LMPK_DP_TRY(dmalloc(&d_rec_ptr, nt + 1));
+  LMPK_DP_TRY(tmp_alloc(&d_rec_ptr, nt + 1, st));
   guard.p.push_back(d_rec_ptr);
-  LMPK_DP_TRY(dmalloc(&d_recs, recs.size()));
+  LMPK_DP_TRY(tmp_alloc(&d_recs, recs.size(), st));
   guard.p.push_back(d_recs);
-  LMPK_DP_TRY(dmalloc(&d_desc, desc.size()));
+  LMPK_DP_TRY(tmp_alloc(&d_desc, desc.size(), st));
   guard.p.push_back(d_desc);
   LMPK_DP_TRY(dmalloc(&T->d_tile_row, nt + 1));
   LMPK_DP_TRY(dmalloc(&T->d_tile_E, nt));

@@ -604,9 +604,9 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   }
   int32_t *d_tdict = nullptr, *d_nd = nullptr, *d_np = nullptr;
   LeanSliceDesc* d_desc = nullptr;
-  LMPK_TRY(lmalloc(&d_tdict, nt));
-  LMPK_TRY(lmalloc(&d_nd, nt));
-  LMPK_TRY(lmalloc(&d_desc, S));
+  LMPK_TRY(tmp_alloc(&d_tdict, nt, st));
+  LMPK_TRY(tmp_alloc(&d_nd, nt, st));
+  LMPK_TRY(tmp_alloc(&d_desc, S, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_tdict, tdict.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_nd, nd.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
   const int ctas = xs ? lean_xs_ctas() : 1;
@@ -628,9 +628,9 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   if (vd == 1 && !any_plain && getenv("LMPK_NO_XP") == nullptr && (xs || (getenv("LMPK_XP") && atoi(getenv("LMPK_XP"))))) {
     int32_t *d_stile = nullptr, *d_tfirst = nullptr;
     int2* d_scan = nullptr;
-    LMPK_TRY(lmalloc(&d_stile, S));
-    LMPK_TRY(lmalloc(&d_tfirst, nt));
-    LMPK_TRY(lmalloc(&d_scan, S));
+    LMPK_TRY(tmp_alloc(&d_stile, S, st));
+    LMPK_TRY(tmp_alloc(&d_tfirst, nt, st));
+    LMPK_TRY(tmp_alloc(&d_scan, S, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_stile, slice_tile.data(), size_t(S) * 4, cudaMemcpyHostToDevice, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_tfirst, first.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
     k_xp_scan<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_stile, d_tfirst, d_width,
@@ -640,9 +640,9 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
     std::vector<int2> scan(S);
     LMPK_CHECK_CUDA(cudaMemcpyAsync(scan.data(), d_scan, size_t(S) * sizeof(int2), cudaMemcpyDeviceToHost, st));
     LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_stile);
-    cudaFree(d_tfirst);
-    cudaFree(d_scan);
+    tmp_free(d_stile, st);
+    tmp_free(d_tfirst, st);
+    tmp_free(d_scan, st);
     int run_max = 4;
     if (const char* e = getenv("LMPK_XP_RUN")) run_max = std::max(1, std::min(8, atoi(e)));
     // staged: the block shares a piece with the x buffer; unstaged: 4 pieces
@@ -739,9 +739,9 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   if (try_pat) {
     int32_t* d_st = nullptr;
     uint64_t* d_sig = nullptr;
-    LMPK_TRY(lmalloc(&d_np, S));
-    LMPK_TRY(lmalloc(&d_st, S));
-    LMPK_TRY(lmalloc(&d_sig, S));
+    LMPK_TRY(tmp_alloc(&d_np, S, st));
+    LMPK_TRY(tmp_alloc(&d_st, S, st));
+    LMPK_TRY(tmp_alloc(&d_sig, S, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_st, slice_tile.data(), size_t(S) * 4, cudaMemcpyHostToDevice, st));
     k_lean_patterns<<<div_up(int64_t(S) * 32, 256), 256, 0, st>>>(row_ptr, col, val, S, d_st, d_width,
                                                                   T->d_tile_row, d_tdict, d_nd, d_dict_tab, d_np, d_sig,
@@ -750,8 +750,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
     LMPK_CHECK_CUDA(cudaMemcpyAsync(np.data(), d_np, size_t(S) * 4, cudaMemcpyDeviceToHost, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(sig.data(), d_sig, size_t(S) * 8, cudaMemcpyDeviceToHost, st));
     LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_st);
-    cudaFree(d_sig);
+    tmp_free(d_st, st);
+    tmp_free(d_sig, st);
   }
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
   pt.mark("  lean: plan + pattern pass");
@@ -863,8 +863,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   LMPK_TRY(lmalloc(&d_ofs, nt + 1));
   LMPK_TRY(lmalloc(&d_lean, size_t(total)));
   LMPK_TRY(lmalloc(&d_rowlen, size_t(std::max(n, 1))));
-  LMPK_TRY(lmalloc(&d_rec_ptr, nt + 1));
-  LMPK_TRY(lmalloc(&d_recs, recs.size()));
+  LMPK_TRY(tmp_alloc(&d_rec_ptr, nt + 1, st));
+  LMPK_TRY(tmp_alloc(&d_recs, recs.size(), st));
   LMPK_CHECK_CUDA(cudaMemsetAsync(d_lean, 0, size_t(total), st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_ofs, ofs.data(), size_t(nt + 1) * 8, cudaMemcpyHostToDevice, st));
   LMPK_CHECK_CUDA(cudaMemcpyAsync(d_rec_ptr, rec_ptr.data(), size_t(nt + 1) * 4, cudaMemcpyHostToDevice, st));
@@ -888,10 +888,10 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   uint16_t* d_bins = nullptr;
   int32_t* d_bin_ptr = nullptr;
   if (any_xp) {
-    LMPK_TRY(lmalloc(&d_xrec_ptr, nt + 1));
-    LMPK_TRY(lmalloc(&d_xrecs, xp_recs.size()));
-    LMPK_TRY(lmalloc(&d_udesc, xp_desc.size()));
-    LMPK_TRY(lmalloc(&d_take, nt));
+    LMPK_TRY(tmp_alloc(&d_xrec_ptr, nt + 1, st));
+    LMPK_TRY(tmp_alloc(&d_xrecs, xp_recs.size(), st));
+    LMPK_TRY(tmp_alloc(&d_udesc, xp_desc.size(), st));
+    LMPK_TRY(tmp_alloc(&d_take, nt, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_xrec_ptr, xp_rec_ptr.data(), size_t(nt + 1) * 4, cudaMemcpyHostToDevice, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_xrecs, xp_recs.data(), xp_recs.size() * 16, cudaMemcpyHostToDevice, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_udesc, xp_desc.data(), xp_desc.size() * sizeof(XpUnitDesc),
@@ -902,8 +902,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
       k_xp_fill<<<div_up(int64_t(nxu) * 32, 256), 256, 0, st>>>(row_ptr, col, val, nxu, d_udesc, d_width,
                                                               T->d_tile_row, d_ofs, d_tdict, d_nd, d_dict_tab,
                                                               d_runs, d_xinfo, cplx ? 16 : 8, d_lean);
-    LMPK_TRY(lmalloc(&d_bins, xp_bins.size()));
-    LMPK_TRY(lmalloc(&d_bin_ptr, nt));
+    LMPK_TRY(tmp_alloc(&d_bins, xp_bins.size(), st));
+    LMPK_TRY(tmp_alloc(&d_bin_ptr, nt, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_bins, xp_bins.data(), xp_bins.size() * 2, cudaMemcpyHostToDevice, st));
     LMPK_CHECK_CUDA(cudaMemcpyAsync(d_bin_ptr, xp_bin_ptr.data(), size_t(nt) * 4, cudaMemcpyHostToDevice, st));
     k_xp_head<<<div_up(int64_t(nt) * 32, 256), 256, 0, st>>>(nt, T->d_tile_row, d_ofs, d_xrec_ptr, d_xrecs, d_take,
@@ -912,18 +912,18 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
     LMPK_CHECK_CUDA(cudaGetLastError());
   }
   LMPK_CHECK_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d_xrec_ptr);
-  cudaFree(d_xrecs);
-  cudaFree(d_udesc);
-  cudaFree(d_take);
-  cudaFree(d_bins);
-  cudaFree(d_bin_ptr);
-  cudaFree(d_rec_ptr);
-  cudaFree(d_recs);
-  cudaFree(d_desc);
-  cudaFree(d_tdict);
-  cudaFree(d_nd);
-  cudaFree(d_np);
+  tmp_free(d_xrec_ptr, st);
+  tmp_free(d_xrecs, st);
+  tmp_free(d_udesc, st);
+  tmp_free(d_take, st);
+  tmp_free(d_bins, st);
+  tmp_free(d_bin_ptr, st);
+  tmp_free(d_rec_ptr, st);
+  tmp_free(d_recs, st);
+  tmp_free(d_desc, st);
+  tmp_free(d_tdict, st);
+  tmp_free(d_nd, st);
+  tmp_free(d_np, st);
   pt.mark("  lean: alloc + fill + frees");
   T->d_lean = d_lean;
   T->d_lean_ofs = d_ofs;
