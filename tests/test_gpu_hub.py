@@ -113,3 +113,39 @@ def test_hub_crs_run_cheb_bitwise(hub_matrix, cplx):
         K.mpk_crs_run(b.device(), y, cfg, acc=acc, use_acc=True)
         ref = O.cheb_batches(b.row_ptr, b.col, b.val, x, cr)
     assert np.array_equal(acc.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("lo,hi", [(20, 31), (10, 128), (90, 128)])
+def test_stream_rows_bitwise(lo, hi):
+    """Medium rows without hubs (10..128 entries, empty rows in between): the
+    row-per-thread kernel on full and partial row ranges and as k x SpMV."""
+    import torch
+
+    n = 20_011
+    rng = np.random.default_rng(lo * 1000 + hi)
+    lens = rng.integers(lo, hi + 1, n)
+    lens[::97] = 0  # empty rows
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.concatenate([np.sort(rng.choice(n, int(k), replace=False)) for k in lens if k]).astype(np.int32)
+    val = rng.standard_normal(col.size) * 10.0 ** rng.integers(-5, 3, col.size)
+    a = lm.CsrMatrix(n, rp.astype(np.int32), col, val)
+    x = rng.uniform(-1, 1, n)
+    ref = O.spmv(a.row_ptr, a.col, a.val, x)
+    d = a.device()
+    xd = torch.from_numpy(x).cuda()
+    out = torch.zeros(n, dtype=torch.float64, device="cuda")
+    K.spmv_rows(d, xd, out, 0, n)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    out.zero_()
+    K.spmv_rows(d, xd, out, 77, 19_001)
+    got = out.cpu().numpy()
+    assert np.array_equal(got[77:19_001], ref[77:19_001]) and not got[:77].any() and not got[19_001:].any()
+    k = 3
+    s = 1.0 / np.abs(val).max() / hi
+    b = lm.CsrMatrix(n, a.row_ptr, a.col, a.val * s)
+    refp = O.mpk_powers(b.row_ptr, b.col, b.val, x, k)
+    y = torch.zeros((k + 1, n), dtype=torch.float64, device="cuda")
+    y[0] = xd
+    K.mpk_baseline(b.device(), y, k)
+    assert np.array_equal(y.cpu().numpy(), refp)
