@@ -1147,8 +1147,9 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
     }
   }
   // DP tiling (mpk_dp.cuh): rows of <= 8 entries whose values defeat the
-  // per-tile dictionaries but whose off-diagonal values come from one small
-  // global dictionary (stencil + potential: cfg5's Anderson operator)
+  // per-tile dictionaries -- or whose column offsets defeat int16 -- but whose
+  // off-diagonal values come from one small global dictionary (stencil +
+  // potential: cfg5's Anderson operator; constant stencils on periodic grids)
   if (default_plan && ring && compress && !xstage && !unstaged && xs_slices == 0 && n > 0 && prm.slots == 0 &&
       prm.tile_nnz_hint == 0 && max_row >= 1 && max_row <= 8) {
     bool dictish = false;
@@ -1160,7 +1161,12 @@ extern "C" int lmpk_tiling_create(lmpk_ctx* ctx, int32_t n, const int32_t* row_p
       std::sort(bits.begin(), bits.end());
       dictish = std::unique(bits.begin(), bits.end()) - bits.begin() <= kDictMax;
     }
-    if (dp_wanted(max_row, dictish)) {
+    // a value set that fits the per-tile dictionaries keeps the lean blocks --
+    // unless some slice's column offsets exceed int16 (periodic grids: those
+    // tiles would stay plain and the tiling would lose its lean blocks)
+    bool any_unfit = false;
+    for (uint8_t f : fit16) any_unfit = any_unfit || f == 0;
+    if (dp_wanted(max_row, dictish && !any_unfit)) {
       lmpk_tiling* D = nullptr;
       LMPK_TRY(dp_build(ctx, n, row_ptr, col, val, width, d_w, d_wmin, cplx_t, st, &D));
       if (D) {

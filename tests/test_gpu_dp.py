@@ -228,3 +228,28 @@ def test_dp_torture_repeated_runs():
         K.mpk_run(t, y, cfg, exact=True, check_errors=(rep % 50 == 49))
         if rep % 10 == 9:
             assert torch.equal(y, ref), rep
+
+
+def test_dp_periodic_constant_stencil():
+    """A constant 7-point stencil on a periodic 112^3 grid: its values fit one
+    dictionary, but the level-ordered column offsets exceed int16 (a level's
+    neighbours lie up to two level widths away), which used to leave the
+    tiling without lean blocks; it now takes DP blocks.  Bitwise against the
+    CRS k x SpMV on the same GPU (itself pinned to the oracle elsewhere)."""
+    import torch
+
+    offs = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
+    a = lm.grid_operator((112, 112, 112), [(o, -1.0) for o in offs], periodic=True, diagonal=np.full(112**3, 6.0))
+    ap = _level_ordered(a)
+    k = 6
+    t = K.Tiling(ap.device(), k)
+    assert t.info["dp_tiles"] == t.info["n_tiles"] > 0  # a level holds ~19.6K rows: offsets up to +-39K
+    x = torch.from_numpy(np.random.default_rng(6).uniform(-1, 1, ap.n_rows)).cuda()
+    y = torch.zeros((k + 1, ap.n_rows), dtype=torch.float64, device="cuda")
+    y[0] = x
+    K.mpk_run(t, y, K.mpk_power_cfg(k), exact=True)
+    yb = torch.zeros_like(y)
+    yb[0] = x
+    K.mpk_baseline(ap.device(), yb, k)
+    assert torch.equal(y, yb)
+    print("periodic 112^3:", {kk: t.info[kk] for kk in ("n_tiles", "dp_tiles", "lean_bytes", "block_bytes")})
