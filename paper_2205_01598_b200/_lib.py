@@ -221,10 +221,17 @@ def context(device=None) -> Context:
 
 
 def stream_handle(stream=None):
+    """cudaStream_t of `stream` (default: torch's current stream of the current
+    device).  The raw-stream query costs ~0.3 us against ~7 us for building a
+    torch.cuda.Stream object -- five of these were 15% of a cfg1 run_plan call."""
     import torch
 
-    s = torch.cuda.current_stream() if stream is None else stream
-    return _vp(s.cuda_stream)
+    if stream is None:
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return _vp(raw(torch.cuda.current_device()))
+        stream = torch.cuda.current_stream()
+    return _vp(stream.cuda_stream)
 
 
 def ptr(t):
