@@ -159,10 +159,6 @@ def _schedule(plan: ExecPlan, til, yv, cfg, av, use_acc, cplx, flags):
         times[name] = best
     del ys, as_
     choice = min(times, key=times.get)
-    # a tie goes to the CRS sweeps (no tile blocks to keep resident, and the
-    # choice does not flip from run to run): a tiled schedule must win by 3%
-    if "crs" in times and choice != "crs" and times[choice] > 0.97 * times["crs"]:
-        choice = "crs"
     plan.set_schedule_choice(cplx, choice, plain)
     return choice
 
