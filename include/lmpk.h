@@ -72,6 +72,11 @@ extern "C" {
                                     /* runs of tiles, tile_nnz_hint = run nnz,  */
                                     /* slots = ring depth <= 16)                */
 #define LMPK_FLAG_PLAIN 0x8000      /* tiling: default plan on plain blocks      */
+#define LMPK_FLAG_NO_HUB_ROWS 0x10000 /* lmpk_spmv_rows / lmpk_mpk_baseline: the    */
+                                    /* caller knows that no row of the range    */
+                                    /* holds more than 128 entries, so the call */
+                                    /* skips the hub-row scan and its one       */
+                                    /* host synchronisation (fully asynchronous)*/
 #define LMPK_FLAG_COMPRESS 0x2000   /* tiling: compressed tile blocks (int16     */
                                     /* column offsets, per-tile dictionary of   */
                                     /* <= 256 values), bitwise-identical sums   */

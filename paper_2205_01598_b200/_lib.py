@@ -34,6 +34,7 @@ FLAG_SWEEP = 0x80
 FLAG_EXACT = 0x400
 FLAG_READY_QUEUE = 0x1000
 FLAG_COMPRESS = 0x2000
+FLAG_NO_HUB_ROWS = 0x10000
 FLAG_RING = 0x4000
 FLAG_PLAIN = 0x8000
 

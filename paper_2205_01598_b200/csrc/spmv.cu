@@ -533,11 +533,13 @@ extern "C" int lmpk_spmv_rows(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr, 
   LMPK_ARG_CHECK(n >= 0 && 0 <= r0 && r0 <= r1 && r1 <= n,
                  "row range [%d, %d) out of bounds for n=%d", r0, r1, n);
   LMPK_ARG_CHECK(x != out, "in_vec and out_vec must not alias");
-  (void)flags;
   if (r1 == r0) return LMPK_OK;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
   int32_t n_heavy = 0, n_huge = 0;
+  if (flags & LMPK_FLAG_NO_HUB_ROWS) {  // no scan, no sync, no shared scratch
+    return spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, nullptr, 0, 0, st);
+  }
   LMPK_TRY(heavy_list(ctx, row_ptr, r0, r1, &heavy, &n_huge, &n_heavy, st));
   LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, x, out, r0, r1, heavy, n_huge, n_heavy, st));
   LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
@@ -551,10 +553,15 @@ extern "C" int lmpk_mpk_baseline(lmpk_ctx* ctx, int32_t n, const int32_t* row_pt
   LMPK_ARG_CHECK(p_m >= 1, "p_m must be >= 1");
   LMPK_ARG_CHECK(ldy >= n, "ldy (%lld) must be >= n (%d)", (long long)ldy, n);
   if (n == 0) return LMPK_OK;
-  (void)flags;
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
   int32_t n_heavy = 0, n_huge = 0;
+  if (flags & LMPK_FLAG_NO_HUB_ROWS) {
+    for (int32_t p = 1; p <= p_m; ++p)
+      LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, nullptr, 0,
+                           0, st));
+    return LMPK_OK;
+  }
   LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_huge, &n_heavy, st));
   for (int32_t p = 1; p <= p_m; ++p)
     LMPK_TRY(spmv_launch(ctx, row_ptr, col, val, y + int64_t(p - 1) * ldy, y + int64_t(p) * ldy, 0, n, heavy,

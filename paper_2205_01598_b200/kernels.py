@@ -36,6 +36,17 @@ class DeviceCsr:
     def nnz(self) -> int:
         return int(self.col.shape[0])
 
+    def hub_flag(self) -> int:
+        """FLAG_NO_HUB_ROWS when no row holds more than 128 entries (one device
+        reduction, cached): the CRS sweeps then skip their per-call hub-row scan
+        and its host synchronisation."""
+        f = getattr(self, "_hub_flag", None)
+        if f is None:
+            mx = int((self.row_ptr[1:] - self.row_ptr[:-1]).max().item()) if self.n > 0 else 0
+            f = _lib.FLAG_NO_HUB_ROWS if mx <= 128 else 0
+            self._hub_flag = f
+        return f
+
     @classmethod
     def from_host(cls, row_ptr, col, val, device=None):
         torch = _torch()
@@ -53,7 +64,7 @@ def spmv_rows(a: DeviceCsr, x, out, r0, r1, flags=0, stream=None):
     """out[r] = sum val*x[col] for r in [r0, r1) (csr.py:195-201 bitwise)."""
     ctx = context()
     check(ctx.lib.lmpk_spmv_rows(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
-                                 ptr(x), ptr(out), int(r0), int(r1), int(flags),
+                                 ptr(x), ptr(out), int(r0), int(r1), int(flags) | a.hub_flag(),
                                  stream_handle(stream)), "spmv_rows")
 
 
@@ -61,7 +72,7 @@ def mpk_baseline(a: DeviceCsr, y, p_m, flags=0, stream=None):
     """p_m back-to-back SpMV sweeps on the slots of y (shape [>=p_m+1, n])."""
     ctx = context()
     check(ctx.lib.lmpk_mpk_baseline(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val),
-                                    ptr(y), int(y.stride(0)), int(p_m), int(flags),
+                                    ptr(y), int(y.stride(0)), int(p_m), int(flags) | a.hub_flag(),
                                     stream_handle(stream)), "mpk_baseline")
 
 
