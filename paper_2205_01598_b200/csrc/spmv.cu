@@ -586,7 +586,8 @@ extern "C" int lmpk_mpk_crs_run(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr
   cudaStream_t st = as_stream(stream);
   int32_t* heavy = nullptr;
   int32_t n_heavy = 0, n_huge = 0;
-  LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_huge, &n_heavy, st));
+  const bool no_hubs = (flags & LMPK_FLAG_NO_HUB_ROWS) != 0;
+  if (!no_hubs) LMPK_TRY(heavy_list(ctx, row_ptr, 0, n, &heavy, &n_huge, &n_heavy, st));
   const int threads = 256;
   const int64_t blocks = (int64_t(n) + threads - 1) / threads;
   const int grid = static_cast<int>(std::min<int64_t>(blocks, int64_t(ctx->sm_count) * 8));
@@ -607,6 +608,6 @@ extern "C" int lmpk_mpk_crs_run(lmpk_ctx* ctx, int32_t n, const int32_t* row_ptr
     launch_count_add(ctx, 1);
   }
   LMPK_CHECK_CUDA(cudaGetLastError());
-  LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
+  if (!no_hubs) LMPK_CHECK_CUDA(cudaEventRecord(ctx->heavy_ev, st));
   return LMPK_OK;
 }

@@ -188,7 +188,7 @@ def mpk_crs_run(a: DeviceCsr, y, cfg, acc=None, use_acc=False, complex_state=Fal
     (SpMV / Chebyshev) and accumulation fused (lmpk_mpk_crs_run): the path of
     level-blocked plans on matrices whose rows exceed the tile format."""
     ctx = context()
-    f = (_lib.FLAG_COMPLEX if complex_state else 0) | _lib.FLAG_EXACT
+    f = (_lib.FLAG_COMPLEX if complex_state else 0) | _lib.FLAG_EXACT | a.hub_flag()
     check(ctx.lib.lmpk_mpk_crs_run(ctx.handle, a.n, ptr(a.row_ptr), ptr(a.col), ptr(a.val), ptr(y),
                                    int(y.stride(0)), int(y.shape[0]), ctypes.byref(cfg), ptr(acc),
                                    1 if use_acc else 0, f, stream_handle(stream)), "mpk_crs_run")
