@@ -45,6 +45,9 @@ constexpr int kLeanDict = 16;         // dictionary byte offset in the block
 constexpr int kLeanRec = 16 + 256;    // first unit record
 constexpr uint32_t kLeanPair = 1u << 8, kLeanPadded = 1u << 9, kLeanPattern = 1u << 10;
 constexpr uint32_t kLeanSameVal = 1u << 11;  // pattern pair whose slices share one row of dictionary values
+// same-value pair of two full, unpadded one-pattern slices (the interior of a grid): the unit body
+// with every check resolved at build time (lean_unit's fast path)
+constexpr uint32_t kLeanFast = 1u << 12;
 
 __host__ __device__ constexpr int lean_wc(int w) { return w <= 0 ? 0 : (w <= 4 ? 4 : 8); }
 // bytes of one slice's column offsets / dictionary codes / raw values
@@ -443,6 +446,27 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
   const uint32_t dict = blk + kLeanDict;
   const int32_t s0 = int32_t(rec.w & 0xffffu), s1 = int32_t(rec.w >> 16);
   const int32_t l0 = s0 * 32 + int32_t(lane), l1 = s1 * 32 + int32_t(lane);
+  if constexpr (VD && !CPLX && !XS && W > 0) {
+    // FAST units (kLeanFast, set by lean_build): a pattern pair of two full,
+    // unpadded slices with one pattern each and the same dictionary indices.
+    // No ids, no bounds, no NaN re-check, no per-slice branches: the ~100
+    // instructions of unit set-up around the 95 of the pair itself (cfg2: 69%
+    // of the units) shrink to the address arithmetic.
+    if (rec.z & kLeanFast) {
+      const char* q0 = pt.yin + int64_t(r0 + l0) * 8;
+      const char* q1 = pt.yin + int64_t(r0 + l1) * 8;
+      const uint32_t ca = blk + rec.x + 32u, cb = blk + rec.y + 32u;
+      if constexpr (GEN) {
+        lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l0), true);
+        lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l1), true);
+      }
+      LeanSum<CPLX> a, b;
+      lean_pair<W, CPLX, EXACT, true, false, true>(ca, ca + 2u * uint32_t(lean_wc(W)), cb, 0u, dict, lane, q0, q1, a, b);
+      lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
+      lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l1), b);
+      return;
+    }
+  }
   const bool pat = VD && (rec.z & kLeanPattern) != 0;
   // lanes past the tile (last slice) use the last valid lane's pattern: gather
   // around that row (their sums are discarded)

@@ -735,7 +735,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   // pass 1: pattern counts per slice (natural slice order)
   std::vector<int32_t> np(S, 32);
   std::vector<uint64_t> sig(S, 0);  // dictionary indices of one-pattern slices (same-value pairs)
-  const bool no_sameval = getenv("LMPK_NO_SAMEVAL") != nullptr;  // A/B switch (tools/lean_ab.py)
+  const bool no_sameval = getenv("LMPK_NO_SAMEVAL") != nullptr;  // A/B switches (tools/sameval_ab.py)
+  const bool no_fast = getenv("LMPK_NO_FAST") != nullptr;
   if (try_pat) {
     int32_t* d_st = nullptr;
     uint64_t* d_sig = nullptr;
@@ -844,7 +845,11 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
       if (pat && w > 0) {
         r.z |= kLeanPattern | (uint32_t(np[sa]) << 16) | (uint32_t(pair ? np[sb] : 0) << 24);
         // both slices one pattern with the same dictionary indices: the values are read once
-        if (pair && np[sa] == 1 && np[sb] == 1 && sig[sa] == sig[sb] && !no_sameval) r.z |= kLeanSameVal;
+        if (pair && np[sa] == 1 && np[sb] == 1 && sig[sa] == sig[sb] && !no_sameval) {
+          r.z |= kLeanSameVal;
+          // both slices full (only the matrix's last slice can be partial) and unpadded: fast unit
+          if (!padded && !xs && (int64_t(sa) + 1) * 32 <= n && (int64_t(sb) + 1) * 32 <= n && !no_fast) r.z |= kLeanFast;
+        }
       }
       r.w = uint32_t(sa - s0) | (uint32_t(sb - s0) << 16);
       recs.push_back(r);

@@ -1,4 +1,4 @@
-"""A/B of the same-value pairs of the lean walk on cfg2 (LMPK_NO_SAMEVAL=1 off),
+"""A/B of the fast units / same-value pairs of the lean walk on cfg2 (LMPK_NO_FAST=1, LMPK_NO_SAMEVAL=1),
 alternating tilings on one box; bitwise against the CRS baseline."""
 import os, sys, json, numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,10 +15,11 @@ cfg = K.mpk_power_cfg(k)
 yb = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); yb[0] = x
 K.mpk_baseline(b, yb, k)
 til = {}
-for name, env in (("sameval", None), ("off", "1")):
-    if env: os.environ["LMPK_NO_SAMEVAL"] = env
-    else: os.environ.pop("LMPK_NO_SAMEVAL", None)
+for name, env in (("fast", {}), ("sameval_only", {"LMPK_NO_FAST": "1"}), ("off", {"LMPK_NO_SAMEVAL": "1"})):
+    for kk in ("LMPK_NO_SAMEVAL", "LMPK_NO_FAST"): os.environ.pop(kk, None)
+    os.environ.update(env)
     til[name] = K.Tiling(b, k)
+for kk in ("LMPK_NO_SAMEVAL", "LMPK_NO_FAST"): os.environ.pop(kk, None)
 y = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); y[0] = x
 res = {kk: [] for kk in til}
 for rnd in range(6):
