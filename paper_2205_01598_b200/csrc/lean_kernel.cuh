@@ -455,6 +455,11 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
     if (rec.z & kLeanFast) {
       const char* q0 = pt.yin + int64_t(r0 + l0) * 8;
       const char* q1 = pt.yin + int64_t(r0 + l1) * 8;
+      // two opaque bases: otherwise the compiler derives the second slice's
+      // gather addresses from the first's with 64-bit add pairs instead of
+      // one IMAD.WIDE per gather
+      asm("" : "+l"(q0));
+      asm("" : "+l"(q1));
       const uint32_t ca = blk + rec.x + 32u, cb = blk + rec.y + 32u;
       if constexpr (GEN) {
         lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l0), true);
