@@ -491,6 +491,10 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
       rp1 = xb + uint32_t(pat ? min(int32_t(lane), nrows - 1 - s1 * 32) : int32_t(lane)) * uint32_t(cw);
     else
       rp1 = pt.yin + int64_t(r0 + (pat ? min(l1, nrows - 1) : l1)) * cw;
+    if constexpr (!XS) {  // opaque bases: one IMAD.WIDE per gather (see the fast path)
+      asm("" : "+l"(rp0));
+      asm("" : "+l"(rp1));
+    }
     uint32_t cp1, vp1;
     if (pat) {
       lean_ptrs<W, VD>(blk, rec.y, rec.z >> 24, true, lane, cp1, vp1, 0u);
@@ -652,6 +656,8 @@ __device__ __forceinline__ void dp_unit(uint32_t blk, uint4 rec, uint32_t lane, 
   } else {
     const char* rp0 = pt.yin + int64_t(r0 + min(l0, nrows - 1)) * cw;
     const char* rp1 = pt.yin + int64_t(r0 + min(l1, nrows - 1)) * cw;
+    asm("" : "+l"(rp0));  // opaque bases: one IMAD.WIDE per gather (see lean_unit's fast path)
+    asm("" : "+l"(rp1));
     uint32_t op0, kp0, pd0, op1, kp1, pd1;
     dp_ptrs<W>(blk + rec.x, (rec.z >> 16) & 255u, lane, dict, op0, kp0, pd0);
     dp_ptrs<W>(blk + rec.y, rec.z >> 24, lane, dict, op1, kp1, pd1);
