@@ -612,6 +612,7 @@ __device__ __forceinline__ void dp_single(uint32_t blk, uint32_t sl_off, uint32_
   const int32_t l0 = sidx * 32 + int32_t(lane);
   // lanes past the tile use the last valid lane's pattern: gather around that row
   const char* rp0 = pt.yin + int64_t(r0 + min(l0, nrows - 1)) * cw;
+  asm("" : "+l"(rp0));  // opaque base: one IMAD.WIDE per gather
   uint32_t op0, kp0, pd0;
   dp_ptrs<W>(blk + sl_off, np, lane, dict, op0, kp0, pd0);
   lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l0), l0 < nrows);
