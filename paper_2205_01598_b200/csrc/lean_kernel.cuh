@@ -967,15 +967,24 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
         }
         u = nu;  // the lean loop below is skipped
       }
-      for (; u < nu; u += NC) {
-        const uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);
+      // a warp's units of one piece come width class by width class (the
+      // builder sorts them): a run of units of one width stays inside that
+      // width's compiled body instead of going through the jump table again
+      while (u < nu) {
+        uint4 rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);
         switch (rec.z & 15u) {
 #define LMPK_LEAN_CASE(Wv)                                                                     \
   case Wv:                                                                                     \
-    if constexpr (DP)                                                                          \
-      dp_unit<Wv, CPLX, EXACT, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen);  \
-    else                                                                                       \
-      lean_unit<Wv, CPLX, EXACT, VD, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen); \
+    for (;;) {                                                                                 \
+      if constexpr (DP)                                                                        \
+        dp_unit<Wv, CPLX, EXACT, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen); \
+      else                                                                                     \
+        lean_unit<Wv, CPLX, EXACT, VD, GEN>(blk, rec, lane, r0, nrows, pt, P.acc, use_acc, L.rowlen); \
+      u += NC;                                                                                 \
+      if (u >= nu) break;                                                                      \
+      rec = lds_v4(blk + kLeanRec + uint32_t(u) * 16u);                                        \
+      if ((rec.z & 15u) != uint32_t(Wv)) break;                                                \
+    }                                                                                          \
     break;
           LMPK_LEAN_CASE(0)
           LMPK_LEAN_CASE(1)
@@ -987,7 +996,7 @@ __global__ void __launch_bounds__(32 * (kLeanConsumers + 2), 1)
           LMPK_LEAN_CASE(7)
           LMPK_LEAN_CASE(8)
 #undef LMPK_LEAN_CASE
-          default: break;
+          default: u += NC; break;
         }
       }
       __syncwarp();
