@@ -48,6 +48,9 @@ constexpr uint32_t kLeanSameVal = 1u << 11;  // pattern pair whose slices share 
 // same-value pair of two full, unpadded one-pattern slices (the interior of a grid): the unit body
 // with every check resolved at build time (lean_unit's fast path)
 constexpr uint32_t kLeanFast = 1u << 12;
+// fast unit whose values are row (z >> 13) & 3 of the tile's value table (the free dictionary slots
+// 8 (1 + row) ..: k_lean_vrows)
+constexpr uint32_t kLeanVRow = 1u << 15;
 
 __host__ __device__ constexpr int lean_wc(int w) { return w <= 0 ? 0 : (w <= 4 ? 4 : 8); }
 // bytes of one slice's column offsets / dictionary codes / raw values
@@ -466,7 +469,29 @@ __device__ __forceinline__ void lean_unit(uint32_t blk, uint4 rec, uint32_t lane
         lean_prefetch_epi<CPLX, GEN>(pt, acc, use_acc, int64_t(r0 + l1), true);
       }
       LeanSum<CPLX> a, b;
-      lean_pair<W, CPLX, EXACT, true, false, true>(ca, ca + 2u * uint32_t(lean_wc(W)), cb, 0u, dict, lane, q0, q1, a, b);
+      if (rec.z & kLeanVRow) {
+        // the seven values as broadcast LDS.128 from the tile's value table
+        const uint32_t vr = dict + 64u * (1u + ((rec.z >> 13) & 3u));
+        int32_t c0[W], c1[W];
+        lean_cols<W>(ca, c0);
+        lean_cols<W>(cb, c1);
+        double x0[W], x1[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) x0[j] = lean_gather<false, false>(q0, c0[j]);
+#pragma unroll
+        for (int j = 0; j < W; ++j) x1[j] = lean_gather<false, false>(q1, c1[j]);
+        double v[W];
+#pragma unroll
+        for (int j = 0; j + 1 < W; j += 2) {
+          const double2 d = lds_d2(vr + 8u * uint32_t(j));
+          v[j] = d.x, v[j + 1] = d.y;
+        }
+        if constexpr (W & 1) v[W - 1] = lds_d(vr + 8u * uint32_t(W - 1));
+        a = lean_chain<W, CPLX, EXACT>(v, x0);
+        b = lean_chain<W, CPLX, EXACT>(v, x1);
+      } else {
+        lean_pair<W, CPLX, EXACT, true, false, true>(ca, ca + 2u * uint32_t(lean_wc(W)), cb, 0u, dict, lane, q0, q1, a, b);
+      }
       lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l0), a);
       lean_store_pf<CPLX, EXACT, GEN>(pt, acc, use_acc, int64_t(r0 + l1), b);
       return;

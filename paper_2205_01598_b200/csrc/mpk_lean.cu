@@ -462,6 +462,22 @@ __global__ void k_lean_head(int32_t nt, const int32_t* tile_row, const int64_t* 
   for (int u = lane; u < nu; u += 32) reinterpret_cast<uint4*>(blk + kLeanRec)[u] = recs[u0 + u];
 }
 
+// Value rows of the fast units: a tile whose dictionary holds <= 8 values has
+// 24 free dictionary slots; up to three rows of 8 doubles go there, row r =
+// the values of index signature vsig[3 t + r] (5 bits per entry), so a fast
+// unit reads its seven values as four broadcast LDS.128 instead of a code word
+// and seven dictionary lookups.  One warp per tile, after k_lean_head.
+__global__ void k_lean_vrows(int32_t nt, const int64_t* lean_ofs, const uint64_t* vsig, unsigned char* lean) {
+  const int32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nt || lane >= 24) return;
+  const int r = lane >> 3, j = lane & 7;
+  const uint64_t sg = vsig[int64_t(t) * 3 + r];
+  if (sg == ~0ull) return;
+  uint64_t* dict = reinterpret_cast<uint64_t*>(lean + lean_ofs[t] + kLeanDict);
+  dict[8 * (1 + r) + j] = dict[(sg >> (5 * j)) & 31u];
+}
+
 __global__ void k_rowlen(const int32_t* row_ptr, int32_t n, uint8_t* out) {
   const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < n) out[r] = uint8_t(min(255, row_ptr[r + 1] - row_ptr[r]));
@@ -737,6 +753,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   std::vector<uint64_t> sig(S, 0);  // dictionary indices of one-pattern slices (same-value pairs)
   const bool no_sameval = getenv("LMPK_NO_SAMEVAL") != nullptr;  // A/B switches (tools/sameval_ab.py)
   const bool no_fast = getenv("LMPK_NO_FAST") != nullptr;
+  const bool no_vrow = getenv("LMPK_NO_VROW") != nullptr;
+  std::vector<uint64_t> vsig(size_t(nt) * 3, ~0ull);
   if (try_pat) {
     int32_t* d_st = nullptr;
     uint64_t* d_sig = nullptr;
@@ -832,6 +850,8 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
       }
     }
     rec_ptr[t] = static_cast<int32_t>(recs.size());
+    uint64_t trow[3] = {~0ull, ~0ull, ~0ull};  // value rows of this tile (k_lean_vrows)
+    const bool vrow_ok = pat && nd[t] <= 8 && !no_vrow;
     for (int32_t i = 0; i < ns;) {
       const int32_t sa = order[i];
       const bool pair = pairing && i + 1 < ns && width[order[i + 1]] == width[sa];
@@ -848,13 +868,24 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
         if (pair && np[sa] == 1 && np[sb] == 1 && sig[sa] == sig[sb] && !no_sameval) {
           r.z |= kLeanSameVal;
           // both slices full (only the matrix's last slice can be partial) and unpadded: fast unit
-          if (!padded && !xs && (int64_t(sa) + 1) * 32 <= n && (int64_t(sb) + 1) * 32 <= n && !no_fast) r.z |= kLeanFast;
+          if (!padded && !xs && (int64_t(sa) + 1) * 32 <= n && (int64_t(sb) + 1) * 32 <= n && !no_fast) {
+            r.z |= kLeanFast;
+            if (vrow_ok) {  // the pair's values as a row of the tile's value table
+              int q = 0;
+              while (q < 3 && trow[q] != ~0ull && trow[q] != sig[sa]) ++q;
+              if (q < 3) {
+                trow[q] = sig[sa];
+                r.z |= kLeanVRow | (uint32_t(q) << 13);
+              }
+            }
+          }
         }
       }
       r.w = uint32_t(sa - s0) | (uint32_t(sb - s0) << 16);
       recs.push_back(r);
       i += pair ? 2 : 1;
     }
+    vsig[size_t(t) * 3] = trow[0], vsig[size_t(t) * 3 + 1] = trow[1], vsig[size_t(t) * 3 + 2] = trow[2];
     ofs[t + 1] = ofs[t] + bytes;
   }
   rec_ptr[nt] = static_cast<int32_t>(recs.size());
@@ -884,6 +915,13 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   k_lean_head<<<div_up(int64_t(nt) * 32, 256), 256, 0, st>>>(nt, T->d_tile_row, d_ofs, d_rec_ptr, d_recs, d_tdict,
                                                              d_nd, d_dict_tab, vd, d_lean);
   k_rowlen<<<div_up(std::max(n, 1), 256), 256, 0, st>>>(row_ptr, n, d_rowlen);
+  uint64_t* d_vsig = nullptr;
+  if (vd == 1) {
+    LMPK_TRY(tmp_alloc(&d_vsig, vsig.size(), st));
+    LMPK_CHECK_CUDA(cudaMemcpyAsync(d_vsig, vsig.data(), vsig.size() * 8, cudaMemcpyHostToDevice, st));
+    k_lean_vrows<<<div_up(int64_t(nt) * 32, 256), 256, 0, st>>>(nt, d_ofs, d_vsig, d_lean);
+    launch_count_add(ctx, 1);
+  }
   launch_count_add(ctx, 3);
   LMPK_CHECK_CUDA(cudaGetLastError());
   int32_t* d_xrec_ptr = nullptr;
@@ -923,6 +961,7 @@ int lean_build(lmpk_ctx* ctx, lmpk_tiling* T, int32_t n, const int32_t* row_ptr,
   tmp_free(d_take, st);
   tmp_free(d_bins, st);
   tmp_free(d_bin_ptr, st);
+  tmp_free(d_vsig, st);
   tmp_free(d_rec_ptr, st);
   tmp_free(d_recs, st);
   tmp_free(d_desc, st);

@@ -15,11 +15,11 @@ cfg = K.mpk_power_cfg(k)
 yb = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); yb[0] = x
 K.mpk_baseline(b, yb, k)
 til = {}
-for name, env in (("fast", {}), ("sameval_only", {"LMPK_NO_FAST": "1"}), ("off", {"LMPK_NO_SAMEVAL": "1"})):
-    for kk in ("LMPK_NO_SAMEVAL", "LMPK_NO_FAST"): os.environ.pop(kk, None)
+for name, env in (("fast", {}), ("fast_novrow", {"LMPK_NO_VROW": "1"}), ("sameval_only", {"LMPK_NO_FAST": "1"}), ("off", {"LMPK_NO_SAMEVAL": "1"})):
+    for kk in ("LMPK_NO_SAMEVAL", "LMPK_NO_FAST", "LMPK_NO_VROW"): os.environ.pop(kk, None)
     os.environ.update(env)
     til[name] = K.Tiling(b, k)
-for kk in ("LMPK_NO_SAMEVAL", "LMPK_NO_FAST"): os.environ.pop(kk, None)
+for kk in ("LMPK_NO_SAMEVAL", "LMPK_NO_FAST", "LMPK_NO_VROW"): os.environ.pop(kk, None)
 y = torch.zeros(k + 1, n, dtype=torch.float64, device="cuda"); y[0] = x
 res = {kk: [] for kk in til}
 for rnd in range(6):
